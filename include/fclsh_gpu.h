@@ -1,0 +1,243 @@
+/*
+ * fclsh_gpu.h -- C-ABI of the B200-native fcLSH engine (libfclsh_b200.so).
+ *
+ * Drop-in boundary for the reference library's hot path (arXiv 1602.02620
+ * reference, /root/reference/proj). The reference has no FFI of its own: its
+ * interface is the C++ API listed next to each entry point below. This ABI
+ * restates that API over plain pointers, sizes and opaque handles, batched
+ * (one call hashes / queries many rows) because per-row calls would be
+ * launch-bound on a GPU. No torch or CUDA types appear in the signatures;
+ * streams travel as `void*` (a cudaStream_t, NULL = the library's own).
+ *
+ * Conventions
+ *  - Rows are row-major uint64 words, bit i of a row in word i/64 at offset
+ *    i%64, padding bits zero: exactly BitVector's layout (bitvec.hpp:13-19).
+ *    For d % 64 == 0 an FCL1 file row is byte-identical (dataset.hpp:20-23).
+ *  - An `Rng&` argument of the reference is passed as the Rng's 64-bit seed:
+ *    every consumer on this path derives its draws through Rng::stream(),
+ *    which depends on the seed alone (rng.cpp:31-37).
+ *  - Return codes mirror the reference's exception classes and CLI exit
+ *    codes (errors.hpp:8-29, tools/fclsh.cpp:302-318):
+ *      0 ok, 2 UsageError, 3 DataError, 4 ResourceError,
+ *      5 CUDA runtime failure (no reference counterpart; the reference never
+ *        touches a device), 1 any other failure.
+ *    fclsh_last_error() returns the message of the last failure on the
+ *    calling thread, with the reference's wording where one exists.
+ *  - Device (`d_`) pointers must be device memory on the handle's device.
+ *  - Handles are bound to one device; calls on one handle serialize. Distinct
+ *    handles may be driven from distinct host threads.
+ */
+#ifndef FCLSH_GPU_H
+#define FCLSH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCLSH_OK 0
+#define FCLSH_ERR_OTHER 1
+#define FCLSH_ERR_USAGE 2
+#define FCLSH_ERR_DATA 3
+#define FCLSH_ERR_RESOURCE 4
+#define FCLSH_ERR_CUDA 5
+
+/* ConstructionKind (covering.hpp:21) and PlanKind (transform.hpp:24). */
+#define FCLSH_KIND_AUTO (-1)
+#define FCLSH_KIND_GENERAL 0
+#define FCLSH_KIND_SPECIFIC 1
+#define FCLSH_PLAN_IDENTITY 0
+#define FCLSH_PLAN_REPLICATE 1
+#define FCLSH_PLAN_PARTITION 2
+
+/* Key layouts of fclsh_hash_batch. */
+#define FCLSH_LAYOUT_TABLE_MAJOR 0 /* key[(part*L + v-1)*key_stride + row] */
+#define FCLSH_LAYOUT_POINT_MAJOR 1 /* key[row*key_stride + part*L + v-1]  */
+
+/* kMersenne61 (modmath.hpp:10) and the 32-bit-key field 2^31-1. */
+#define FCLSH_PRIME_M61 ((uint64_t)0x1FFFFFFFFFFFFFFFull)
+#define FCLSH_PRIME_M31 ((uint64_t)0x7FFFFFFFull)
+/* kDefaultTableBudget (transform.hpp:52) */
+#define FCLSH_DEFAULT_TABLE_BUDGET ((uint64_t)1 << 21)
+
+const char* fclsh_version(void);
+const char* fclsh_last_error(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int fclsh_device_count(int* out);
+
+/* ------------------------------------------------------------------ Rng ---
+ * Rng(seed).stream(label) / .stream(label, index) seeds (rng.cpp:31-37). */
+uint64_t fclsh_rng_stream(uint64_t seed, const char* label);
+uint64_t fclsh_rng_stream_index(uint64_t seed, const char* label, uint64_t index);
+
+/* ---------------------------------------------------------------- family ---
+ * An r-covering family over one view (covering.hpp:34-43). */
+typedef struct fclsh_family fclsh_family;
+
+typedef struct {
+    uint64_t dims;
+    uint32_t radius;
+    int32_t kind;    /* FCLSH_KIND_* (never AUTO once built) */
+    uint64_t prime;
+    uint64_t tables; /* 2^(radius+1) - 1 */
+} fclsh_family_info;
+
+/* build_covering_family(dims, radius[, kind], Rng(rng_seed), {prime, include_zero_column})
+ * (covering.hpp:55-60, covering.cpp:40-80). kind = FCLSH_KIND_AUTO derives it
+ * from the widths (covering.cpp:74-80). */
+int fclsh_family_build(uint64_t dims, uint32_t radius, int32_t kind, uint64_t rng_seed,
+                       uint64_t prime, int include_zero_column, fclsh_family** out);
+/* make_covering_family(dims, radius, kind, mapping, seeds, prime)
+ * (covering.hpp:62-66, covering.cpp:84-111): explicit, validated. */
+int fclsh_family_make(uint64_t dims, uint32_t radius, int32_t kind, const uint32_t* mapping,
+                      const uint64_t* seeds, uint64_t prime, fclsh_family** out);
+int fclsh_family_info_get(const fclsh_family* f, fclsh_family_info* out);
+/* Copies mapping[dims] / seeds[dims] out (either may be NULL). */
+int fclsh_family_export(const fclsh_family* f, uint32_t* mapping, uint64_t* seeds);
+void fclsh_family_destroy(fclsh_family* f);
+
+/* hash_batch_into for n rows at once (covering.hpp:83-84, covering.cpp:169-182):
+ * keys of row i, table v (1..L) = h[v]; canonical residues mod prime.
+ * key_bytes: 4 (prime < 2^32) or 8. key_stride in keys (>= n for TABLE_MAJOR,
+ * >= L for POINT_MAJOR). Device buffers; asynchronous on `stream`. */
+int fclsh_hash_batch(const fclsh_family* f, const uint64_t* d_rows, uint64_t n,
+                     uint32_t row_words, void* d_keys, uint32_t key_bytes, uint64_t key_stride,
+                     int32_t layout, int device, void* stream);
+/* Same from host buffers (copies in, hashes, copies out; synchronous).
+ * keys is point-major [n][L]. */
+int fclsh_hash_batch_host(const fclsh_family* f, const uint64_t* rows, uint64_t n,
+                          uint32_t row_words, void* keys, uint32_t key_bytes, int device);
+
+/* ------------------------------------------------------------------ plan ---
+ * PreprocessPlan (transform.hpp:26-44) */
+typedef struct fclsh_plan fclsh_plan;
+
+typedef struct {
+    int32_t kind; /* FCLSH_PLAN_* */
+    uint32_t t;
+} fclsh_plan_override;
+
+typedef struct {
+    int32_t kind;
+    uint64_t dims;
+    uint32_t radius;
+    uint32_t t;
+    uint32_t per_part_radius;
+    uint32_t part_count;
+    uint64_t table_count; /* plan_table_count (transform.cpp:155-158) */
+} fclsh_plan_info;
+
+/* make_plan(dims, radius, c, n, Rng(rng_seed), force, table_budget)
+ * (transform.hpp:57-59, transform.cpp:32-113). force may be NULL. */
+int fclsh_plan_make(uint64_t dims, uint32_t radius, double c, uint64_t n, uint64_t rng_seed,
+                    const fclsh_plan_override* force, uint64_t table_budget, fclsh_plan** out);
+int fclsh_plan_info_get(const fclsh_plan* p, fclsh_plan_info* out);
+/* permutation[dims] and parts[2*t] (begin, end) of a partition plan. */
+int fclsh_plan_export(const fclsh_plan* p, uint32_t* permutation, uint64_t* parts);
+void fclsh_plan_destroy(fclsh_plan* p);
+
+/* ----------------------------------------------------------------- index ---
+ * IndexSet (index.hpp:42-52), built on one device. Owns a device copy of
+ * the rows (needed by the verify pass) and every table. */
+typedef struct fclsh_index fclsh_index;
+
+typedef struct {
+    uint64_t prime;              /* IndexOptions::prime (index.hpp:25) */
+    int32_t include_zero_column; /* IndexOptions::include_zero_column */
+    uint64_t table_budget;       /* IndexOptions::table_budget */
+    int32_t device;              /* CUDA device ordinal */
+    uint64_t id_offset;          /* added to every reported id (shards) */
+    int32_t directory_bits;      /* 0 = automatic */
+} fclsh_index_options;
+
+void fclsh_index_options_default(fclsh_index_options* o);
+
+/* build_index(data, Method::covering_batch, radius, plan, Rng(rng_seed), opt)
+ * (index.hpp:70-71, index.cpp:49-119). rows: n x row_words words, host
+ * memory (rows_on_device = 0) or device memory on opt->device (1). */
+int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint64_t dims,
+                      uint32_t radius, const fclsh_plan* plan, uint64_t rng_seed,
+                      const fclsh_index_options* opt, fclsh_index** out);
+typedef struct {
+    uint64_t n;
+    uint64_t dims;
+    uint32_t radius;
+    uint64_t table_count; /* IndexSet::table_count (index.cpp:20-24) */
+    uint64_t entry_count; /* IndexSet::entry_count (index.cpp:26-31) */
+    uint32_t directory_bits;
+    uint64_t device_bytes;
+    double build_ms; /* device time of the last build, CUDA events */
+} fclsh_index_info;
+int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out);
+/* Part p's family (a new handle the caller destroys). */
+int fclsh_index_family(const fclsh_index* ix, uint32_t part, fclsh_family** out);
+void fclsh_index_destroy(fclsh_index* ix);
+
+/* ----------------------------------------------------------------- query ---
+ * query_r_nn (index.hpp:78-79, index.cpp:157-188) for nq rows at once.
+ * Result triples (query, id, distance) are sorted by (query, id); per-query
+ * QueryReport counters (report.hpp:14-21) equal the reference's exactly. */
+typedef struct {
+    uint64_t nq;
+    uint64_t total;      /* number of triples */
+    uint32_t* query;     /* [total] */
+    uint32_t* id;        /* [total], id_offset applied */
+    uint32_t* distance;  /* [total] */
+    uint64_t* offsets;   /* [nq+1]: query q owns triples [offsets[q], offsets[q+1]) */
+    uint64_t* collisions;/* [nq] */
+    uint64_t* candidates;/* [nq] */
+    uint64_t* found;     /* [nq] */
+    double time_hash_ms, time_probe_ms, time_verify_ms; /* S1 / S2 / S3, CUDA events */
+} fclsh_result;
+
+/* Host rows in, host result out (the library allocates; free with
+ * fclsh_result_free). Synchronous. */
+int fclsh_query(fclsh_index* ix, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
+                fclsh_result** out);
+void fclsh_result_free(fclsh_result* r);
+
+/* Device-resident variant: q rows already on the device, results stay in
+ * index-owned device buffers that live until the next query on `ix`.
+ * Pointers returned are device pointers; *total is read back to the host
+ * (one 8-byte D2H). All work is enqueued on `stream`. */
+typedef struct {
+    uint64_t nq;
+    uint64_t total;
+    uint32_t* d_query;
+    uint32_t* d_id;
+    uint32_t* d_distance;
+    uint64_t* d_offsets;    /* [nq+1] */
+    uint64_t* d_collisions; /* [nq] */
+    uint64_t* d_candidates; /* [nq] */
+    uint64_t* d_found;      /* [nq] */
+} fclsh_device_result;
+int fclsh_query_device(fclsh_index* ix, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
+                       void* stream, fclsh_device_result* out);
+
+/* Number of kernels the library launched on this thread since the last
+ * reset (launch accounting for the bench). */
+uint64_t fclsh_launch_count(void);
+void fclsh_launch_count_reset(void);
+
+/* ------------------------------------------------------------- workloads ---
+ * Seeded synthetic inputs of the BASELINE configs. Host
+ * buffers, multithreaded, counter-based (deterministic for any thread count).
+ *   bernoulli: n rows of d i.i.d. Bernoulli(0.5) bits.
+ *   clustered: centres rows of Bernoulli(0.5) bits; each of n rows copies a
+ *              uniformly drawn centre and flips each bit w.p. flip_p.
+ *   planted:   nq queries, each a uniformly drawn data row with k flipped
+ *              distinct positions, k uniform in [0, kmax]; src_out gets the
+ *              source row id (may be NULL).                                */
+int fclsh_gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
+int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p,
+                        uint64_t* rows, int threads);
+int fclsh_gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq,
+                      uint32_t kmax, uint64_t* qrows, uint32_t* src_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FCLSH_GPU_H */

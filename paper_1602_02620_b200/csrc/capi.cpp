@@ -1,0 +1,403 @@
+// C-ABI of libfclsh_b200.so (include/fclsh_gpu.h). Every entry point maps the
+// reference's exceptions to return codes (errors.hpp:8-29) and records the
+// message for fclsh_last_error().
+
+#include "../../include/fclsh_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "hash.cuh"
+#include "host.hpp"
+#include "index.cuh"
+
+namespace fclsh_b200 {
+void gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
+void gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p, uint64_t* rows,
+                   int threads);
+void gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
+                 uint64_t* qrows, uint32_t* src_out);
+
+uint64_t& launch_counter() {
+    static thread_local uint64_t c = 0;
+    return c;
+}
+} // namespace fclsh_b200
+
+using namespace fclsh_b200;
+
+struct fclsh_family {
+    Family f;
+    std::mutex mu;
+    std::map<int, std::unique_ptr<DeviceFamilySet>> dev;
+    DeviceFamilySet& on(int device) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& slot = dev[device];
+        if (!slot) slot = make_device_family_set(f, device);
+        return *slot;
+    }
+};
+
+struct fclsh_plan {
+    Plan p;
+};
+
+struct fclsh_index {
+    std::unique_ptr<DeviceIndex> ix;
+    DevBuf q_host_rows; // device staging for fclsh_query
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FCLSH_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host memory exhausted";
+        return FCLSH_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FCLSH_ERR_OTHER;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw UsageError(std::string(what) + " must not be NULL");
+}
+
+} // namespace
+
+extern "C" {
+
+const char* fclsh_version(void) { return "fclsh_b200 0.1 (sm_100a)"; }
+const char* fclsh_last_error(void) { return g_err.c_str(); }
+
+int fclsh_device_count(int* out) {
+    return guarded([&] {
+        need(out, "out");
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *out = c;
+    });
+}
+
+uint64_t fclsh_rng_stream(uint64_t seed, const char* label) { return Rng(seed).stream(label ? label : "").seed(); }
+uint64_t fclsh_rng_stream_index(uint64_t seed, const char* label, uint64_t index) {
+    return Rng(seed).stream(label ? label : "", index).seed();
+}
+
+int fclsh_family_build(uint64_t dims, uint32_t radius, int32_t kind, uint64_t rng_seed, uint64_t prime,
+                       int include_zero_column, fclsh_family** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (kind < -1 || kind > 1) throw UsageError("covering family: unknown construction kind");
+        auto h = std::make_unique<fclsh_family>();
+        h->f = build_family(dims, radius, kind, rng_seed, prime, include_zero_column != 0);
+        *out = h.release();
+    });
+}
+
+int fclsh_family_make(uint64_t dims, uint32_t radius, int32_t kind, const uint32_t* mapping,
+                      const uint64_t* seeds, uint64_t prime, fclsh_family** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (kind != 0 && kind != 1) throw UsageError("covering family: unknown construction kind");
+        if (dims && (!mapping || !seeds)) throw UsageError("covering family: mapping/seeds must have one entry per dimension");
+        auto h = std::make_unique<fclsh_family>();
+        h->f = make_family(dims, radius, static_cast<Kind>(kind), std::vector<uint32_t>(mapping, mapping + dims),
+                           std::vector<uint64_t>(seeds, seeds + dims), prime);
+        *out = h.release();
+    });
+}
+
+int fclsh_family_info_get(const fclsh_family* f, fclsh_family_info* out) {
+    return guarded([&] {
+        need(f, "family");
+        need(out, "out");
+        out->dims = f->f.dims;
+        out->radius = f->f.radius;
+        out->kind = static_cast<int32_t>(f->f.kind);
+        out->prime = f->f.prime;
+        out->tables = f->f.tables();
+    });
+}
+
+int fclsh_family_export(const fclsh_family* f, uint32_t* mapping, uint64_t* seeds) {
+    return guarded([&] {
+        need(f, "family");
+        if (mapping) std::memcpy(mapping, f->f.mapping.data(), f->f.dims * 4);
+        if (seeds) std::memcpy(seeds, f->f.seeds.data(), f->f.dims * 8);
+    });
+}
+
+void fclsh_family_destroy(fclsh_family* f) { delete f; }
+
+int fclsh_hash_batch(const fclsh_family* fc, const uint64_t* d_rows, uint64_t n, uint32_t row_words, void* d_keys,
+                     uint32_t key_bytes, uint64_t key_stride, int32_t layout, int device, void* stream) {
+    return guarded([&] {
+        need(fc, "family");
+        auto* f = const_cast<fclsh_family*>(fc);
+        if (row_words != (f->f.dims + 63) / 64) throw UsageError("hash: vector width does not match the family");
+        if (n && (!d_rows || !d_keys)) throw UsageError("hash: NULL buffer");
+        FCLSH_CUDA(cudaSetDevice(device));
+        hash_rows(f->on(device), d_rows, n, d_keys, key_bytes, key_stride, layout,
+                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fclsh_hash_batch_host(const fclsh_family* fc, const uint64_t* rows, uint64_t n, uint32_t row_words, void* keys,
+                          uint32_t key_bytes, int device) {
+    return guarded([&] {
+        need(fc, "family");
+        auto* f = const_cast<fclsh_family*>(fc);
+        if (row_words != (f->f.dims + 63) / 64) throw UsageError("hash: vector width does not match the family");
+        if (n == 0) return;
+        need(rows, "rows");
+        need(keys, "keys");
+        FCLSH_CUDA(cudaSetDevice(device));
+        DeviceFamilySet& fs = f->on(device);
+        DevBuf dr, dk;
+        const uint64_t L = f->f.tables();
+        dr.ensure(n * row_words * 8);
+        dk.ensure(n * L * key_bytes);
+        FCLSH_CUDA(cudaMemcpy(dr.p, rows, n * row_words * 8, cudaMemcpyHostToDevice));
+        hash_rows(fs, dr.as<uint64_t>(), n, dk.p, key_bytes, L, kLayoutPointMajor, nullptr);
+        FCLSH_CUDA(cudaMemcpy(keys, dk.p, n * L * key_bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+int fclsh_plan_make(uint64_t dims, uint32_t radius, double c, uint64_t n, uint64_t rng_seed,
+                    const fclsh_plan_override* force, uint64_t table_budget, fclsh_plan** out) {
+    return guarded([&] {
+        need(out, "out");
+        PlanOverride ov{};
+        if (force) {
+            if (force->kind < 0 || force->kind > 2) throw UsageError("plan: unknown plan kind");
+            ov = PlanOverride{static_cast<PlanKind>(force->kind), force->t};
+        }
+        auto h = std::make_unique<fclsh_plan>();
+        h->p = make_plan(dims, radius, c, n, rng_seed, force ? &ov : nullptr, table_budget);
+        *out = h.release();
+    });
+}
+
+int fclsh_plan_info_get(const fclsh_plan* p, fclsh_plan_info* out) {
+    return guarded([&] {
+        need(p, "plan");
+        need(out, "out");
+        out->kind = static_cast<int32_t>(p->p.kind);
+        out->dims = p->p.dims;
+        out->radius = p->p.radius;
+        out->t = p->p.t;
+        out->per_part_radius = p->p.per_part_radius;
+        out->part_count = p->p.part_count();
+        out->table_count = p->p.table_count();
+    });
+}
+
+int fclsh_plan_export(const fclsh_plan* p, uint32_t* permutation, uint64_t* parts) {
+    return guarded([&] {
+        need(p, "plan");
+        if (permutation && !p->p.permutation.empty())
+            std::memcpy(permutation, p->p.permutation.data(), p->p.permutation.size() * 4);
+        if (parts)
+            for (size_t i = 0; i < p->p.parts.size(); ++i) {
+                parts[2 * i] = p->p.parts[i].first;
+                parts[2 * i + 1] = p->p.parts[i].second;
+            }
+    });
+}
+
+void fclsh_plan_destroy(fclsh_plan* p) { delete p; }
+
+void fclsh_index_options_default(fclsh_index_options* o) {
+    if (!o) return;
+    o->prime = FCLSH_PRIME_M61;
+    o->include_zero_column = 0;
+    o->table_budget = FCLSH_DEFAULT_TABLE_BUDGET;
+    o->device = 0;
+    o->id_offset = 0;
+    o->directory_bits = 0;
+}
+
+int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint64_t dims, uint32_t radius,
+                      const fclsh_plan* plan, uint64_t rng_seed, const fclsh_index_options* opt, fclsh_index** out) {
+    return guarded([&] {
+        need(out, "out");
+        need(plan, "plan");
+        if (n) need(rows, "rows");
+        fclsh_index_options o;
+        fclsh_index_options_default(&o);
+        if (opt) o = *opt;
+        IndexBuildOptions bo;
+        bo.prime = o.prime;
+        bo.include_zero_column = o.include_zero_column != 0;
+        bo.table_budget = o.table_budget;
+        bo.device = o.device;
+        bo.id_offset = o.id_offset;
+        bo.directory_bits = o.directory_bits;
+        auto h = std::make_unique<fclsh_index>();
+        h->ix = build_index(rows, rows_on_device != 0, n, dims, radius, plan->p, rng_seed, bo);
+        *out = h.release();
+    });
+}
+
+int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out) {
+    return guarded([&] {
+        need(ix, "index");
+        need(out, "out");
+        const DeviceIndex& d = *ix->ix;
+        out->n = d.n;
+        out->dims = d.dims;
+        out->radius = d.radius;
+        out->table_count = d.tables;
+        out->entry_count = d.tables * d.n;
+        out->directory_bits = d.dir_bits;
+        out->device_bytes = d.device_bytes();
+        out->build_ms = d.build_ms;
+    });
+}
+
+int fclsh_index_family(const fclsh_index* ix, uint32_t part, fclsh_family** out) {
+    return guarded([&] {
+        need(ix, "index");
+        need(out, "out");
+        if (part >= ix->ix->fs->parts) throw UsageError("index: part out of range");
+        auto h = std::make_unique<fclsh_family>();
+        h->f = ix->ix->fs->families[part];
+        *out = h.release();
+    });
+}
+
+void fclsh_index_destroy(fclsh_index* ix) { delete ix; }
+
+int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t radius, fclsh_result** out) {
+    return guarded([&] {
+        need(ixh, "index");
+        need(out, "out");
+        if (nq) need(q_rows, "q_rows");
+        DeviceIndex& ix = *ixh->ix;
+        FCLSH_CUDA(cudaSetDevice(ix.device));
+        const uint64_t W = ix.row_words;
+        uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
+        if (nq) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
+        QueryOutput o = query_device(ix, dq, nq, radius, ix.stream);
+        auto* r = static_cast<fclsh_result*>(std::calloc(1, sizeof(fclsh_result)));
+        if (!r) throw std::bad_alloc();
+        r->nq = nq;
+        r->total = o.total;
+        const uint64_t tb = std::max<uint64_t>(1, o.total) * 4, qb = (nq + 1) * 8;
+        r->query = static_cast<uint32_t*>(std::malloc(tb));
+        r->id = static_cast<uint32_t*>(std::malloc(tb));
+        r->distance = static_cast<uint32_t*>(std::malloc(tb));
+        r->offsets = static_cast<uint64_t*>(std::malloc(qb));
+        r->collisions = static_cast<uint64_t*>(std::malloc(qb));
+        r->candidates = static_cast<uint64_t*>(std::malloc(qb));
+        r->found = static_cast<uint64_t*>(std::malloc(qb));
+        if (!r->query || !r->id || !r->distance || !r->offsets || !r->collisions || !r->candidates || !r->found) {
+            fclsh_result_free(r);
+            throw std::bad_alloc();
+        }
+        cudaStream_t s = ix.stream;
+        if (o.total) {
+            FCLSH_CUDA(cudaMemcpyAsync(r->query, o.d_query, o.total * 4, cudaMemcpyDeviceToHost, s));
+            FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
+            FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
+        }
+        FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, (nq + 1) * 8, cudaMemcpyDeviceToHost, s));
+        if (nq) {
+            FCLSH_CUDA(cudaMemcpyAsync(r->collisions, o.d_coll, nq * 8, cudaMemcpyDeviceToHost, s));
+            FCLSH_CUDA(cudaMemcpyAsync(r->candidates, o.d_cand, nq * 8, cudaMemcpyDeviceToHost, s));
+            FCLSH_CUDA(cudaMemcpyAsync(r->found, o.d_found, nq * 8, cudaMemcpyDeviceToHost, s));
+        }
+        FCLSH_CUDA(cudaStreamSynchronize(s));
+        r->time_hash_ms = ix.t_hash_ms;
+        r->time_probe_ms = ix.t_probe_ms;
+        r->time_verify_ms = ix.t_verify_ms;
+        *out = r;
+    });
+}
+
+void fclsh_result_free(fclsh_result* r) {
+    if (!r) return;
+    std::free(r->query);
+    std::free(r->id);
+    std::free(r->distance);
+    std::free(r->offsets);
+    std::free(r->collisions);
+    std::free(r->candidates);
+    std::free(r->found);
+    std::free(r);
+}
+
+int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius, void* stream,
+                       fclsh_device_result* out) {
+    return guarded([&] {
+        need(ixh, "index");
+        need(out, "out");
+        if (nq) need(d_q_rows, "d_q_rows");
+        QueryOutput o = query_device(*ixh->ix, d_q_rows, nq, radius, static_cast<cudaStream_t>(stream));
+        out->nq = nq;
+        out->total = o.total;
+        out->d_query = o.d_query;
+        out->d_id = o.d_id;
+        out->d_distance = o.d_dist;
+        out->d_offsets = o.d_offsets;
+        out->d_collisions = o.d_coll;
+        out->d_candidates = o.d_cand;
+        out->d_found = o.d_found;
+    });
+}
+
+uint64_t fclsh_launch_count(void) { return launch_counter(); }
+void fclsh_launch_count_reset(void) { launch_counter() = 0; }
+
+int fclsh_gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
+    return guarded([&] {
+        if (dims == 0) throw UsageError("gen: dims must be positive");
+        if (n) need(rows, "rows");
+        gen_bernoulli(seed, n, dims, rows, threads);
+    });
+}
+
+int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p, uint64_t* rows,
+                        int threads) {
+    return guarded([&] {
+        if (dims == 0) throw UsageError("gen: dims must be positive");
+        if (centres == 0) throw UsageError("gen: need at least one centre");
+        if (!(flip_p >= 0.0 && flip_p <= 1.0)) throw UsageError("gen: flip probability out of [0, 1]");
+        if (n) need(rows, "rows");
+        gen_clustered(seed, centres, n, dims, flip_p, rows, threads);
+    });
+}
+
+int fclsh_gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
+                      uint64_t* qrows, uint32_t* src_out) {
+    return guarded([&] {
+        if (dims == 0) throw UsageError("gen: dims must be positive");
+        if (n == 0) throw UsageError("gen: data size must be positive");
+        if (kmax > dims) throw UsageError("gen: planted distance exceeds dims");
+        need(data, "data");
+        if (nq) need(qrows, "qrows");
+        gen_planted(seed, data, n, dims, nq, kmax, qrows, src_out);
+    });
+}
+
+} // extern "C"

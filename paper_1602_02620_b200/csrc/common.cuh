@@ -1,0 +1,65 @@
+// Shared device/host helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "host.hpp"
+
+namespace fclsh_b200 {
+
+#define FCLSH_CUDA(call)                                                                     \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            throw ::fclsh_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// Per-thread count of kernels launched by this library (bench accounting).
+uint64_t& launch_counter();
+
+#define FCLSH_LAUNCHED()                                                                     \
+    do {                                                                                     \
+        ::fclsh_b200::launch_counter()++;                                                    \
+        cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e != cudaSuccess)                                                               \
+            throw ::fclsh_b200::CudaError(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr int kNumSMs = 148; // B200
+
+inline int sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+        return kNumSMs;
+    return v;
+}
+
+// RAII device buffer (grow-only when reused as a workspace).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void* ensure(size_t want) {
+        if (want <= bytes && p) return p;
+        release();
+        if (want == 0) want = 16;
+        FCLSH_CUDA(cudaMalloc(&p, want));
+        bytes = want;
+        return p;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+} // namespace fclsh_b200

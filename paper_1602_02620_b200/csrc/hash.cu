@@ -1,0 +1,625 @@
+// K1 -- batched fcLSH covering hash for sm_100a.
+//
+// Reference semantics (hash_batch_into, covering.cpp:169-182 and
+// batch_hash_kernel, hadamard.cpp:66-72): per row, scatter the seeds of set
+// bits onto their code columns (sketch t), run an N-point Hadamard transform
+// mod P, map x -> (l1 - x)/2 mod P and drop entry 0. Equivalently
+//     key[v] = sum_{c : popcount(v & c) odd} t[c]   (mod P),  v = 1..N-1.
+//
+// Fast path (P = 2^31 - 1, the 32-bit-key field of the BASELINE configs):
+// exact integer arithmetic, reduced once at the end. Seeds are split into a
+// 16-bit plane and a 15-bit plane; the signed transform F of each plane fits
+// int32 (|F| <= sum of the plane <= d' * 2^16 < 2^31 for d' <= 2^15), so the
+// butterflies are single 32-bit adds with no modular reduction. Finally
+//     O = (F[0] - F[v]) / 2  per plane,   key = (O_lo + 2^16 O_hi) mod P,
+// which is the canonical residue the reference stores (bit-exact).
+//
+// Work decomposition (N = 2^LOGN): G lanes cooperate on one row, each lane
+// holding E = N/G elements per plane in registers. Phase 1 runs log2(E)
+// butterfly stages in registers, one swizzled shared-memory transpose
+// (warp-local, __syncwarp only) regroups the elements, phase 2 runs the
+// remaining log2(G) stages in registers. Keys are staged in shared memory
+// and written with 16-byte stores so every table row receives full 32-byte
+// sectors (table-major layout) -- the pass is a pure stream: rows in, keys
+// out, no re-reads. A CTA owns PT = 256/G rows per tile; the grid is
+// persistent over tiles.
+//
+// Generic path (any odd P < 2^63, u64 keys, any N): one CTA per row, mod-P
+// butterflies in shared/global memory exactly as the reference sequences
+// them. Used for the M61 default field and the small-prime golden tests.
+
+#include "hash.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace fclsh_b200 {
+
+namespace {
+
+constexpr uint32_t kP31 = 0x7FFFFFFFu;
+constexpr int kMaxParts = 32;
+
+// lanes per row for a given LOGN
+__host__ __device__ constexpr int lanes_for(int logn) {
+    return logn <= 5 ? 1 : (logn <= 7 ? 8 : (logn <= 9 ? 16 : 32));
+}
+
+struct FastParams {
+    const uint64_t* rows;
+    uint64_t n;
+    uint32_t row_words;
+    uint32_t parts;
+    uint32_t part_words;   // uint2 per part in fam
+    uint32_t lane_entries; // M (general path)
+    const uint2* fam;
+    void* keys;
+    uint64_t key_stride;
+    uint64_t L;
+    int layout;
+    int key_bytes;
+};
+
+template <int SIZE>
+__device__ __forceinline__ void fht_signed(uint32_t* x) {
+#pragma unroll
+    for (int h = 1; h < SIZE; h <<= 1) {
+#pragma unroll
+        for (int i = 0; i < SIZE; ++i) {
+            if ((i & h) == 0) {
+                uint32_t a = x[i], b = x[i + h];
+                x[i] = a + b;
+                x[i + h] = a - b;
+            }
+        }
+    }
+}
+
+// (O_lo + 2^16 * O_hi) mod (2^31-1), canonical. O_lo = (Tlo - Flo)/2 < 2^31,
+// O_hi = (Thi - Fhi)/2 < 2^30.
+__device__ __forceinline__ uint32_t finish_key(uint32_t Tlo, uint32_t Thi, uint32_t Flo, uint32_t Fhi) {
+    uint32_t slo = (Tlo - Flo) >> 1;
+    uint32_t shi = (Thi - Fhi) >> 1;
+    // 2^16 * shi = (shi >> 15) * 2^31 + (shi & 0x7fff) * 2^16 == (shi >> 15) + ((shi & 0x7fff) << 16)
+    uint32_t s = slo + (shi >> 15) + ((shi & 0x7FFFu) << 16); // < 2^32
+    s = (s & kP31) + (s >> 31);                               // <= 2^31
+    uint32_t s1 = s + 1;
+    return (s1 & kP31) + (s1 >> 31) - 1;                      // canonical in [0, P)
+}
+
+__device__ __forceinline__ uint32_t row_bit(const uint32_t* row32, uint32_t pos) {
+    return (row32[pos >> 5] >> (pos & 31)) & 1u;
+}
+
+// staging swizzle for slot s (see the store loop): spreads the PT/4 slot
+// groups read by one warp over disjoint bank ranges
+template <int PT>
+__device__ __forceinline__ uint32_t stage_swz(uint32_t s) {
+    constexpr int M = PT / 4;
+    constexpr int V = 32 / M;
+    return (((s >> 2) & (M - 1)) * V) ^ ((s & 3) << 4);
+}
+
+template <int LOGN, bool DIRECT>
+__global__ void __launch_bounds__(256) k_hash_m31(const FastParams p) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = lanes_for(LOGN);
+    constexpr int E = N / G;
+    constexpr int PT = 256 / G;
+    constexpr int EG = (G > 1) ? E / G : 1;
+    static_assert(G == 1 || EG == 1 || EG == 2, "phase-2 layout");
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* xbuf = reinterpret_cast<uint64_t*>(smem);    // 256 * E u64
+    uint64_t* rows_s = xbuf + 256 * E;                      // PT * row_words u64
+    uint2* fam_s = reinterpret_cast<uint2*>(rows_s + PT * p.row_words);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int slot = tid / G;
+    const int g = tid % G;
+
+    for (uint32_t i = tid; i < p.parts * p.part_words; i += 256) fam_s[i] = p.fam[i];
+
+    const uint64_t ntiles = (p.n + PT - 1) / PT;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t p0 = tile * PT;
+        __syncthreads(); // previous tile done with rows_s / xbuf; fam_s staged
+        {
+            const uint64_t base = p0 * p.row_words;
+            const uint64_t lim = p.n * p.row_words;
+            for (uint32_t i = tid; i < PT * p.row_words; i += 256)
+                rows_s[i] = (base + i < lim) ? __ldg(p.rows + base + i) : 0ull;
+        }
+        __syncthreads();
+        const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rows_s + slot * p.row_words);
+        const uint64_t my_point = p0 + slot;
+
+        for (uint32_t part = 0; part < p.parts; ++part) {
+            const uint2* fam = fam_s + part * p.part_words;
+            uint32_t lo[E], hi[E];
+
+            // ---- sketch: t[c] for this lane's columns c = g*E + j, split into planes
+            if constexpr (DIRECT) {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint2 e = fam[g * E + j];
+                    const uint32_t m = 0u - row_bit(myrow, e.x);
+                    lo[j] = e.y & m & 0xFFFFu;
+                    hi[j] = (e.y >> 16) & m;
+                }
+            } else {
+                // warp-local accumulation buffer sk[col][lane] (conflict-free for any col)
+                uint64_t* sk = xbuf + warp * 32 * E;
+#pragma unroll
+                for (int j = 0; j < E; ++j) sk[j * 32 + lane] = 0ull;
+                const uint2* le = fam + g * p.lane_entries;
+                uint32_t cur = le[0].x >> 24;
+                uint64_t acc = 0;
+                for (uint32_t k = 0; k < p.lane_entries; ++k) {
+                    const uint2 e = le[k];
+                    const uint32_t col = e.x >> 24;
+                    if (col != cur) {
+                        sk[cur * 32 + lane] = acc;
+                        acc = 0;
+                        cur = col;
+                    }
+                    const uint64_t packed = (uint64_t(e.y >> 16) << 32) | (e.y & 0xFFFFu);
+                    acc += row_bit(myrow, e.x & 0xFFFFFFu) ? packed : 0ull;
+                }
+                sk[cur * 32 + lane] = acc;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint64_t v = sk[j * 32 + lane];
+                    lo[j] = uint32_t(v);
+                    hi[j] = uint32_t(v >> 32);
+                }
+                __syncwarp();
+            }
+
+            // ---- phase 1: log2(E) stages in registers
+            fht_signed<E>(lo);
+            fht_signed<E>(hi);
+
+            uint32_t Tlo, Thi;
+            if constexpr (G > 1) {
+                // ---- swizzled transpose through this row's slot region (warp-local)
+                uint64_t* xs = xbuf + slot * N;
+#pragma unroll
+                for (int j = 0; j < E; j += 2) {
+                    const int idx = g * E + (j ^ ((2 * g) & (E - 1)));
+                    *reinterpret_cast<uint4*>(xs + idx) = make_uint4(lo[j], hi[j], lo[j + 1], hi[j + 1]);
+                }
+                __syncwarp();
+                // phase-2 layout: register k*G + h holds element c = h*E + g*EG + k
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const int idx = h * E + ((g * EG) ^ ((2 * h) & (E - 1)));
+                    if constexpr (EG == 2) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(xs + idx);
+                        lo[h] = v.x;
+                        hi[h] = v.y;
+                        lo[G + h] = v.z;
+                        hi[G + h] = v.w;
+                    } else {
+                        const uint2 v = *reinterpret_cast<const uint2*>(xs + idx);
+                        lo[h] = v.x;
+                        hi[h] = v.y;
+                    }
+                }
+                __syncwarp();
+                // ---- phase 2: log2(G) stages in registers
+#pragma unroll
+                for (int k = 0; k < EG; ++k) {
+                    fht_signed<G>(lo + k * G);
+                    fht_signed<G>(hi + k * G);
+                }
+                // totals F[0] sit in lane g == 0 of the row, register 0
+                const int src = lane & ~(G - 1);
+                Tlo = __shfl_sync(0xffffffffu, lo[0], src);
+                Thi = __shfl_sync(0xffffffffu, hi[0], src);
+            } else {
+                Tlo = lo[0];
+                Thi = hi[0];
+            }
+
+            // ---- final reduction + output
+            if constexpr (G == 1) {
+                // thread per row: table-major stores are coalesced across lanes directly
+                if (my_point < p.n) {
+#pragma unroll
+                    for (int v = 1; v < N; ++v) {
+                        const uint32_t key = finish_key(Tlo, Thi, lo[v], hi[v]);
+                        const uint64_t t = part * p.L + (v - 1);
+                        const uint64_t off = p.layout == 0 ? t * p.key_stride + my_point
+                                                           : my_point * p.key_stride + t;
+                        if (p.key_bytes == 4)
+                            static_cast<uint32_t*>(p.keys)[off] = key;
+                        else
+                            static_cast<uint64_t*>(p.keys)[off] = key;
+                    }
+                }
+            } else {
+                // stage keys: slot s occupies u32 [2sN, 2sN + N), element v at v ^ swz(s)
+                uint32_t* stg = reinterpret_cast<uint32_t*>(xbuf) + 2 * slot * N;
+                const uint32_t sw = stage_swz<PT>(slot);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const int v0 = h * E + g * EG;
+                    if constexpr (EG == 2) {
+                        const uint32_t k0 = finish_key(Tlo, Thi, lo[h], hi[h]);
+                        const uint32_t k1 = finish_key(Tlo, Thi, lo[G + h], hi[G + h]);
+                        *reinterpret_cast<uint2*>(stg + (v0 ^ sw)) = make_uint2(k0, k1);
+                    } else {
+                        stg[v0 ^ sw] = finish_key(Tlo, Thi, lo[h], hi[h]);
+                    }
+                }
+                __syncthreads();
+                const uint32_t* stg_all = reinterpret_cast<const uint32_t*>(xbuf);
+                if (p.layout == 0) {
+                    constexpr int M = PT / 4;
+                    for (uint32_t i = tid; i < uint32_t(N) * M; i += 256) {
+                        const uint32_t m = i % M;
+                        const uint32_t v = i / M;
+                        if (v == 0) continue;
+                        uint32_t kk[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t s = 4 * m + q;
+                            kk[q] = stg_all[2 * s * N + (v ^ stage_swz<PT>(s))];
+                        }
+                        const uint64_t t = part * p.L + (v - 1);
+                        const uint64_t pt = p0 + 4 * m;
+                        const uint64_t off = t * p.key_stride + pt;
+                        if (p.key_bytes == 4) {
+                            uint32_t* kp = static_cast<uint32_t*>(p.keys);
+                            if (pt + 4 <= p.n && (off & 3) == 0) {
+                                *reinterpret_cast<uint4*>(kp + off) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    if (pt + q < p.n) kp[off + q] = kk[q];
+                            }
+                        } else {
+                            uint64_t* kp = static_cast<uint64_t*>(p.keys);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (pt + q < p.n) kp[off + q] = kk[q];
+                        }
+                    }
+                } else {
+                    for (uint32_t i = tid; i < uint32_t(N) * PT; i += 256) {
+                        const uint32_t s = i / N;
+                        const uint32_t v = i % N;
+                        if (v == 0 || p0 + s >= p.n) continue;
+                        const uint32_t key = stg_all[2 * s * N + (v ^ stage_swz<PT>(s))];
+                        const uint64_t off = (p0 + s) * p.key_stride + part * p.L + (v - 1);
+                        if (p.key_bytes == 4)
+                            static_cast<uint32_t*>(p.keys)[off] = key;
+                        else
+                            static_cast<uint64_t*>(p.keys)[off] = key;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- generic path
+
+struct GenericParams {
+    const uint64_t* rows;
+    uint64_t n;
+    uint32_t row_words;
+    uint32_t parts;
+    uint64_t N;
+    uint64_t L;
+    uint64_t prime;
+    uint64_t max_dims;
+    const uint32_t* col_ptr;  // [parts][N+1]
+    const uint32_t* ent_pos;  // [parts][max_dims]
+    const uint64_t* ent_seed; // [parts][max_dims]
+    uint64_t* scratch;        // [gridDim.x][N] when not in shared memory
+    int use_smem;
+    void* keys;
+    uint64_t key_stride;
+    int layout;
+    int key_bytes;
+};
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t p) { // modmath.hpp:12-15
+    uint64_t s = a + b;
+    return s >= p ? s - p : s;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t p) { // modmath.hpp:17-19
+    return a >= b ? a - b : a + p - b;
+}
+
+__global__ void __launch_bounds__(256) k_hash_generic(const GenericParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t red[8];
+    uint64_t* t = p.use_smem ? reinterpret_cast<uint64_t*>(smem) : p.scratch + blockIdx.x * p.N;
+    const uint64_t P = p.prime;
+    const int tid = threadIdx.x;
+    for (uint64_t pt = blockIdx.x; pt < p.n; pt += gridDim.x) {
+        const uint64_t* row = p.rows + pt * p.row_words;
+        for (uint32_t part = 0; part < p.parts; ++part) {
+            const uint32_t* cp = p.col_ptr + part * (p.N + 1);
+            const uint32_t* ep = p.ent_pos + part * p.max_dims;
+            const uint64_t* es = p.ent_seed + part * p.max_dims;
+            // sketch (covering.cpp:174-179): per column, seeds of set bits in view order
+            uint64_t part_l1 = 0;
+            for (uint64_t c = tid; c < p.N; c += blockDim.x) {
+                uint64_t acc = 0;
+                for (uint32_t k = cp[c]; k < cp[c + 1]; ++k) {
+                    const uint32_t pos = ep[k];
+                    if ((row[pos >> 6] >> (pos & 63)) & 1ull) acc = add_mod(acc, es[k], P);
+                }
+                t[c] = acc;
+                part_l1 = add_mod(part_l1, acc, P);
+            }
+            // l1 = total mass mod P (exact modular sum, order-free for P < 2^63)
+            for (int o = 16; o > 0; o >>= 1) part_l1 = add_mod(part_l1, __shfl_xor_sync(0xffffffffu, part_l1, o), P);
+            if ((tid & 31) == 0) red[tid >> 5] = part_l1;
+            __syncthreads();
+            uint64_t l1 = 0;
+            for (int w = 0; w < int(blockDim.x >> 5); ++w) l1 = add_mod(l1, red[w], P);
+            // fht_mod_in_place (hadamard.cpp:51-64)
+            for (uint64_t half = 1; half < p.N; half <<= 1) {
+                for (uint64_t b = tid; b < p.N / 2; b += blockDim.x) {
+                    const uint64_t i = (b / half) * 2 * half + (b % half);
+                    const uint64_t a = t[i], c = t[i + half];
+                    t[i] = add_mod(a, c, P);
+                    t[i + half] = sub_mod(a, c, P);
+                }
+                __syncthreads();
+            }
+            // x <- half * (l1 - x) mod P (hadamard.cpp:69-71); for canonical y,
+            // half*y mod P is y/2 (y even) or (y+P)/2 (y odd).
+            for (uint64_t v = 1 + tid; v < p.N; v += blockDim.x) {
+                const uint64_t y = sub_mod(l1, t[v], P);
+                const uint64_t key = (y & 1) ? (y >> 1) + (P >> 1) + 1 : (y >> 1);
+                const uint64_t tt = part * p.L + (v - 1);
+                const uint64_t off = p.layout == 0 ? tt * p.key_stride + pt : pt * p.key_stride + tt;
+                if (p.key_bytes == 4)
+                    static_cast<uint32_t*>(p.keys)[off] = uint32_t(key);
+                else
+                    static_cast<uint64_t*>(p.keys)[off] = key;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int LOGN, bool DIRECT>
+size_t fast_smem_bytes(const DeviceFamilySet& fs) {
+    constexpr int G = lanes_for(LOGN);
+    constexpr int E = (1 << LOGN) / G;
+    constexpr int PT = 256 / G;
+    return size_t(256) * E * 8 + size_t(PT) * fs.row_words * 8 + size_t(fs.parts) * fs.part_words * 8;
+}
+
+template <int LOGN, bool DIRECT>
+void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream) {
+    constexpr int G = lanes_for(LOGN);
+    constexpr int PT = 256 / G;
+    const size_t smem = fast_smem_bytes<LOGN, DIRECT>(fs);
+    auto kern = k_hash_m31<LOGN, DIRECT>;
+    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
+    const uint64_t tiles = (prm.n + PT - 1) / PT;
+    const uint64_t grid = std::min<uint64_t>(tiles, uint64_t(per_sm) * sm_count(fs.device));
+    kern<<<unsigned(std::max<uint64_t>(grid, 1)), 256, smem, stream>>>(prm);
+    FCLSH_LAUNCHED();
+}
+
+template <bool DIRECT>
+void dispatch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t s) {
+    switch (fs.logn) {
+    case 2: launch_fast<2, DIRECT>(fs, prm, s); break;
+    case 3: launch_fast<3, DIRECT>(fs, prm, s); break;
+    case 4: launch_fast<4, DIRECT>(fs, prm, s); break;
+    case 5: launch_fast<5, DIRECT>(fs, prm, s); break;
+    case 6: launch_fast<6, DIRECT>(fs, prm, s); break;
+    case 7: launch_fast<7, DIRECT>(fs, prm, s); break;
+    case 8: launch_fast<8, DIRECT>(fs, prm, s); break;
+    case 9: launch_fast<9, DIRECT>(fs, prm, s); break;
+    case 10: launch_fast<10, DIRECT>(fs, prm, s); break;
+    case 11: launch_fast<11, DIRECT>(fs, prm, s); break;
+    default: throw UsageError("hash: no fast kernel for this code order");
+    }
+}
+
+} // namespace
+
+std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::vector<Family> families,
+                                                        int device) {
+    auto fs = std::make_unique<DeviceFamilySet>();
+    fs->device = device;
+    fs->parts = plan.part_count();
+    if (families.size() != fs->parts) throw UsageError("hash: one family per plan part required");
+    if (fs->parts > kMaxParts) throw ResourceError("hash: too many plan parts");
+    fs->radius = families[0].radius;
+    fs->logn = fs->radius + 1;
+    fs->order = uint64_t(1) << fs->logn;
+    fs->tables = fs->order - 1;
+    fs->prime = families[0].prime;
+    fs->dims = plan.dims;
+    fs->row_words = uint32_t((plan.dims + 63) / 64);
+    for (uint32_t p = 0; p < fs->parts; ++p) {
+        const Family& f = families[p];
+        if (f.radius != fs->radius || f.prime != fs->prime)
+            throw UsageError("hash: plan parts must share radius and prime");
+        if (f.dims != plan.part_dims(p)) throw UsageError("hash: family width does not match the plan part");
+        fs->max_part_dims = std::max<uint64_t>(fs->max_part_dims, f.dims);
+    }
+    const uint64_t N = fs->order;
+    FCLSH_CUDA(cudaSetDevice(device));
+
+    // ---------------- generic CSR (always built; the fast path may be unavailable)
+    {
+        std::vector<uint32_t> cp(size_t(fs->parts) * (N + 1), 0);
+        std::vector<uint32_t> epos(size_t(fs->parts) * fs->max_part_dims, 0);
+        std::vector<uint64_t> eseed(size_t(fs->parts) * fs->max_part_dims, 0);
+        for (uint32_t p = 0; p < fs->parts; ++p) {
+            const Family& f = families[p];
+            uint32_t* c = cp.data() + size_t(p) * (N + 1);
+            for (uint64_t j = 0; j < f.dims; ++j) c[f.mapping[j] + 1]++;
+            for (uint64_t k = 0; k < N; ++k) c[k + 1] += c[k];
+            std::vector<uint32_t> fill(c, c + N);
+            for (uint64_t j = 0; j < f.dims; ++j) { // ascending view position per column
+                const uint32_t at = fill[f.mapping[j]]++;
+                epos[size_t(p) * fs->max_part_dims + at] = uint32_t(plan.source_bit(p, j));
+                eseed[size_t(p) * fs->max_part_dims + at] = f.seeds[j];
+            }
+        }
+        FCLSH_CUDA(cudaMemcpy(fs->col_ptr.ensure(cp.size() * 4), cp.data(), cp.size() * 4, cudaMemcpyHostToDevice));
+        FCLSH_CUDA(cudaMemcpy(fs->ent_pos.ensure(epos.size() * 4), epos.data(), epos.size() * 4, cudaMemcpyHostToDevice));
+        FCLSH_CUDA(cudaMemcpy(fs->ent_seed.ensure(eseed.size() * 8), eseed.data(), eseed.size() * 8, cudaMemcpyHostToDevice));
+    }
+
+    // ---------------- fast path tables
+    fs->fast = fs->prime == kMersenne31 && fs->logn >= 2 && fs->logn <= 11 &&
+               fs->max_part_dims <= (uint64_t(1) << 15) && plan.dims < (uint64_t(1) << 24);
+    if (fs->fast) {
+        // Positions on column 0 never reach a key (they cancel in l1 - FHT[v]); drop them.
+        bool direct = true;
+        for (const Family& f : families) {
+            std::vector<uint32_t> cnt(N, 0);
+            for (uint64_t j = 0; j < f.dims; ++j)
+                if (f.mapping[j] != 0 && ++cnt[f.mapping[j]] > 1) direct = false;
+        }
+        fs->direct = direct;
+        const int G = lanes_for(int(fs->logn));
+        const uint64_t E = N / G;
+        std::vector<uint2> blob;
+        if (direct) {
+            fs->part_words = uint32_t(N);
+            blob.assign(size_t(fs->parts) * N, make_uint2(0, 0));
+            for (uint32_t p = 0; p < fs->parts; ++p) {
+                const Family& f = families[p];
+                for (uint64_t j = 0; j < f.dims; ++j)
+                    if (f.mapping[j] != 0)
+                        blob[size_t(p) * N + f.mapping[j]] =
+                            make_uint2(uint32_t(plan.source_bit(p, j)), uint32_t(f.seeds[j]));
+            }
+        } else {
+            // per lane g: entries of columns [gE, gE+E), sorted by column, padded to M
+            std::vector<std::vector<std::vector<uint2>>> lists(fs->parts, std::vector<std::vector<uint2>>(G));
+            uint32_t M = 1;
+            for (uint32_t p = 0; p < fs->parts; ++p) {
+                const Family& f = families[p];
+                std::vector<std::vector<uint64_t>> bycol(N);
+                for (uint64_t j = 0; j < f.dims; ++j)
+                    if (f.mapping[j] != 0) bycol[f.mapping[j]].push_back(j);
+                for (int g = 0; g < G; ++g) {
+                    auto& L = lists[p][g];
+                    for (uint64_t c = g * E; c < (g + 1) * E; ++c)
+                        for (uint64_t j : bycol[c])
+                            L.push_back(make_uint2(uint32_t(plan.source_bit(p, j)) | (uint32_t(c - g * E) << 24),
+                                                   uint32_t(f.seeds[j])));
+                    M = std::max<uint32_t>(M, uint32_t(L.size()));
+                }
+            }
+            fs->lane_entries = M;
+            fs->part_words = uint32_t(G) * M;
+            blob.assign(size_t(fs->parts) * fs->part_words, make_uint2(uint32_t(E - 1) << 24, 0));
+            for (uint32_t p = 0; p < fs->parts; ++p)
+                for (int g = 0; g < G; ++g)
+                    std::copy(lists[p][g].begin(), lists[p][g].end(),
+                              blob.begin() + size_t(p) * fs->part_words + size_t(g) * M);
+        }
+        // shared-memory budget check (227 KB per CTA)
+        const uint64_t smem = uint64_t(256) * E * 8 + uint64_t(256 / G) * fs->row_words * 8 +
+                              uint64_t(fs->parts) * fs->part_words * 8;
+        if (smem > 227 * 1024) {
+            fs->fast = false;
+        } else {
+            FCLSH_CUDA(cudaMemcpy(fs->fam.ensure(blob.size() * 8), blob.data(), blob.size() * 8,
+                                  cudaMemcpyHostToDevice));
+        }
+    }
+    fs->families = std::move(families);
+    return fs;
+}
+
+std::unique_ptr<DeviceFamilySet> make_device_family_set(const Family& f, int device) {
+    Plan plan;
+    plan.kind = PlanKind::identity;
+    plan.dims = f.dims;
+    plan.radius = f.radius;
+    plan.t = 1;
+    plan.per_part_radius = f.radius;
+    return make_device_family_set(plan, std::vector<Family>{f}, device);
+}
+
+void hash_rows(DeviceFamilySet& fs, const uint64_t* d_rows, uint64_t n, void* d_keys,
+               uint32_t key_bytes, uint64_t key_stride, int layout, cudaStream_t stream,
+               uint32_t part_begin, uint32_t part_count) {
+    if (part_count == 0) part_count = fs.parts - part_begin;
+    if (part_begin + part_count > fs.parts) throw UsageError("hash: part range out of bounds");
+    if (key_bytes != 4 && key_bytes != 8) throw UsageError("hash: key_bytes must be 4 or 8");
+    if (key_bytes == 4 && fs.prime > 0xFFFFFFFFull)
+        throw UsageError("hash: 4-byte keys need a prime below 2^32");
+    if (layout != 0 && layout != 1) throw UsageError("hash: unknown key layout");
+    if (layout == 0 && key_stride < n) throw UsageError("hash: key_stride below the row count");
+    if (layout == 1 && key_stride < uint64_t(part_count) * fs.tables)
+        throw UsageError("hash: key_stride below the table count");
+    if (n == 0) return;
+    FCLSH_CUDA(cudaSetDevice(fs.device));
+    if (fs.fast) {
+        FastParams prm{};
+        prm.rows = d_rows;
+        prm.n = n;
+        prm.row_words = fs.row_words;
+        prm.parts = part_count;
+        prm.part_words = fs.part_words;
+        prm.lane_entries = fs.lane_entries;
+        prm.fam = fs.fam.as<uint2>() + size_t(part_begin) * fs.part_words;
+        prm.keys = d_keys;
+        prm.key_stride = key_stride;
+        prm.L = fs.tables;
+        prm.layout = layout;
+        prm.key_bytes = int(key_bytes);
+        if (fs.direct)
+            dispatch_fast<true>(fs, prm, stream);
+        else
+            dispatch_fast<false>(fs, prm, stream);
+        return;
+    }
+    GenericParams prm{};
+    prm.rows = d_rows;
+    prm.n = n;
+    prm.row_words = fs.row_words;
+    prm.parts = part_count;
+    prm.N = fs.order;
+    prm.L = fs.tables;
+    prm.prime = fs.prime;
+    prm.max_dims = fs.max_part_dims;
+    prm.col_ptr = fs.col_ptr.as<uint32_t>() + size_t(part_begin) * (fs.order + 1);
+    prm.ent_pos = fs.ent_pos.as<uint32_t>() + size_t(part_begin) * fs.max_part_dims;
+    prm.ent_seed = fs.ent_seed.as<uint64_t>() + size_t(part_begin) * fs.max_part_dims;
+    prm.keys = d_keys;
+    prm.key_stride = key_stride;
+    prm.layout = layout;
+    prm.key_bytes = int(key_bytes);
+    const size_t tbytes = size_t(fs.order) * 8;
+    const uint64_t grid = std::min<uint64_t>(n, uint64_t(sm_count(fs.device)) * 8);
+    size_t smem = 0;
+    if (tbytes <= 96 * 1024) {
+        prm.use_smem = 1;
+        smem = tbytes;
+        FCLSH_CUDA(cudaFuncSetAttribute(k_hash_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    } else {
+        prm.use_smem = 0;
+        prm.scratch = static_cast<uint64_t*>(fs.scratch.ensure(grid * tbytes));
+    }
+    k_hash_generic<<<unsigned(grid), 256, smem, stream>>>(prm);
+    FCLSH_LAUNCHED();
+}
+
+} // namespace fclsh_b200

@@ -1,0 +1,560 @@
+// K2 (table build) and K3-K5 (probe, gather + dedup, verify) for sm_100a.
+//
+// Build (reference: build_index index.cpp:49-119 + PostingTable::finalize
+// posting.cpp:9-12): for each part, K1 writes the part's L key columns
+// table-major; then per table a counting pass over the top key bits builds
+// the cell directory (CSR offsets), a scatter pass places (key, id) into the
+// cells, and a per-cell sort orders each cell by (key, id) -- so every table
+// ends up exactly as the reference's sorted posting array, plus O(1) cell
+// lookup instead of a binary search. Cells are tiny on i.i.d. data (about
+// two entries); long cells from clustered data go to a CTA-wide sort.
+//
+// Query (reference: query_r_nn index.cpp:157-188):
+//   S1  K1 hashes the query rows point-major.
+//   S2  K3 probes every (query, table): directory cell -> matching key run;
+//       counts are the reference's `collisions`. K4 gathers the ids of all
+//       runs per query and sorts each query's list (dedup = adjacent
+//       uniques, `candidates`).
+//   S3  K5 verifies each distinct candidate with XOR+popcount over the full
+//       row and keeps dist <= radius (`found`, ids ascending as the
+//       reference's std::sort leaves them); a compaction writes the sorted
+//       (query, id, distance) triples.
+
+#include "index.cuh"
+
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+namespace fclsh_b200 {
+
+namespace {
+
+struct NarrowEntry {
+    using E = unsigned long long;
+    using K = uint32_t;
+    __device__ __forceinline__ static uint64_t key(E e) { return e >> 32; }
+    __device__ __forceinline__ static uint32_t id(E e) { return uint32_t(e); }
+    __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return (E(k) << 32) | i; }
+    __device__ __forceinline__ static bool less(E a, E b) { return a < b; }
+    __device__ __forceinline__ static E maxval() { return ~0ull; }
+};
+
+struct WideEntry {
+    using E = ulonglong2; // x = key, y = id
+    using K = uint64_t;
+    __device__ __forceinline__ static uint64_t key(E e) { return e.x; }
+    __device__ __forceinline__ static uint32_t id(E e) { return uint32_t(e.y); }
+    __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return make_ulonglong2(k, i); }
+    __device__ __forceinline__ static bool less(E a, E b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+    __device__ __forceinline__ static E maxval() { return make_ulonglong2(~0ull, ~0ull); }
+};
+
+// ----------------------------------------------------------------- build
+
+template <typename K>
+__global__ void k_hist(const K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t cells,
+                       uint32_t* __restrict__ cnt) {
+    const uint32_t t = blockIdx.y;
+    const K* kt = keys + uint64_t(t) * n;
+    uint32_t* ct = cnt + uint64_t(t) * (cells + 1);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(ct + (uint64_t(kt[i]) >> shift), 1u);
+}
+
+// One CTA per table: exclusive scan of cnt[0..cells] -> dir and cursor.
+__global__ void __launch_bounds__(1024) k_scan_cells(const uint32_t* __restrict__ cnt, uint64_t cells,
+                                                     uint32_t* __restrict__ dir, uint32_t* __restrict__ cursor) {
+    using BlockScan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ uint32_t carry_s;
+    const uint32_t t = blockIdx.x;
+    const uint32_t* c = cnt + uint64_t(t) * (cells + 1);
+    uint32_t* d = dir + uint64_t(t) * (cells + 1);
+    uint32_t* u = cursor + uint64_t(t) * (cells + 1);
+    uint32_t carry = 0;
+    constexpr int IPT = 4;
+    for (uint64_t base = 0; base < cells + 1; base += 1024 * IPT) {
+        uint32_t v[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const uint64_t i = base + threadIdx.x * IPT + k;
+            v[k] = i < cells + 1 ? c[i] : 0u;
+        }
+        uint32_t agg;
+        BlockScan(tmp).ExclusiveSum(v, v, agg);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const uint64_t i = base + threadIdx.x * IPT + k;
+            if (i < cells + 1) {
+                d[i] = v[k] + carry;
+                u[i] = v[k] + carry;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + agg;
+        __syncthreads();
+        carry = carry_s;
+    }
+}
+
+template <typename T, typename K>
+__global__ void k_scatter(const K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t cells,
+                          uint32_t* __restrict__ cursor, typename T::E* __restrict__ entries) {
+    const uint32_t t = blockIdx.y;
+    const K* kt = keys + uint64_t(t) * n;
+    uint32_t* ut = cursor + uint64_t(t) * (cells + 1);
+    typename T::E* et = entries + uint64_t(t) * n;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t key = kt[i];
+        const uint32_t pos = atomicAdd(ut + (key >> shift), 1u);
+        et[pos] = T::make(key, uint32_t(i));
+    }
+}
+
+constexpr uint32_t kSmallCell = 16;
+
+// Thread per cell: insertion-sort cells up to kSmallCell entries; longer
+// cells are queued for k_sort_big.
+template <typename T>
+__global__ void k_sort_cells(const uint32_t* __restrict__ dir, uint64_t cells, uint64_t n, uint32_t tables,
+                             typename T::E* __restrict__ entries, uint2* __restrict__ big,
+                             unsigned int* __restrict__ big_count) {
+    using E = typename T::E;
+    const uint64_t total = uint64_t(tables) * cells;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t t = uint32_t(i / cells);
+        const uint64_t c = i % cells;
+        const uint32_t* d = dir + uint64_t(t) * (cells + 1);
+        const uint32_t b = d[c], e = d[c + 1];
+        const uint32_t len = e - b;
+        if (len <= 1) continue;
+        if (len > kSmallCell) {
+            const unsigned int slot = atomicAdd(big_count, 1u);
+            big[slot] = make_uint2(t, uint32_t(c));
+            continue;
+        }
+        E* p = entries + uint64_t(t) * n + b;
+        E v[kSmallCell];
+#pragma unroll
+        for (uint32_t k = 0; k < kSmallCell; ++k)
+            if (k < len) v[k] = p[k];
+        for (uint32_t k = 1; k < len; ++k) {
+            E x = v[k];
+            int j = int(k) - 1;
+            while (j >= 0 && T::less(x, v[j])) {
+                v[j + 1] = v[j];
+                --j;
+            }
+            v[j + 1] = x;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kSmallCell; ++k)
+            if (k < len) p[k] = v[k];
+    }
+}
+
+// Ascending-only bitonic network (every compare puts the min at the lower
+// index), so positions >= len behave as +inf padding and are never touched.
+template <typename T, typename Ptr>
+__device__ void bitonic_sort(Ptr a, uint32_t len, uint32_t pow2) {
+    for (uint32_t k = 2; k <= pow2; k <<= 1) {
+        for (uint32_t i = threadIdx.x; i < pow2 / 2; i += blockDim.x) { // flip step
+            const uint32_t blk = i / (k / 2), off = i % (k / 2);
+            const uint32_t lo = blk * k + off, hi = blk * k + (k - 1 - off);
+            if (hi < len && T::less(a[hi], a[lo])) {
+                auto tmp = a[lo];
+                a[lo] = a[hi];
+                a[hi] = tmp;
+            }
+        }
+        __syncthreads();
+        for (uint32_t j = k / 4; j > 0; j >>= 1) { // half cleaners
+            for (uint32_t i = threadIdx.x; i < pow2 / 2; i += blockDim.x) {
+                const uint32_t blk = i / j, off = i % j;
+                const uint32_t lo = blk * 2 * j + off, hi = lo + j;
+                if (hi < len && T::less(a[hi], a[lo])) {
+                    auto tmp = a[lo];
+                    a[lo] = a[hi];
+                    a[hi] = tmp;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ dir, uint64_t cells, uint64_t n,
+                                                  typename T::E* __restrict__ entries, const uint2* __restrict__ big,
+                                                  uint32_t cap) {
+    using E = typename T::E;
+    extern __shared__ __align__(16) unsigned char smem[];
+    E* s = reinterpret_cast<E*>(smem);
+    const uint2 bc = big[blockIdx.x];
+    const uint32_t* d = dir + uint64_t(bc.x) * (cells + 1);
+    const uint32_t b = d[bc.y], len = d[bc.y + 1] - b;
+    E* p = entries + uint64_t(bc.x) * n + b;
+    uint32_t pow2 = 1;
+    while (pow2 < len) pow2 <<= 1;
+    if (len <= cap) {
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) s[i] = p[i];
+        __syncthreads();
+        bitonic_sort<T>(s, len, pow2);
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) p[i] = s[i];
+    } else {
+        bitonic_sort<T>(p, len, pow2); // in global memory (very long cells only)
+    }
+}
+
+// ----------------------------------------------------------------- query
+
+template <typename T>
+__global__ void k_probe(const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables,
+                        const uint32_t* __restrict__ dir, uint64_t cells, uint32_t shift, uint64_t n,
+                        const typename T::E* __restrict__ entries, uint32_t* __restrict__ r_start,
+                        uint32_t* __restrict__ r_count, unsigned long long* __restrict__ coll) {
+    const uint64_t total = nq * tables;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = i / tables;
+        const uint32_t t = uint32_t(i % tables);
+        const uint64_t key = qkeys[i];
+        const uint32_t* d = dir + uint64_t(t) * (cells + 1);
+        const uint64_t c = key >> shift;
+        uint32_t s = __ldg(d + c);
+        const uint32_t e = __ldg(d + c + 1);
+        const typename T::E* et = entries + uint64_t(t) * n;
+        while (s < e && T::key(et[s]) < key) ++s;
+        uint32_t f = s;
+        while (f < e && T::key(et[f]) == key) ++f;
+        r_start[i] = s;
+        r_count[i] = f - s;
+        if (f > s) atomicAdd(coll + q, (unsigned long long)(f - s));
+    }
+}
+
+template <typename T>
+__global__ void k_gather(uint64_t nq, uint32_t tables, uint64_t n, const typename T::E* __restrict__ entries,
+                         const uint32_t* __restrict__ r_start, const uint32_t* __restrict__ r_count,
+                         const unsigned long long* __restrict__ coll_off, unsigned long long* __restrict__ fill,
+                         uint32_t* __restrict__ cand) {
+    const uint64_t total = nq * tables;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t cnt = r_count[i];
+        if (cnt == 0) continue;
+        const uint64_t q = i / tables;
+        const uint32_t t = uint32_t(i % tables);
+        const uint64_t dst = coll_off[q] + atomicAdd(fill + q, (unsigned long long)cnt);
+        const typename T::E* et = entries + uint64_t(t) * n + r_start[i];
+        for (uint32_t k = 0; k < cnt; ++k) cand[dst + k] = T::id(et[k]);
+    }
+}
+
+// Warp per query over its sorted candidate list.
+__global__ void k_verify(uint64_t nq, const unsigned long long* __restrict__ coll_off, const uint32_t* __restrict__ sorted,
+                         const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words,
+                         uint32_t radius, uint32_t* __restrict__ res_id, uint32_t* __restrict__ res_dist,
+                         unsigned long long* __restrict__ cand_cnt, unsigned long long* __restrict__ found) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
+        const uint64_t beg = coll_off[q], end = coll_off[q + 1];
+        const uint64_t* qr = qrows + q * words;
+        uint64_t ncand = 0, nfound = 0;
+        for (uint64_t base = beg; base < end; base += 32) {
+            const uint64_t k = base + lane;
+            const bool valid = k < end;
+            const uint32_t id = valid ? sorted[k] : 0u;
+            uint32_t prev = __shfl_up_sync(0xffffffffu, id, 1);
+            if (lane == 0 && valid && k > beg) prev = sorted[k - 1];
+            const bool uniq = valid && (k == beg || id != prev);
+            uint32_t dist = 0;
+            if (uniq) {
+                const uint64_t* r = rows + uint64_t(id) * words;
+                for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+            }
+            const bool pass = uniq && dist <= radius;
+            const uint32_t bu = __ballot_sync(0xffffffffu, uniq);
+            const uint32_t bp = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t rank = __popc(bp & ((1u << lane) - 1u));
+                res_id[beg + nfound + rank] = id;
+                res_dist[beg + nfound + rank] = dist;
+            }
+            ncand += __popc(bu);
+            nfound += __popc(bp);
+        }
+        if (lane == 0) {
+            cand_cnt[q] = ncand;
+            found[q] = nfound;
+        }
+    }
+}
+
+__global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ coll_off,
+                          const unsigned long long* __restrict__ res_off, const uint32_t* __restrict__ res_id,
+                          const uint32_t* __restrict__ res_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
+                          uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
+        const uint64_t src = coll_off[q], dst = res_off[q], cnt = res_off[q + 1] - dst;
+        for (uint64_t k = lane; k < cnt; k += 32) {
+            out_q[dst + k] = uint32_t(q);
+            out_id[dst + k] = uint32_t(res_id[src + k] + id_offset);
+            out_dist[dst + k] = res_dist[src + k];
+        }
+    }
+}
+
+uint32_t bit_length(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
+
+unsigned grid_for(uint64_t work, int device, unsigned threads = 256, unsigned per_sm = 8) {
+    const uint64_t want = (work + threads - 1) / threads;
+    return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sm_count(device)) * per_sm)));
+}
+
+template <typename T>
+void build_tables(DeviceIndex& ix, const void* keys, uint32_t t0, uint32_t count, DevBuf& cnt_buf,
+                  DevBuf& cur_buf, DevBuf& big_buf, DevBuf& big_cnt, cudaStream_t s) {
+    using K = typename T::K;
+    const uint64_t n = ix.n, cells = ix.cells();
+    const uint64_t cbytes = uint64_t(count) * (cells + 1) * 4;
+    uint32_t* cnt = static_cast<uint32_t*>(cnt_buf.ensure(cbytes));
+    uint32_t* cur = static_cast<uint32_t*>(cur_buf.ensure(cbytes));
+    uint32_t* dir = ix.dir.as<uint32_t>() + uint64_t(t0) * (cells + 1);
+    auto* entries = static_cast<typename T::E*>(ix.entries.p) + uint64_t(t0) * n;
+    FCLSH_CUDA(cudaMemsetAsync(cnt, 0, cbytes, s));
+    const dim3 g2(std::max<unsigned>(1, grid_for(n, ix.device, 256, 8) / count), count);
+    k_hist<K><<<g2, 256, 0, s>>>(static_cast<const K*>(keys), n, ix.key_shift, cells, cnt);
+    FCLSH_LAUNCHED();
+    k_scan_cells<<<count, 1024, 0, s>>>(cnt, cells, dir, cur);
+    FCLSH_LAUNCHED();
+    k_scatter<T, K><<<g2, 256, 0, s>>>(static_cast<const K*>(keys), n, ix.key_shift, cells, cur, entries);
+    FCLSH_LAUNCHED();
+    // cells longer than kSmallCell: at most n / (kSmallCell+1) per table
+    const uint64_t max_big = uint64_t(count) * (n / (kSmallCell + 1) + 1);
+    uint2* big = static_cast<uint2*>(big_buf.ensure(max_big * sizeof(uint2)));
+    unsigned int* bc = static_cast<unsigned int*>(big_cnt.ensure(sizeof(unsigned int)));
+    FCLSH_CUDA(cudaMemsetAsync(bc, 0, sizeof(unsigned int), s));
+    k_sort_cells<T><<<grid_for(uint64_t(count) * cells, ix.device), 256, 0, s>>>(dir, cells, n, count, entries, big, bc);
+    FCLSH_LAUNCHED();
+    unsigned int nbig = 0;
+    FCLSH_CUDA(cudaMemcpyAsync(&nbig, bc, sizeof(nbig), cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    if (nbig > 0) {
+        const uint32_t cap = uint32_t((96 * 1024) / sizeof(typename T::E));
+        const size_t smem = size_t(cap) * sizeof(typename T::E);
+        FCLSH_CUDA(cudaFuncSetAttribute(k_sort_big<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_sort_big<T><<<nbig, 512, smem, s>>>(dir, cells, n, entries, big, cap);
+        FCLSH_LAUNCHED();
+    }
+}
+
+template <typename T>
+void build_all(DeviceIndex& ix) {
+    using K = typename T::K;
+    const uint64_t n = ix.n, L = ix.fs->tables;
+    const uint32_t kb = sizeof(K);
+    cudaStream_t s = ix.stream;
+    DevBuf keys, cnt, cur, big, bigc;
+    keys.ensure(L * n * kb);
+    // tables per directory chunk: keep one chunk's working set near L2 size
+    const uint64_t per_table = n * (kb + ix.entry_bytes()) + (ix.cells() + 1) * 8;
+    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (64ull << 20) / per_table)));
+    for (uint32_t p = 0; p < ix.fs->parts; ++p) {
+        hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, n, kLayoutTableMajor, s, p, 1);
+        for (uint32_t t = 0; t < L; t += chunk) {
+            const uint32_t c = uint32_t(std::min<uint64_t>(chunk, L - t));
+            build_tables<T>(ix, static_cast<const K*>(keys.p) + uint64_t(t) * n, uint32_t(p * L + t), c, cnt, cur,
+                            big, bigc, s);
+        }
+    }
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
+    using K = typename T::K;
+    QueryOutput out;
+    out.nq = nq;
+    const uint64_t T_ = ix.tables, cells = ix.cells();
+    const uint64_t pairs = nq * T_;
+    K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, pairs) * sizeof(K)));
+    uint32_t* rs = static_cast<uint32_t*>(ix.r_start.ensure(std::max<uint64_t>(1, pairs) * 4));
+    uint32_t* rc = static_cast<uint32_t*>(ix.r_count.ensure(std::max<uint64_t>(1, pairs) * 4));
+    auto* coll = static_cast<unsigned long long*>(ix.coll.ensure((nq + 1) * 8));
+    auto* coll_off = static_cast<unsigned long long*>(ix.coll_off.ensure((nq + 1) * 8));
+    auto* fill = static_cast<unsigned long long*>(ix.fill.ensure((nq + 1) * 8));
+    auto* cand_cnt = static_cast<unsigned long long*>(ix.cand_cnt.ensure((nq + 1) * 8));
+    auto* found = static_cast<unsigned long long*>(ix.found.ensure((nq + 1) * 8));
+    auto* res_off = static_cast<unsigned long long*>(ix.res_off.ensure((nq + 1) * 8));
+    for (auto& e : ix.ev)
+        if (!e) FCLSH_CUDA(cudaEventCreate(&e));
+
+    FCLSH_CUDA(cudaEventRecord(ix.ev[0], s));
+    // S1: hash (point-major: key[q*T + t])
+    if (nq) hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
+    FCLSH_CUDA(cudaEventRecord(ix.ev[1], s));
+    // S2: probe + gather + per-query sort
+    FCLSH_CUDA(cudaMemsetAsync(coll, 0, (nq + 1) * 8, s));
+    FCLSH_CUDA(cudaMemsetAsync(fill, 0, (nq + 1) * 8, s));
+    if (pairs) {
+        k_probe<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, nq, uint32_t(T_), ix.dir.as<uint32_t>(), cells,
+                                                               ix.key_shift, ix.n,
+                                                               static_cast<const typename T::E*>(ix.entries.p), rs, rc, coll);
+        FCLSH_LAUNCHED();
+    }
+    size_t tmp_bytes = 0;
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, coll, coll_off, nq + 1, s));
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, coll, coll_off, nq + 1, s));
+    unsigned long long total_coll = 0;
+    FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + nq, 8, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    uint32_t* cand = static_cast<uint32_t*>(ix.cand.ensure(std::max<uint64_t>(1, total_coll) * 4));
+    uint32_t* sorted = static_cast<uint32_t*>(ix.cand_sorted.ensure(std::max<uint64_t>(1, total_coll) * 4));
+    uint32_t* res_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
+    uint32_t* res_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
+    if (total_coll) {
+        k_gather<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(nq, uint32_t(T_), ix.n,
+                                                                static_cast<const typename T::E*>(ix.entries.p), rs, rc,
+                                                                coll_off, fill, cand);
+        FCLSH_LAUNCHED();
+        size_t sb = 0;
+        FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(nq),
+                                                      coll_off, coll_off + 1, s));
+        FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted, int64_t(total_coll),
+                                                      int64_t(nq), coll_off, coll_off + 1, s));
+    }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
+    // S3: verify + compact
+    if (nq) {
+        k_verify<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, coll_off, sorted, ix.rows.as<uint64_t>(), d_q,
+                                                              ix.row_words, radius, res_id, res_dist, cand_cnt, found);
+        FCLSH_LAUNCHED();
+    }
+    FCLSH_CUDA(cudaMemsetAsync(found + nq, 0, 8, s));
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found, res_off, nq + 1, s));
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found, res_off, nq + 1, s));
+    unsigned long long total = 0;
+    FCLSH_CUDA(cudaMemcpyAsync(&total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(std::max<uint64_t>(1, total) * 4));
+    uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(std::max<uint64_t>(1, total) * 4));
+    uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(std::max<uint64_t>(1, total) * 4));
+    if (total) {
+        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, coll_off, res_off, res_id, res_dist, ix.id_offset,
+                                                               oq, oi, od);
+        FCLSH_LAUNCHED();
+    }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
+    out.total = total;
+    out.d_query = oq;
+    out.d_id = oi;
+    out.d_dist = od;
+    out.d_offsets = reinterpret_cast<uint64_t*>(res_off);
+    out.d_coll = reinterpret_cast<uint64_t*>(coll);
+    out.d_cand = reinterpret_cast<uint64_t*>(cand_cnt);
+    out.d_found = reinterpret_cast<uint64_t*>(found);
+    ix.last_total = total;
+    return out;
+}
+
+} // namespace
+
+DeviceIndex::~DeviceIndex() {
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_device, uint64_t n, uint64_t dims,
+                                         uint32_t radius, const Plan& plan, uint64_t rng_seed,
+                                         const IndexBuildOptions& opt) {
+    // index.cpp:51-53, 78-79
+    if (n == 0) throw UsageError("index: empty dataset");
+    if (dims != plan.dims) throw UsageError("index: dataset width does not match the plan");
+    if (radius != plan.radius) throw UsageError("index: radius does not match the plan");
+    if (plan.table_count() > opt.table_budget) throw ResourceError("index: table count exceeds the budget");
+    if (n + opt.id_offset > (uint64_t(1) << 32)) throw UsageError("index: ids must fit 32 bits");
+
+    auto ix = std::make_unique<DeviceIndex>();
+    ix->device = opt.device;
+    ix->plan = plan;
+    ix->radius = radius;
+    ix->n = n;
+    ix->dims = dims;
+    ix->row_words = uint32_t((dims + 63) / 64);
+    ix->prime = opt.prime;
+    ix->wide = opt.prime > 0xFFFFFFFFull;
+    ix->id_offset = opt.id_offset;
+
+    // families per part from rng.stream("family", p) (index.cpp:83-88)
+    std::vector<Family> fams;
+    Rng rng(rng_seed);
+    for (uint32_t p = 0; p < plan.part_count(); ++p)
+        fams.push_back(build_family(plan.part_dims(p), plan.per_part_radius, -1, rng.stream("family", p).seed(),
+                                    opt.prime, opt.include_zero_column));
+
+    FCLSH_CUDA(cudaSetDevice(opt.device));
+    FCLSH_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    ix->fs = make_device_family_set(plan, std::move(fams), opt.device);
+    ix->tables = ix->fs->total_tables();
+
+    const uint32_t kbits = bit_length(opt.prime - 1);
+    uint32_t b = opt.directory_bits > 0 ? uint32_t(opt.directory_bits)
+                                        : std::max<uint32_t>(1, bit_length(n - 1) > 1 ? bit_length(n - 1) - 1 : 1);
+    b = std::min<uint32_t>({b, kbits, 30u});
+    ix->dir_bits = b;
+    ix->key_shift = kbits - b;
+
+    const uint64_t W = ix->row_words;
+    try {
+        ix->rows.ensure(n * W * 8);
+        ix->entries.ensure(ix->tables * n * ix->entry_bytes());
+        ix->dir.ensure(ix->tables * (ix->cells() + 1) * 4);
+    } catch (const CudaError& e) {
+        throw ResourceError(std::string("index: device memory exhausted (") + e.what() + ")");
+    }
+    FCLSH_CUDA(cudaMemcpyAsync(ix->rows.p, rows, n * W * 8,
+                               rows_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ix->stream));
+    cudaEvent_t e0, e1;
+    FCLSH_CUDA(cudaEventCreate(&e0));
+    FCLSH_CUDA(cudaEventCreate(&e1));
+    FCLSH_CUDA(cudaEventRecord(e0, ix->stream));
+    if (ix->wide)
+        build_all<WideEntry>(*ix);
+    else
+        build_all<NarrowEntry>(*ix);
+    FCLSH_CUDA(cudaEventRecord(e1, ix->stream));
+    FCLSH_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ix->build_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ix;
+}
+
+QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream) {
+    if (radius > ix.radius) // index.cpp:147-153
+        throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
+                         std::to_string(ix.radius));
+    FCLSH_CUDA(cudaSetDevice(ix.device));
+    cudaStream_t s = stream ? stream : ix.stream;
+    QueryOutput o = ix.wide ? query_impl<WideEntry>(ix, d_q, nq, radius, s)
+                            : query_impl<NarrowEntry>(ix, d_q, nq, radius, s);
+    float a = 0, b = 0, c = 0;
+    FCLSH_CUDA(cudaEventSynchronize(ix.ev[3]));
+    cudaEventElapsedTime(&a, ix.ev[0], ix.ev[1]);
+    cudaEventElapsedTime(&b, ix.ev[1], ix.ev[2]);
+    cudaEventElapsedTime(&c, ix.ev[2], ix.ev[3]);
+    ix.t_hash_ms = a;
+    ix.t_probe_ms = b;
+    ix.t_verify_ms = c;
+    return o;
+}
+
+} // namespace fclsh_b200

@@ -1,0 +1,77 @@
+// K2 table build and K3-K5 query (reference: build_index, index.cpp:49-119;
+// PostingTable, posting.cpp:9-21; query_r_nn, index.cpp:125-188).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "hash.cuh"
+#include "host.hpp"
+
+namespace fclsh_b200 {
+
+// Device layout of one shard's index:
+//   rows     n x W u64            the shard's points (verify reads them)
+//   entries  T x n                per table, (key, id) sorted by (key, id):
+//                                 u64 (key << 32 | id) when prime < 2^32,
+//                                 else {u64 key, u64 id} pairs
+//   dir      T x (D + 1) u32      per table, CSR offsets of D = 2^b key
+//                                 cells (cell = key >> shift): the entries
+//                                 with key in cell c are [dir[c], dir[c+1])
+struct DeviceIndex {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    Plan plan;
+    uint32_t radius = 0;
+    uint64_t n = 0, dims = 0;
+    uint32_t row_words = 0;
+    uint64_t prime = 0;
+    bool wide = false;        // 16-byte entries (prime >= 2^32)
+    uint64_t tables = 0;      // T
+    uint32_t dir_bits = 0;    // b
+    uint32_t key_shift = 0;   // cell = key >> key_shift
+    uint64_t id_offset = 0;
+    double build_ms = 0;
+    std::unique_ptr<DeviceFamilySet> fs;
+    DevBuf rows, entries, dir;
+
+    // query workspace (grow-only)
+    DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, fill, cand, cand_sorted, cand_cnt,
+        found, res_off, res_tmp_id, res_tmp_dist, out_q, out_id, out_dist, cub_tmp;
+    uint64_t last_total = 0;
+    double t_hash_ms = 0, t_probe_ms = 0, t_verify_ms = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    ~DeviceIndex();
+    uint64_t cells() const { return uint64_t(1) << dir_bits; }
+    uint64_t entry_bytes() const { return wide ? 16 : 8; }
+    uint64_t device_bytes() const { return rows.bytes + entries.bytes + dir.bytes; }
+};
+
+struct IndexBuildOptions {
+    uint64_t prime = kMersenne61;
+    bool include_zero_column = false;
+    uint64_t table_budget = kDefaultTableBudget;
+    int device = 0;
+    uint64_t id_offset = 0;
+    int directory_bits = 0;
+};
+
+// build_index(data, covering_batch, radius, plan, Rng(rng_seed), opt).
+std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_device, uint64_t n,
+                                         uint64_t dims, uint32_t radius, const Plan& plan,
+                                         uint64_t rng_seed, const IndexBuildOptions& opt);
+
+struct QueryOutput {
+    uint64_t nq = 0, total = 0;
+    uint32_t *d_query = nullptr, *d_id = nullptr, *d_dist = nullptr;
+    uint64_t *d_offsets = nullptr, *d_coll = nullptr, *d_cand = nullptr, *d_found = nullptr;
+};
+
+// query_r_nn for nq device rows; results in index-owned device buffers.
+QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
+                         cudaStream_t stream);
+
+} // namespace fclsh_b200

@@ -1,0 +1,431 @@
+"""Reference-shaped Python API over the C-ABI (include/fclsh_gpu.h).
+
+Names, argument meaning and error classes follow the reference library
+(/root/reference/proj/include/fclsh/*.hpp) so that parity tests read like its
+own tests:
+
+    build_covering_family / make_covering_family   covering.hpp:55-66
+    hash_batch  (hash_batch_into for many rows)    covering.hpp:83-84
+    make_plan / PlanOverride / PlanKind            transform.hpp:24-59
+    build_index / IndexSet.query_r_nn              index.hpp:70-79
+    UsageError / DataError / ResourceError         errors.hpp:8-29
+
+An ``Rng&`` argument of the reference is passed as the Rng's seed (its
+sub-streams depend on the seed only, rng.cpp:31-37). Rows are numpy uint64
+arrays [n, ceil(d/64)] (BitVector word layout) or, for the device entry
+points, CUDA tensors of dtype int64/uint64 with the same layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+M61 = (1 << 61) - 1  # kMersenne61, modmath.hpp:10
+M31 = (1 << 31) - 1
+DEFAULT_TABLE_BUDGET = 1 << 21  # transform.hpp:52
+
+
+class FclshError(RuntimeError):
+    code = 1
+
+
+class UsageError(FclshError):
+    code = 2
+
+
+class DataError(FclshError):
+    code = 3
+
+
+class ResourceError(FclshError):
+    code = 4
+
+
+class CudaRuntimeError(FclshError):
+    code = 5
+
+
+_ERRORS = {2: UsageError, 3: DataError, 4: ResourceError, 5: CudaRuntimeError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = N.lib().fclsh_last_error().decode()
+        raise _ERRORS.get(rc, FclshError)(msg)
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def _ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def words_for(dims: int) -> int:
+    return (dims + 63) // 64
+
+
+def rng_stream(seed: int, label: str, index: int | None = None) -> int:
+    """Seed of Rng(seed).stream(label[, index]) (rng.cpp:31-37)."""
+    L = N.lib()
+    if index is None:
+        return int(L.fclsh_rng_stream(seed, label.encode()))
+    return int(L.fclsh_rng_stream_index(seed, label.encode(), index))
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    _check(N.lib().fclsh_device_count(C.byref(c)))
+    return c.value
+
+
+class ConstructionKind(enum.IntEnum):  # covering.hpp:21
+    general = 0
+    specific = 1
+
+
+class PlanKind(enum.IntEnum):  # transform.hpp:24
+    identity = 0
+    replicate = 1
+    partition = 2
+
+
+@dataclass
+class PlanOverride:  # transform.hpp:46-50
+    kind: PlanKind
+    t: int = 1
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:  # pragma: no cover - torch is always present in this image
+            return C.c_void_p(0)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class CoveringFamily:
+    """CoveringFamily (covering.hpp:34-43), host-built, device-uploaded lazily."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        info = N.FamilyInfo()
+        _check(N.lib().fclsh_family_info_get(self._h, C.byref(info)))
+        self.dims = int(info.dims)
+        self.radius = int(info.radius)
+        self.kind = ConstructionKind(info.kind)
+        self.prime = int(info.prime)
+        self._mapping = None
+        self._seeds = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().fclsh_family_destroy(h)
+            self._h = None
+
+    def code_order(self) -> int:
+        return 1 << (self.radius + 1)
+
+    def table_count(self) -> int:
+        return self.code_order() - 1
+
+    def _export(self):
+        m = np.zeros(self.dims, np.uint32)
+        s = np.zeros(self.dims, np.uint64)
+        _check(N.lib().fclsh_family_export(self._h, _ptr(m, N.u32p), _ptr(s, N.u64p)))
+        self._mapping, self._seeds = m, s
+
+    @property
+    def mapping(self) -> np.ndarray:
+        if self._mapping is None:
+            self._export()
+        return self._mapping
+
+    @property
+    def seeds(self) -> np.ndarray:
+        if self._seeds is None:
+            self._export()
+        return self._seeds
+
+
+def build_covering_family(dims: int, radius: int, rng_seed: int, kind: ConstructionKind | None = None,
+                          prime: int = M61, include_zero_column: bool = False) -> CoveringFamily:
+    """build_covering_family (covering.cpp:40-80); kind None derives it from the widths."""
+    h = C.c_void_p()
+    k = -1 if kind is None else int(kind)
+    _check(N.lib().fclsh_family_build(dims, radius, k, rng_seed, prime, int(include_zero_column), C.byref(h)))
+    return CoveringFamily(h)
+
+
+def make_covering_family(dims: int, radius: int, kind: ConstructionKind, mapping, seeds,
+                         prime: int = M61) -> CoveringFamily:
+    """make_covering_family (covering.cpp:84-111)."""
+    m = np.ascontiguousarray(mapping, dtype=np.uint32)
+    s = _u64(seeds)
+    if m.size != dims or s.size != dims:
+        raise UsageError("covering family: mapping/seeds must have one entry per dimension")
+    h = C.c_void_p()
+    _check(N.lib().fclsh_family_make(dims, radius, int(kind), _ptr(m, N.u32p), _ptr(s, N.u64p), prime,
+                                     C.byref(h)))
+    return CoveringFamily(h)
+
+
+def hash_batch(family: CoveringFamily, rows, device: int = 0, key_bytes: int | None = None) -> np.ndarray:
+    """hash_batch_into for every row: keys [n, L] (point-major), via the GPU.
+
+    key_bytes defaults to 4 when the prime fits 32 bits (uint32 result), else 8.
+    """
+    r = _u64(rows)
+    if r.ndim == 1:
+        r = r.reshape(1, -1)
+    n, w = r.shape
+    kb = key_bytes or (4 if family.prime < (1 << 32) else 8)
+    out = np.zeros((n, family.table_count()), np.uint32 if kb == 4 else np.uint64)
+    _check(N.lib().fclsh_hash_batch_host(family._h, _ptr(r, N.u64p), n, w, out.ctypes.data_as(C.c_void_p), kb,
+                                         device))
+    return out
+
+
+def hash_batch_device(family: CoveringFamily, rows, keys, *, layout: int = 0, key_stride: int | None = None,
+                      device: int | None = None, stream=None) -> None:
+    """Device-buffer hash: rows / keys are CUDA tensors (rows int64/uint64 [n, W];
+    keys int32/uint32 or int64/uint64). layout 0 = table-major, 1 = point-major."""
+    n = rows.shape[0]
+    kb = keys.element_size()
+    stride = key_stride if key_stride is not None else (n if layout == 0 else family.table_count())
+    dev = rows.device.index if device is None else device
+    _check(N.lib().fclsh_hash_batch(family._h, C.c_void_p(rows.data_ptr()), n, rows.shape[1],
+                                    C.c_void_p(keys.data_ptr()), kb, stride, layout, dev or 0, _stream_ptr(stream)))
+
+
+class PreprocessPlan:
+    """PreprocessPlan (transform.hpp:26-44)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = N.PlanInfo()
+        _check(N.lib().fclsh_plan_info_get(self._h, C.byref(info)))
+        self.kind = PlanKind(info.kind)
+        self.dims = int(info.dims)
+        self.radius = int(info.radius)
+        self.t = int(info.t)
+        self.per_part_radius = int(info.per_part_radius)
+        self._part_count = int(info.part_count)
+        self._table_count = int(info.table_count)
+        perm = np.zeros(max(self.dims, 1), np.uint32)
+        parts = np.zeros(2 * max(self.t, 1), np.uint64)
+        _check(N.lib().fclsh_plan_export(self._h, _ptr(perm, N.u32p), _ptr(parts, N.u64p)))
+        if self.kind == PlanKind.partition:
+            self.permutation = perm[: self.dims]
+            self.parts = [(int(parts[2 * i]), int(parts[2 * i + 1])) for i in range(self.t)]
+        else:
+            self.permutation = np.zeros(0, np.uint32)
+            self.parts = []
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().fclsh_plan_destroy(h)
+            self._h = None
+
+    def part_count(self) -> int:
+        return self._part_count
+
+    def part_dims(self, p: int) -> int:
+        if self.kind == PlanKind.partition:
+            b, e = self.parts[p]
+            return e - b
+        return self.dims * self.t if self.kind == PlanKind.replicate else self.dims
+
+    def table_count(self) -> int:  # plan_table_count (transform.cpp:155-158)
+        return self._table_count
+
+
+def make_plan(dims: int, radius: int, c: float, n: int, rng_seed: int, force: PlanOverride | None = None,
+              table_budget: int = DEFAULT_TABLE_BUDGET) -> PreprocessPlan:
+    """make_plan (transform.cpp:32-113)."""
+    h = C.c_void_p()
+    fp = None
+    if force is not None:
+        fp = C.byref(N.PlanOverride(int(force.kind), int(force.t)))
+    _check(N.lib().fclsh_plan_make(dims, radius, float(c), n, rng_seed, fp, table_budget, C.byref(h)))
+    return PreprocessPlan(h)
+
+
+@dataclass
+class QueryResults:
+    """query_r_nn over a batch: per-query ids (ascending) + QueryReport counters."""
+    query: np.ndarray       # uint32 [total]
+    id: np.ndarray          # uint32 [total]
+    distance: np.ndarray    # uint32 [total]
+    offsets: np.ndarray     # uint64 [nq+1]
+    collisions: np.ndarray  # uint64 [nq]
+    candidates: np.ndarray  # uint64 [nq]
+    found: np.ndarray       # uint64 [nq]
+    time_s1_ms: float = 0.0
+    time_s2_ms: float = 0.0
+    time_s3_ms: float = 0.0
+
+    def ids(self, q: int) -> np.ndarray:
+        return self.id[int(self.offsets[q]): int(self.offsets[q + 1])]
+
+    def triples(self) -> np.ndarray:
+        return np.stack([self.query, self.id, self.distance], axis=1)
+
+
+@dataclass
+class DeviceQueryResults:
+    nq: int
+    total: int
+    d_query: int
+    d_id: int
+    d_distance: int
+    d_offsets: int
+    d_collisions: int
+    d_candidates: int
+    d_found: int
+
+
+class IndexSet:
+    """IndexSet (index.hpp:42-52) resident on one GPU."""
+
+    def __init__(self, handle, plan: PreprocessPlan):
+        self._h = handle
+        self.plan = plan
+        info = N.IndexInfo()
+        _check(N.lib().fclsh_index_info_get(self._h, C.byref(info)))
+        self.n = int(info.n)
+        self.dims = int(info.dims)
+        self.radius = int(info.radius)
+        self._tables = int(info.table_count)
+        self._entries = int(info.entry_count)
+        self.directory_bits = int(info.directory_bits)
+        self.device_bytes = int(info.device_bytes)
+        self.build_ms = float(info.build_ms)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().fclsh_index_destroy(h)
+            self._h = None
+
+    def table_count(self) -> int:
+        return self._tables
+
+    def entry_count(self) -> int:
+        return self._entries
+
+    def family(self, part: int) -> CoveringFamily:
+        h = C.c_void_p()
+        _check(N.lib().fclsh_index_family(self._h, part, C.byref(h)))
+        return CoveringFamily(h)
+
+    def query_r_nn(self, q_rows, radius: int) -> QueryResults:
+        """query_r_nn (index.cpp:157-188) for every row of q_rows (host)."""
+        q = _u64(q_rows)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        nq = q.shape[0]
+        if nq and q.shape[1] != words_for(self.dims):
+            raise UsageError("query width does not match the index")
+        rp = C.POINTER(N.Result)()
+        _check(N.lib().fclsh_query(self._h, _ptr(q, N.u64p), nq, radius, C.byref(rp)))
+        try:
+            r = rp.contents
+            tot = int(r.total)
+
+            def arr(p, cnt, dt):
+                if cnt == 0:
+                    return np.zeros(0, dt)
+                return np.ctypeslib.as_array(p, shape=(cnt,)).copy().astype(dt, copy=False)
+
+            res = QueryResults(arr(r.query, tot, np.uint32), arr(r.id, tot, np.uint32), arr(r.distance, tot, np.uint32),
+                               arr(r.offsets, nq + 1, np.uint64), arr(r.collisions, nq, np.uint64),
+                               arr(r.candidates, nq, np.uint64), arr(r.found, nq, np.uint64),
+                               float(r.time_hash_ms), float(r.time_probe_ms), float(r.time_verify_ms))
+        finally:
+            N.lib().fclsh_result_free(rp)
+        return res
+
+    def query_device(self, q_rows, radius: int, stream=None) -> DeviceQueryResults:
+        """Device rows in (CUDA tensor), device results out (index-owned buffers)."""
+        out = N.DeviceResult()
+        _check(N.lib().fclsh_query_device(self._h, C.c_void_p(q_rows.data_ptr()), q_rows.shape[0], radius,
+                                          _stream_ptr(stream), C.byref(out)))
+        return DeviceQueryResults(int(out.nq), int(out.total), out.d_query or 0, out.d_id or 0,
+                                  out.d_distance or 0, out.d_offsets or 0, out.d_collisions or 0,
+                                  out.d_candidates or 0, out.d_found or 0)
+
+
+def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, prime: int = M61,
+                include_zero_column: bool = False, table_budget: int = DEFAULT_TABLE_BUDGET, device: int = 0,
+                id_offset: int = 0, directory_bits: int = 0, dims: int | None = None) -> IndexSet:
+    """build_index(data, Method::covering_batch, radius, plan, Rng(rng_seed), IndexOptions{...})
+    (index.cpp:49-119). data_rows: numpy uint64 [n, W] or a CUDA tensor."""
+    opt = N.IndexOptions()
+    N.lib().fclsh_index_options_default(C.byref(opt))
+    opt.prime = prime
+    opt.include_zero_column = int(include_zero_column)
+    opt.table_budget = table_budget
+    opt.device = device
+    opt.id_offset = id_offset
+    opt.directory_bits = directory_bits
+    d = plan.dims if dims is None else dims
+    h = C.c_void_p()
+    if hasattr(data_rows, "data_ptr"):  # torch tensor on the device
+        n = data_rows.shape[0] if data_rows.ndim == 2 else 0
+        ptr = C.c_void_p(data_rows.data_ptr())
+        on_dev = 1 if data_rows.is_cuda else 0
+        if not data_rows.is_cuda:
+            data_rows = data_rows.contiguous()
+        _check(N.lib().fclsh_index_build(ptr, on_dev, n, d, radius, plan._h, rng_seed, C.byref(opt), C.byref(h)))
+    else:
+        r = _u64(data_rows)
+        n = r.shape[0] if r.ndim == 2 else 0
+        if n and r.shape[1] != words_for(d):
+            raise UsageError("index: dataset width does not match the plan")
+        _check(N.lib().fclsh_index_build(r.ctypes.data_as(C.c_void_p), 0, n, d, radius, plan._h, rng_seed,
+                                         C.byref(opt), C.byref(h)))
+    return IndexSet(h, plan)
+
+
+def launch_count() -> int:
+    return int(N.lib().fclsh_launch_count())
+
+
+def launch_count_reset() -> None:
+    N.lib().fclsh_launch_count_reset()
+
+
+# ------------------------------------------------------------------ workloads
+
+def gen_bernoulli(seed: int, n: int, dims: int, threads: int = 8) -> np.ndarray:
+    out = np.zeros((n, words_for(dims)), np.uint64)
+    _check(N.lib().fclsh_gen_bernoulli(seed, n, dims, _ptr(out, N.u64p), threads))
+    return out
+
+
+def gen_clustered(seed: int, centres: int, n: int, dims: int, flip_p: float, threads: int = 8) -> np.ndarray:
+    out = np.zeros((n, words_for(dims)), np.uint64)
+    _check(N.lib().fclsh_gen_clustered(seed, centres, n, dims, float(flip_p), _ptr(out, N.u64p), threads))
+    return out
+
+
+def gen_planted(seed: int, data: np.ndarray, dims: int, nq: int, kmax: int):
+    d = _u64(data)
+    out = np.zeros((nq, words_for(dims)), np.uint64)
+    src = np.zeros(nq, np.uint32)
+    _check(N.lib().fclsh_gen_planted(seed, _ptr(d, N.u64p), d.shape[0], dims, nq, kmax, _ptr(out, N.u64p),
+                                     _ptr(src, N.u32p)))
+    return out, src

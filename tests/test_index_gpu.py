@@ -1,0 +1,120 @@
+"""K2-K5 parity on the GPU: build_index + query_r_nn through the C-ABI must
+return the oracle's ids and QueryReport counters (collisions, candidates,
+found) for every query, and the (query, id, distance) triples of
+scan_truth (workload.cpp:56-71)."""
+import numpy as np
+import pytest
+
+from paper_1602_02620_b200 import fclsh as F
+from tests.helpers import planted_queries, random_rows
+
+pytestmark = pytest.mark.gpu
+
+M31, M61 = F.M31, F.M61
+
+
+def check_against_oracle(oracle, rows, q, d, radius, override, prime, plan_seed=11, index_seed=22, qradius=None,
+                         directory_bits=0):
+    qradius = radius if qradius is None else qradius
+    force = F.PlanOverride(F.PlanKind(override[0]), override[1])
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], plan_seed, force)
+    ix = F.build_index(rows, radius, plan, index_seed, prime=prime, directory_bits=directory_bits)
+    assert ix.table_count() == plan.table_count()
+    assert ix.entry_count() == plan.table_count() * rows.shape[0]
+    res = ix.query_r_nn(q, qradius)
+    oi = oracle.index_build(rows, d, radius, plan_seed, index_seed, override=override, prime=prime, threads=4)
+    counters, offsets, ids = oi.query(q, qradius, threads=4)
+    got_counters = np.stack([res.collisions, res.candidates, res.found], axis=1)
+    bad = np.argwhere((got_counters != counters).any(1)).ravel()
+    assert bad.size == 0, f"counter mismatch at queries {bad[:8].tolist()}: got {got_counters[bad[:3]].tolist()} " \
+                          f"want {counters[bad[:3]].tolist()}"
+    assert (res.offsets == offsets).all()
+    assert (res.id == ids).all()
+    truth = oracle.scan_truth(rows, q, d, qradius, threads=4)
+    assert (res.triples() == truth).all()
+    return res
+
+
+@pytest.mark.parametrize("override,radius", [((0, 1), 3), ((0, 1), 4), ((2, 2), 8), ((1, 2), 3), ((2, 3), 9)])
+def test_small_indexes_match_oracle(oracle, override, radius):
+    rng = np.random.default_rng(radius * 10 + override[0])
+    d = 128
+    rows = random_rows(rng, 3000, d)
+    q = planted_queries(rng, rows, d, 120, radius + 2)
+    check_against_oracle(oracle, rows, q, d, radius, override, M31)
+
+
+def test_query_radius_below_index_radius(oracle):
+    rng = np.random.default_rng(3)
+    rows = random_rows(rng, 2000, 64)
+    q = planted_queries(rng, rows, 64, 50, 6)
+    for qr in (0, 1, 3):
+        check_against_oracle(oracle, rows, q, 64, 4, (0, 1), M31, qradius=qr)
+
+
+def test_m61_and_small_prime_indexes(oracle):
+    """Wide (key, id) entries for the reference's default field, and a prime
+    so small that bucket merges are frequent (counter parity under merges)."""
+    rng = np.random.default_rng(61)
+    rows = random_rows(rng, 1500, 96)
+    q = planted_queries(rng, rows, 96, 60, 5)
+    check_against_oracle(oracle, rows, q, 96, 4, (0, 1), M61)
+    check_against_oracle(oracle, rows, q, 96, 4, (2, 2), M61)
+    check_against_oracle(oracle, rows, q, 96, 3, (0, 1), 101)
+
+
+def test_clustered_data_long_cells(oracle):
+    """Duplicate-heavy data: long buckets exercise the CTA-wide cell sort."""
+    cl = F.gen_clustered(5, 20, 6000, 128, 0.02)
+    cl[:500] = cl[0]  # 500 identical rows -> one bucket of >= 500 per table
+    q = F.gen_clustered(5, 20, 6100, 128, 0.02)[6000:]
+    q[:3] = cl[0]
+    res = check_against_oracle(oracle, cl, q, 128, 6, (0, 1), M31)
+    assert res.found.max() >= 500
+
+
+def test_directory_extremes(oracle):
+    """A 2-cell directory (long scans) and a fine one give the same answers."""
+    rng = np.random.default_rng(9)
+    rows = random_rows(rng, 2500, 64)
+    q = planted_queries(rng, rows, 64, 40, 4)
+    for bits in (1, 4, 18):
+        check_against_oracle(oracle, rows, q, 64, 3, (0, 1), M31, directory_bits=bits)
+
+
+def test_edge_queries(oracle):
+    rng = np.random.default_rng(17)
+    rows = random_rows(rng, 1000, 128)
+    plan = F.make_plan(128, 4, 1.0, 1000, 1, F.PlanOverride(F.PlanKind.identity, 1))
+    ix = F.build_index(rows, 4, plan, 2, prime=M31)
+    empty = ix.query_r_nn(np.zeros((0, 2), np.uint64), 4)
+    assert empty.id.size == 0 and empty.offsets.tolist() == [0]
+    one = ix.query_r_nn(rows[5:6], 4)
+    assert 5 in one.ids(0).tolist()
+    with pytest.raises(F.UsageError, match="exceeds the index radius"):
+        ix.query_r_nn(rows[:2], 5)
+    with pytest.raises(F.UsageError, match="width"):
+        ix.query_r_nn(np.zeros((2, 3), np.uint64), 4)
+    with pytest.raises(F.UsageError, match="empty dataset"):
+        F.build_index(np.zeros((0, 2), np.uint64), 4, plan, 2, prime=M31)
+    with pytest.raises(F.UsageError, match="radius does not match"):
+        F.build_index(rows, 3, plan, 2, prime=M31)
+    with pytest.raises(F.ResourceError):
+        F.build_index(rows, 4, plan, 2, prime=M31, table_budget=5)
+
+
+def test_id_offset_shards_reassemble(oracle):
+    """Two shards with id offsets return the single index's answer (counters add)."""
+    rng = np.random.default_rng(21)
+    rows = random_rows(rng, 4000, 128)
+    q = planted_queries(rng, rows, 128, 80, 5)
+    plan = F.make_plan(128, 4, 1.0, 4000, 1, F.PlanOverride(F.PlanKind.identity, 1))
+    full = F.build_index(rows, 4, plan, 2, prime=M31).query_r_nn(q, 4)
+    a = F.build_index(rows[:2500], 4, plan, 2, prime=M31).query_r_nn(q, 4)
+    b = F.build_index(rows[2500:], 4, plan, 2, prime=M31, id_offset=2500).query_r_nn(q, 4)
+    for k in ("collisions", "candidates", "found"):
+        assert (getattr(a, k) + getattr(b, k) == getattr(full, k)).all()
+    merged = []
+    for qi in range(80):
+        merged.extend(a.ids(qi).tolist() + b.ids(qi).tolist())
+    assert merged == full.id.tolist()
