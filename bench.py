@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""fcLSH B200 bench -- one JSON line on rank 0.
+
+Headline workload (BASELINE.json configs[1], "cfg2"): n = 1,000,000 points of
+d = 256 i.i.d. Bernoulli(0.5) bits, r = 8, identity plan, L = 511 tables,
+P = 2^31 - 1 (32-bit keys); 10,000 planted + 1,000 uniform queries. A step is
+one query_r_nn pass over the whole 11,000-query batch (hash -> probe ->
+gather/dedup -> verify -> sorted (query, id, distance) triples + counters).
+`value` = queries/s with the query rows already in HBM; `e2e` = the same
+through the host C-ABI call fclsh_query (pinned host rows in, host results
+out, copies inside the timed region). The step's results are checked against
+the reference CPU path (oracle/_ref) in the same run (`parity`).
+
+Also reported: the fcLSH hash-evaluation microbenchmark (configs[4], "cfg5":
+8M x 1024-bit rows, r = 10, 2047 keys/row written table-major in 1M-row
+chunks) as `hash`, and the index build time as `build`.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU (torchrun): every rank holds its own 1M-point shard (weak scaling:
+the global dataset is N x 1M points), all ranks answer the same query batch
+and rank 0 gathers triples / reduces counters over NCCL
+(paper_1602_02620_b200.cluster).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def hbm_peak():
+    try:
+        p = json.load(open(PEAKS_PATH))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def cpu_reference_queries(cfg, data, queries, radius, threads, sample_q=None):
+    """The reference CPU path (oracle/_ref if compiled, else the C port) on this host:
+    index build (untimed) + query_r_nn on `threads` threads."""
+    from oracle import oracle as O
+    orc = O.best()
+    t0 = time.perf_counter()
+    oi = orc.index_build(data, cfg.dims, cfg.radius, cfg.plan_seed(), cfg.index_seed(),
+                         override=(int(cfg.plan_kind), cfg.t), prime=(1 << 31) - 1, threads=threads)
+    build_s = time.perf_counter() - t0
+    q = queries if sample_q is None else queries[:sample_q]
+    t0 = time.perf_counter()
+    counters, offsets, ids = oi.query(q, radius, threads=threads)
+    wall = time.perf_counter() - t0
+    el = getattr(oi, "last_elapsed", wall) if orc.kind == "reference" else wall
+    return orc, oi, (counters, offsets, ids), q.shape[0] / el, build_s
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's own CPU implementation on the host cores."""
+    if rank != 0:
+        return
+    from paper_1602_02620_b200.configs import CONFIGS, make_data, make_queries
+    cfg = CONFIGS[2]
+    threads = os.cpu_count() or 1
+    data = make_data(cfg, threads)
+    queries = make_queries(cfg, data, threads)
+    from oracle import oracle as O
+    orc = O.best()
+    t0 = time.perf_counter()
+    oi = orc.index_build(data, cfg.dims, cfg.radius, cfg.plan_seed(), cfg.index_seed(),
+                         override=(int(cfg.plan_kind), cfg.t), prime=(1 << 31) - 1, threads=threads)
+    build_s = time.perf_counter() - t0
+    sample = min(queries.shape[0], args.ref_sample)
+    for _ in range(args.warmup):
+        oi.query(queries[:min(sample, 200)], cfg.radius, threads=threads)
+    times = []
+    for k in range(args.steps):
+        lo = (k * sample) % queries.shape[0]
+        q = np.roll(queries, -lo, axis=0)[:sample]
+        t0 = time.perf_counter()
+        oi.query(q, cfg.radius, threads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded Bernoulli(0.5) rows; planted + uniform queries)",
+        "config": config_block(cfg, world),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": orc.kind,
+                         "sample": f"{sample} of the 11,000 cfg2 queries per step against the full 1M-point "
+                                   f"reference index (PostingTable binary search, index built once in "
+                                   f"{build_s:.1f} s, untimed)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "queries/sec at 100% recall (result set == oracle), cfg2"
+
+
+def config_block(cfg, world):
+    return {"workload": "cfg2 (BASELINE configs[1])", "n_per_gpu": cfg.n, "n_total": cfg.n * world, "d": cfg.dims,
+            "r": cfg.radius, "plan": "identity", "tables": cfg.tables, "queries": cfg.queries,
+            "prime": "2^31-1 (32-bit keys)", "l2": "flushed between steps (256 MiB device write)",
+            "parallelism": f"points sharded x{world}, queries replicated, NCCL gather" if world > 1 else "1 GPU"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-hash", action="store_true", help="skip the cfg5 hash microbenchmark")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--hash-points", type=int, default=8_000_000)
+    ap.add_argument("--ref-sample", type=int, default=2000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import torch
+
+    from paper_1602_02620_b200 import fclsh as F
+    from paper_1602_02620_b200.configs import CONFIGS, make_data, make_queries
+    import dataclasses
+
+    dev = local
+    torch.cuda.set_device(dev)
+    threads = os.cpu_count() or 8
+    cfg0 = CONFIGS[2]
+    cfg = dataclasses.replace(cfg0, seed=cfg0.seed + 7919 * rank) if rank else cfg0
+    data = make_data(cfg, threads)
+    data0 = data if rank == 0 else make_data(cfg0, threads)
+    queries = make_queries(cfg0, data0, threads)
+    nq, W = queries.shape
+    hbm, peak_src = hbm_peak()
+
+    # ---------------- build (untimed for the query metric; reported)
+    plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg0.plan_seed(), cfg.override())
+    t0 = time.perf_counter()
+    ix = F.build_index(data, cfg.radius, plan, cfg0.index_seed(), prime=F.M31, device=dev,
+                       id_offset=rank * cfg.n)
+    build_wall = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    q_dev = torch.from_numpy(queries.view(np.int64)).to(f"cuda:{dev}")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{dev}")  # 256 MiB > 126 MB L2
+
+    cluster = None
+    if world > 1:
+        from paper_1602_02620_b200.cluster import ShardedQueryGather
+        cluster = ShardedQueryGather(rank, world, torch.device(f"cuda:{dev}"))
+
+    def step():
+        r = ix.query_device(q_dev, cfg.radius, stream)
+        if cluster is not None:
+            cluster.gather(r)
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    F.launch_count_reset()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stages = []
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clocks:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            r = step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+            stages.append(ix.stage_ms())
+    torch.cuda.synchronize()
+    launches = F.launch_count()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = nq * args.steps / (total_ms / 1e3)
+    stage_avg = {k: statistics.mean(s[k] for s in stages) for k in stages[0]}
+
+    # ---------------- counters of the timed batch (for algorithmic bytes) + parity
+    res = ix.query_r_nn(queries, cfg.radius)
+    coll, cand, found = res.collisions.astype(np.float64), res.candidates.astype(np.float64), \
+        res.found.astype(np.float64)
+    T_ = cfg.tables
+    R = max(32, cfg.dims // 8)
+    algo = {
+        "hash": nq * (cfg.dims / 8 + T_ * 4),
+        "probe": nq * T_ * (32 + 32 + 4 + 8),  # dir sector + entry sector (random) + qkey + range write
+        "gather": coll.sum() * (4 + 4) + nq * T_ * 8,
+        "verify": cand.sum() * (4 + R) + found.sum() * 8 + nq * cfg.dims / 8,
+    }
+    dominant = max(stage_avg, key=stage_avg.get)
+    dom_bytes = algo.get(dominant)
+    roofline = None
+    if dom_bytes is not None:
+        ach = dom_bytes / (stage_avg[dominant] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": dom_bytes}
+    stage_rooflines = {k: {"ms": stage_avg[k], "GB/s": algo[k] / (stage_avg[k] / 1e3) / 1e9,
+                           "frac": algo[k] / (stage_avg[k] / 1e3) / 1e9 / hbm}
+                       for k in algo if stage_avg.get(k, 0) > 0}
+
+    # ---------------- e2e: host C-ABI call with pinned host rows, copies inside the timed region
+    pinned = torch.from_numpy(queries.view(np.int64)).pin_memory()
+    pq = pinned.numpy().view(np.uint64)
+    for _ in range(2):
+        ix.query_r_nn(pq, cfg.radius)
+    e2e_t = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = ix.query_r_nn(pq, cfg.radius)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e = {"value": nq * args.steps / sum(e2e_t), "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
+           "d2h_bytes_per_step": int(rr.id.size * 12 + nq * 3 * 8 + (nq + 1) * 8),
+           "api": "fclsh_query (include/fclsh_gpu.h)"}
+
+    # ---------------- CPU baseline + parity against the reference on the same batch
+    cpu = None
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            orc, oi, (counters, offsets, ids), qps, rbuild = cpu_reference_queries(cfg0, data0, queries, cfg.radius,
+                                                                                   threads)
+            cpu = {"value": qps, "unit": "queries/s", "cores": threads, "kind": orc.kind,
+                   "sample": f"all {nq} cfg2 queries vs the full 1M-point reference index on {threads} threads "
+                             f"(query_r_nn only; index built in {rbuild:.1f} s, untimed)"}
+            if world == 1:
+                parity = bool((np.stack([res.collisions, res.candidates, res.found], 1) == counters).all()
+                              and (res.offsets == offsets).all() and (res.id == ids).all())
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "queries/s", "cores": threads, "kind": "unavailable", "sample": str(e)}
+
+    # ---------------- hash microbenchmark (cfg5)
+    hash_block = None
+    if not args.no_hash:
+        hash_block = bench_hash(F, CONFIGS[5], dev, args, hbm, peak_src, flush, stream, threads)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded Bernoulli(0.5) rows; 10k planted + 1k uniform queries)",
+        "config": config_block(cfg, world),
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
+        "gpu_launches_note": "own kernels only; CUB scan/segmented-sort launches are not counted",
+        "clocks": clocks.summary(), "parity_vs_reference": parity,
+        "stages_ms": stage_avg, "stage_rooflines": stage_rooflines,
+        "counters": {"collisions_mean": float(coll.mean()), "candidates_mean": float(cand.mean()),
+                     "found_total": int(found.sum())},
+        "build": {"device_ms": ix.build_ms, "wall_s": build_wall, "entries": ix.entry_count(),
+                  "device_bytes": ix.device_bytes},
+        "hash": hash_block,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
+    """cfg5: 8M x 1024-bit rows, r = 10 -> 2047 keys per row, table-major in
+    1M-row chunks. Step = all chunks. Algorithmic bytes = rows read once +
+    every key written once = n * (d/8 + L*4)."""
+    import torch
+    n = args.hash_points
+    chunk = min(1_000_000, n)
+    rows = F.gen_bernoulli(cfg5.root(), n, cfg5.dims, threads)
+    fam = F.build_covering_family(cfg5.dims, cfg5.radius, cfg5.index_seed(), prime=F.M31)
+    L = fam.table_count()
+    d_rows = torch.from_numpy(rows.view(np.int64)).to(f"cuda:{dev}")
+    keys = torch.empty((L, chunk), dtype=torch.int32, device=f"cuda:{dev}")
+
+    def step():
+        for c0 in range(0, n, chunk):
+            m = min(chunk, n - c0)
+            F.hash_batch_device(fam, d_rows[c0:c0 + m], keys, layout=0, key_stride=chunk, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    avg = statistics.mean(ms)
+    algo_bytes = n * (cfg5.dims / 8 + L * 4)
+    ach = algo_bytes / (avg / 1e3) / 1e9
+    # spot-check one chunk's first rows against the oracle
+    check = None
+    try:
+        from oracle import oracle as O
+        orc = O.best()
+        m0 = 64
+        F.hash_batch_device(fam, d_rows[:chunk], keys, layout=0, key_stride=chunk, stream=stream)
+        torch.cuda.synchronize()
+        got = keys[:, :m0].cpu().numpy().T.astype(np.uint64)
+        want = orc.hash_batch(fam.mapping, fam.seeds, cfg5.dims, cfg5.radius, F.M31, rows[:m0], kind=int(fam.kind))
+        check = bool((got == want).all())
+    except Exception as e:  # noqa: BLE001
+        check = str(e)
+    return {"metric": "fcLSH hash keys/sec (cfg5: 8M x 1024-bit rows, r=10, L=2047, 32-bit keys)",
+            "value": n * L / (avg / 1e3), "unit": "keys/s", "ms_per_step": avg, "points": n, "chunk": chunk,
+            "roofline": {"bound": "hbm", "kernel": "k_hash_m31<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_step": algo_bytes},
+            "keys_match_oracle_sample": check}
+
+
+if __name__ == "__main__":
+    main()

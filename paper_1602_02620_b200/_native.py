@@ -85,6 +85,7 @@ SIGNATURES = {
     "fclsh_query": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.POINTER(C.POINTER(Result))]),
     "fclsh_result_free": (None, [C.POINTER(Result)]),
     "fclsh_query_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, C.POINTER(DeviceResult)]),
+    "fclsh_query_stage_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
     "fclsh_launch_count": (C.c_uint64, []),
     "fclsh_launch_count_reset": (None, []),
     "fclsh_gen_bernoulli": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]),

@@ -366,6 +366,16 @@ int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, 
     });
 }
 
+int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n) {
+    if (!ix || (!ms && n > 0)) {
+        g_err = "fclsh_query_stage_ms: NULL argument";
+        return -FCLSH_ERR_USAGE;
+    }
+    const int k = std::min(n, DeviceIndex::kStages);
+    for (int i = 0; i < k; ++i) ms[i] = ix->ix->stage_ms[i];
+    return k;
+}
+
 uint64_t fclsh_launch_count(void) { return launch_counter(); }
 void fclsh_launch_count_reset(void) { launch_counter() = 0; }
 

@@ -407,9 +407,11 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                                                static_cast<const typename T::E*>(ix.entries.p), rs, rc, coll);
         FCLSH_LAUNCHED();
     }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
     size_t tmp_bytes = 0;
     FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, coll, coll_off, nq + 1, s));
     FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, coll, coll_off, nq + 1, s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
     unsigned long long total_coll = 0;
     FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + nq, 8, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
@@ -422,22 +424,27 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                                                 static_cast<const typename T::E*>(ix.entries.p), rs, rc,
                                                                 coll_off, fill, cand);
         FCLSH_LAUNCHED();
+    }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
+    if (total_coll) {
         size_t sb = 0;
         FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(nq),
                                                       coll_off, coll_off + 1, s));
         FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted, int64_t(total_coll),
                                                       int64_t(nq), coll_off, coll_off + 1, s));
     }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
     // S3: verify + compact
     if (nq) {
         k_verify<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, coll_off, sorted, ix.rows.as<uint64_t>(), d_q,
                                                               ix.row_words, radius, res_id, res_dist, cand_cnt, found);
         FCLSH_LAUNCHED();
     }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
     FCLSH_CUDA(cudaMemsetAsync(found + nq, 0, 8, s));
     FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found, res_off, nq + 1, s));
     FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found, res_off, nq + 1, s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[7], s));
     unsigned long long total = 0;
     FCLSH_CUDA(cudaMemcpyAsync(&total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
@@ -449,7 +456,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                                                oq, oi, od);
         FCLSH_LAUNCHED();
     }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[8], s));
     out.total = total;
     out.d_query = oq;
     out.d_id = oi;
@@ -546,14 +553,15 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
     cudaStream_t s = stream ? stream : ix.stream;
     QueryOutput o = ix.wide ? query_impl<WideEntry>(ix, d_q, nq, radius, s)
                             : query_impl<NarrowEntry>(ix, d_q, nq, radius, s);
-    float a = 0, b = 0, c = 0;
-    FCLSH_CUDA(cudaEventSynchronize(ix.ev[3]));
-    cudaEventElapsedTime(&a, ix.ev[0], ix.ev[1]);
-    cudaEventElapsedTime(&b, ix.ev[1], ix.ev[2]);
-    cudaEventElapsedTime(&c, ix.ev[2], ix.ev[3]);
-    ix.t_hash_ms = a;
-    ix.t_probe_ms = b;
-    ix.t_verify_ms = c;
+    FCLSH_CUDA(cudaEventSynchronize(ix.ev[DeviceIndex::kStages]));
+    for (int i = 0; i < DeviceIndex::kStages; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ix.ev[i], ix.ev[i + 1]);
+        ix.stage_ms[i] = ms;
+    }
+    ix.t_hash_ms = ix.stage_ms[0];
+    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2] + ix.stage_ms[3] + ix.stage_ms[4];
+    ix.t_verify_ms = ix.stage_ms[5] + ix.stage_ms[6] + ix.stage_ms[7];
     return o;
 }
 

@@ -42,7 +42,11 @@ struct DeviceIndex {
         found, res_off, res_tmp_id, res_tmp_dist, out_q, out_id, out_dist, cub_tmp;
     uint64_t last_total = 0;
     double t_hash_ms = 0, t_probe_ms = 0, t_verify_ms = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // per-kernel device time of the last query: hash, probe, collision scan,
+    // gather, segmented sort, verify, found scan, compaction
+    static constexpr int kStages = 8;
+    double stage_ms[kStages] = {};
+    cudaEvent_t ev[kStages + 1] = {};
 
     ~DeviceIndex();
     uint64_t cells() const { return uint64_t(1) << dir_bits; }

@@ -358,6 +358,16 @@ class IndexSet:
             N.lib().fclsh_result_free(rp)
         return res
 
+    STAGES = ("hash", "probe", "collision_scan", "gather", "segment_sort", "verify", "found_scan", "compact")
+
+    def stage_ms(self) -> dict:
+        """Device time per stage of the last query (CUDA events)."""
+        buf = (C.c_double * 8)()
+        k = N.lib().fclsh_query_stage_ms(self._h, buf, 8)
+        if k < 0:
+            _check(-k)
+        return {name: float(buf[i]) for i, name in enumerate(self.STAGES[:k])}
+
     def query_device(self, q_rows, radius: int, stream=None) -> DeviceQueryResults:
         """Device rows in (CUDA tensor), device results out (index-owned buffers)."""
         out = N.DeviceResult()
