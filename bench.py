@@ -281,10 +281,11 @@ def main():
     T_ = cfg.tables
     R = max(32, cfg.dims // 8)
     algo = {
+        # rows read once + every key written once
         "hash": nq * (cfg.dims / 8 + T_ * 4),
-        "probe": nq * T_ * (32 + 32 + 4 + 8),  # dir sector + entry sector (random) + qkey + range write
-        "gather": coll.sum() * (4 + 4) + nq * T_ * 8,
-        "verify": cand.sum() * (4 + R) + found.sum() * 8 + nq * cfg.dims / 8,
+        # per (query, table): qkey (4 B) + one random directory sector + one random
+        # entry sector; per distinct candidate one row (>= one 32-B sector); results
+        "fused": nq * T_ * (4 + 32 + 32) + cand.sum() * R + found.sum() * 8 + nq * cfg.dims / 8,
     }
     dominant = max(stage_avg, key=stage_avg.get)
     dom_bytes = algo.get(dominant)

@@ -217,9 +217,10 @@ int fclsh_query_device(fclsh_index* ix, const uint64_t* d_q_rows, uint64_t nq, u
                        void* stream, fclsh_device_result* out);
 
 /* Device time (CUDA events, ms) of each stage of the last query on ix:
- * [0] hash (S1) [1] probe [2] collision scan [3] gather [4] per-query sort
- * (S2) [5] verify [6] found scan [7] compaction (S3). Writes min(n, 8)
- * values; returns the number written (negative on error). */
+ * [0] hash (S1) [1] fused probe + dedup + verify (S2+S3, warp per query)
+ * [2] general path for queries that overflowed the fused kernel
+ * [3] found scan [4] compaction. Writes min(n, 5) values; returns the number
+ * written (negative on error). */
 int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n);
 
 /* Number of kernels the library launched on this thread since the last

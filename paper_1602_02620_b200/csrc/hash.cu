@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_hash_m31(const FastParams p) {
             if constexpr (DIRECT) {
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
-                    const uint2 e = fam[g * E + j];
+                    const uint2 e = fam[j * G + g]; // lane-fastest: conflict-free
                     const uint32_t m = 0u - row_bit(myrow, e.x);
                     lo[j] = e.y & m & 0xFFFFu;
                     hi[j] = (e.y >> 16) & m;
@@ -154,11 +154,11 @@ __global__ void __launch_bounds__(256) k_hash_m31(const FastParams p) {
                 uint64_t* sk = xbuf + warp * 32 * E;
 #pragma unroll
                 for (int j = 0; j < E; ++j) sk[j * 32 + lane] = 0ull;
-                const uint2* le = fam + g * p.lane_entries;
+                const uint2* le = fam + g; // entry k of lane g at le[k * G]
                 uint32_t cur = le[0].x >> 24;
                 uint64_t acc = 0;
                 for (uint32_t k = 0; k < p.lane_entries; ++k) {
-                    const uint2 e = le[k];
+                    const uint2 e = le[k * G];
                     const uint32_t col = e.x >> 24;
                     if (col != cur) {
                         sk[cur * 32 + lane] = acc;
@@ -504,7 +504,7 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
                 const Family& f = families[p];
                 for (uint64_t j = 0; j < f.dims; ++j)
                     if (f.mapping[j] != 0)
-                        blob[size_t(p) * N + f.mapping[j]] =
+                        blob[size_t(p) * N + (f.mapping[j] % E) * G + f.mapping[j] / E] =
                             make_uint2(uint32_t(plan.source_bit(p, j)), uint32_t(f.seeds[j]));
             }
         } else {
@@ -530,8 +530,8 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
             blob.assign(size_t(fs->parts) * fs->part_words, make_uint2(uint32_t(E - 1) << 24, 0));
             for (uint32_t p = 0; p < fs->parts; ++p)
                 for (int g = 0; g < G; ++g)
-                    std::copy(lists[p][g].begin(), lists[p][g].end(),
-                              blob.begin() + size_t(p) * fs->part_words + size_t(g) * M);
+                    for (size_t k = 0; k < lists[p][g].size(); ++k) // lane-fastest: conflict-free
+                        blob[size_t(p) * fs->part_words + k * G + g] = lists[p][g][k];
         }
         // shared-memory budget check (227 KB per CTA)
         const uint64_t smem = uint64_t(256) * E * 8 + uint64_t(256 / G) * fs->row_words * 8 +

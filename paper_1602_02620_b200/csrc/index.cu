@@ -211,16 +211,161 @@ __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ d
 
 // ----------------------------------------------------------------- query
 
+// K3+K4+K5 fused, one warp per query (the common path):
+//   probe   each lane probes tables lane, lane+32, ... four at a time (their
+//           key / directory / entry loads in flight together); matching ids
+//           are appended to the warp's shared-memory list; the list length
+//           is the reference's `collisions`;
+//   dedup   warp bitonic sort of the list, adjacent uniques = `candidates`;
+//   verify  XOR+popcount over the full row, dist <= radius = `found`, ids
+//           ascending; results go to the query's slot (slot_cap entries).
+// A query whose list exceeds CAP or whose results exceed slot_cap is queued
+// for the general multi-kernel path (overflow list) and written by it.
+template <typename T, int CAP>
+__global__ void __launch_bounds__(256) k_query_fused(
+    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const uint32_t* __restrict__ dir,
+    uint64_t cells, uint32_t shift, uint64_t n, const typename T::E* __restrict__ entries,
+    const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
+    uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
+    unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
+    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count) {
+    using E = typename T::E;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* cnt_s = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* ids = reinterpret_cast<uint32_t*>(smem) + 8 + warp * CAP;
+    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+    for (uint64_t q = uint64_t(blockIdx.x) * 8 + warp; q < nq; q += nwarps) {
+        if (lane == 0) cnt_s[warp] = 0;
+        __syncwarp();
+        const typename T::K* qk = qkeys + q * tables;
+        for (uint32_t t0 = 0; t0 < tables; t0 += 128) {
+            uint64_t key[4];
+            uint32_t s[4], e[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = t0 + u * 32 + lane;
+                key[u] = t < tables ? uint64_t(qk[t]) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = t0 + u * 32 + lane;
+                if (t < tables) {
+                    const uint32_t* d = dir + uint64_t(t) * (cells + 1) + (key[u] >> shift);
+                    s[u] = __ldg(d);
+                    e[u] = __ldg(d + 1);
+                } else {
+                    s[u] = e[u] = 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (s[u] < e[u]) {
+                    const uint32_t t = t0 + u * 32 + lane;
+                    const E* et = entries + uint64_t(t) * n;
+                    uint32_t a = s[u];
+                    while (a < e[u] && T::key(et[a]) < key[u]) ++a;
+                    uint32_t b = a;
+                    while (b < e[u] && T::key(et[b]) == key[u]) ++b;
+                    if (b > a) {
+                        const uint32_t pos = atomicAdd(cnt_s + warp, b - a);
+                        for (uint32_t k = a; k < b; ++k)
+                            if (pos + (k - a) < CAP) ids[pos + (k - a)] = T::id(et[k]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const uint32_t m = cnt_s[warp];
+        if (m > CAP) {
+            if (lane == 0) overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+            continue;
+        }
+        // dedup: ascending-only bitonic sort of the list (padding = +inf)
+        uint32_t P = 1, lp = 0;
+        while (P < m) {
+            P <<= 1;
+            ++lp;
+        }
+        for (uint32_t i = m + lane; i < P; i += 32) ids[i] = 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t lk = 1; lk <= lp; ++lk) {
+            const uint32_t k = 1u << lk;
+            for (uint32_t i = lane; i < P / 2; i += 32) {
+                const uint32_t blk = i >> (lk - 1), off = i & ((k >> 1) - 1);
+                const uint32_t lo = blk * k + off, hi = blk * k + k - 1 - off;
+                const uint32_t x = ids[lo], y = ids[hi];
+                if (y < x) {
+                    ids[lo] = y;
+                    ids[hi] = x;
+                }
+            }
+            __syncwarp();
+            for (int lj = int(lk) - 2; lj >= 0; --lj) {
+                const uint32_t j = 1u << lj;
+                for (uint32_t i = lane; i < P / 2; i += 32) {
+                    const uint32_t lo = ((i >> lj) << (lj + 1)) + (i & (j - 1)), hi = lo + j;
+                    const uint32_t x = ids[lo], y = ids[hi];
+                    if (y < x) {
+                        ids[lo] = y;
+                        ids[hi] = x;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // verify distinct candidates, results in ascending id order
+        const uint64_t* qr = qrows + q * words;
+        uint32_t ncand = 0, nfound = 0;
+        for (uint32_t base = 0; base < m; base += 32) {
+            const uint32_t k = base + lane;
+            const bool valid = k < m;
+            const uint32_t id = valid ? ids[k] : 0u;
+            const bool uniq = valid && (k == 0 || ids[k - 1] != id);
+            uint32_t dist = 0;
+            if (uniq) {
+                const uint64_t* r = rows + uint64_t(id) * words;
+                for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+            }
+            const bool pass = uniq && dist <= radius;
+            const uint32_t bu = __ballot_sync(0xffffffffu, uniq);
+            const uint32_t bp = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t pos = nfound + __popc(bp & ((1u << lane) - 1u));
+                if (pos < slot_cap) {
+                    tmp_id[q * slot_cap + pos] = id;
+                    tmp_dist[q * slot_cap + pos] = dist;
+                }
+            }
+            ncand += __popc(bu);
+            nfound += __popc(bp);
+        }
+        if (nfound > slot_cap) {
+            if (lane == 0) overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+            continue;
+        }
+        if (lane == 0) {
+            coll_q[q] = m;
+            cand_q[q] = ncand;
+            found_q[q] = nfound;
+            src_pos[q] = q * slot_cap;
+        }
+    }
+}
+
+// General path, for the selected queries qsel[0..ns) (overflow of the fused
+// kernel): probe -> per-selection collision counts; scan; gather; CUB
+// segmented sort; verify.
 template <typename T>
-__global__ void k_probe(const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables,
-                        const uint32_t* __restrict__ dir, uint64_t cells, uint32_t shift, uint64_t n,
+__global__ void k_probe(const typename T::K* __restrict__ qkeys, const uint32_t* __restrict__ qsel, uint64_t ns,
+                        uint32_t tables, const uint32_t* __restrict__ dir, uint64_t cells, uint32_t shift, uint64_t n,
                         const typename T::E* __restrict__ entries, uint32_t* __restrict__ r_start,
                         uint32_t* __restrict__ r_count, unsigned long long* __restrict__ coll) {
-    const uint64_t total = nq * tables;
+    const uint64_t total = ns * tables;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t q = i / tables;
+        const uint64_t s_ = i / tables;
         const uint32_t t = uint32_t(i % tables);
-        const uint64_t key = qkeys[i];
+        const uint64_t key = qkeys[uint64_t(qsel[s_]) * tables + t];
         const uint32_t* d = dir + uint64_t(t) * (cells + 1);
         const uint64_t c = key >> shift;
         uint32_t s = __ldg(d + c);
@@ -231,45 +376,47 @@ __global__ void k_probe(const typename T::K* __restrict__ qkeys, uint64_t nq, ui
         while (f < e && T::key(et[f]) == key) ++f;
         r_start[i] = s;
         r_count[i] = f - s;
-        if (f > s) atomicAdd(coll + q, (unsigned long long)(f - s));
+        if (f > s) atomicAdd(coll + s_, (unsigned long long)(f - s));
     }
 }
 
 template <typename T>
-__global__ void k_gather(uint64_t nq, uint32_t tables, uint64_t n, const typename T::E* __restrict__ entries,
+__global__ void k_gather(uint64_t ns, uint32_t tables, uint64_t n, const typename T::E* __restrict__ entries,
                          const uint32_t* __restrict__ r_start, const uint32_t* __restrict__ r_count,
                          const unsigned long long* __restrict__ coll_off, unsigned long long* __restrict__ fill,
                          uint32_t* __restrict__ cand) {
-    const uint64_t total = nq * tables;
+    const uint64_t total = ns * tables;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t cnt = r_count[i];
         if (cnt == 0) continue;
-        const uint64_t q = i / tables;
+        const uint64_t s_ = i / tables;
         const uint32_t t = uint32_t(i % tables);
-        const uint64_t dst = coll_off[q] + atomicAdd(fill + q, (unsigned long long)cnt);
+        const uint64_t dst = coll_off[s_] + atomicAdd(fill + s_, (unsigned long long)cnt);
         const typename T::E* et = entries + uint64_t(t) * n + r_start[i];
         for (uint32_t k = 0; k < cnt; ++k) cand[dst + k] = T::id(et[k]);
     }
 }
 
-// Warp per query over its sorted candidate list.
-__global__ void k_verify(uint64_t nq, const unsigned long long* __restrict__ coll_off, const uint32_t* __restrict__ sorted,
-                         const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words,
-                         uint32_t radius, uint32_t* __restrict__ res_id, uint32_t* __restrict__ res_dist,
-                         unsigned long long* __restrict__ cand_cnt, unsigned long long* __restrict__ found) {
+// Warp per selected query over its sorted candidate list; writes the query's
+// counters and its results at base + coll_off[s].
+__global__ void k_verify(uint64_t ns, const uint32_t* __restrict__ qsel, const unsigned long long* __restrict__ coll_off,
+                         const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ rows,
+                         const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius, uint64_t base_pos,
+                         uint32_t* __restrict__ res_id, uint32_t* __restrict__ res_dist,
+                         unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
+                         unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
-        const uint64_t beg = coll_off[q], end = coll_off[q + 1];
+    for (uint64_t s_ = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s_ < ns; s_ += warps) {
+        const uint64_t q = qsel[s_];
+        const uint64_t beg = coll_off[s_], end = coll_off[s_ + 1];
         const uint64_t* qr = qrows + q * words;
         uint64_t ncand = 0, nfound = 0;
         for (uint64_t base = beg; base < end; base += 32) {
             const uint64_t k = base + lane;
             const bool valid = k < end;
             const uint32_t id = valid ? sorted[k] : 0u;
-            uint32_t prev = __shfl_up_sync(0xffffffffu, id, 1);
-            if (lane == 0 && valid && k > beg) prev = sorted[k - 1];
-            const bool uniq = valid && (k == beg || id != prev);
+            const bool uniq = valid && (k == beg || sorted[k - 1] != id);
             uint32_t dist = 0;
             if (uniq) {
                 const uint64_t* r = rows + uint64_t(id) * words;
@@ -279,32 +426,46 @@ __global__ void k_verify(uint64_t nq, const unsigned long long* __restrict__ col
             const uint32_t bu = __ballot_sync(0xffffffffu, uniq);
             const uint32_t bp = __ballot_sync(0xffffffffu, pass);
             if (pass) {
-                const uint32_t rank = __popc(bp & ((1u << lane) - 1u));
-                res_id[beg + nfound + rank] = id;
-                res_dist[beg + nfound + rank] = dist;
+                const uint64_t pos = beg + nfound + __popc(bp & ((1u << lane) - 1u));
+                res_id[pos] = id;
+                res_dist[pos] = dist;
             }
             ncand += __popc(bu);
             nfound += __popc(bp);
         }
         if (lane == 0) {
-            cand_cnt[q] = ncand;
-            found[q] = nfound;
+            coll_q[q] = end - beg;
+            cand_q[q] = ncand;
+            found_q[q] = nfound;
+            src_pos[q] = base_pos + beg;
         }
     }
 }
 
-__global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ coll_off,
-                          const unsigned long long* __restrict__ res_off, const uint32_t* __restrict__ res_id,
-                          const uint32_t* __restrict__ res_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
+// Copies every query's results (slot of the fused path, or region of the
+// general path) to its place in the (query, id) ordered output.
+__global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ src_pos,
+                          const unsigned long long* __restrict__ res_off, const uint32_t* __restrict__ tmp_id,
+                          const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len, const uint32_t* __restrict__ tmp2_id,
+                          const uint32_t* __restrict__ tmp2_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
                           uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
-        const uint64_t src = coll_off[q], dst = res_off[q], cnt = res_off[q + 1] - dst;
+        const uint64_t dst = res_off[q], cnt = res_off[q + 1] - dst;
+        if (cnt == 0) continue;
+        uint64_t src = src_pos[q];
+        const uint32_t* ti = tmp_id;
+        const uint32_t* td = tmp_dist;
+        if (src >= tmp_len) {
+            src -= tmp_len;
+            ti = tmp2_id;
+            td = tmp2_dist;
+        }
         for (uint64_t k = lane; k < cnt; k += 32) {
             out_q[dst + k] = uint32_t(q);
-            out_id[dst + k] = uint32_t(res_id[src + k] + id_offset);
-            out_dist[dst + k] = res_dist[src + k];
+            out_id[dst + k] = uint32_t(ti[src + k] + id_offset);
+            out_dist[dst + k] = td[src + k];
         }
     }
 }
@@ -375,22 +536,42 @@ void build_all(DeviceIndex& ix) {
     FCLSH_CUDA(cudaStreamSynchronize(s));
 }
 
+template <typename T, int CAP>
+void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
+                  uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
+                  unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
+                  uint32_t* ovf, unsigned int* ovf_cnt, cudaStream_t s) {
+    auto kern = k_query_fused<T, CAP>;
+    const size_t smem = (8 + size_t(8) * CAP) * 4;
+    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
+    kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), ix.dir.as<uint32_t>(), ix.cells(),
+                                           ix.key_shift, ix.n, static_cast<const typename T::E*>(ix.entries.p),
+                                           ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q,
+                                           found_q, src_pos, tmp_id, tmp_dist, ovf, ovf_cnt);
+    FCLSH_LAUNCHED();
+}
+
 template <typename T>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
     using K = typename T::K;
     QueryOutput out;
     out.nq = nq;
     const uint64_t T_ = ix.tables, cells = ix.cells();
-    const uint64_t pairs = nq * T_;
-    K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, pairs) * sizeof(K)));
-    uint32_t* rs = static_cast<uint32_t*>(ix.r_start.ensure(std::max<uint64_t>(1, pairs) * 4));
-    uint32_t* rc = static_cast<uint32_t*>(ix.r_count.ensure(std::max<uint64_t>(1, pairs) * 4));
-    auto* coll = static_cast<unsigned long long*>(ix.coll.ensure((nq + 1) * 8));
-    auto* coll_off = static_cast<unsigned long long*>(ix.coll_off.ensure((nq + 1) * 8));
-    auto* fill = static_cast<unsigned long long*>(ix.fill.ensure((nq + 1) * 8));
-    auto* cand_cnt = static_cast<unsigned long long*>(ix.cand_cnt.ensure((nq + 1) * 8));
-    auto* found = static_cast<unsigned long long*>(ix.found.ensure((nq + 1) * 8));
+    const bool big = T_ > 600;
+    const uint32_t slot_cap = big ? 128 : 32;
+    K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
+    auto* coll_q = static_cast<unsigned long long*>(ix.coll.ensure((nq + 1) * 8));
+    auto* cand_q = static_cast<unsigned long long*>(ix.cand_cnt.ensure((nq + 1) * 8));
+    auto* found_q = static_cast<unsigned long long*>(ix.found.ensure((nq + 1) * 8));
     auto* res_off = static_cast<unsigned long long*>(ix.res_off.ensure((nq + 1) * 8));
+    auto* src_pos = static_cast<unsigned long long*>(ix.src_pos.ensure((nq + 1) * 8));
+    uint32_t* tmp_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
+    uint32_t* tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
+    uint32_t* ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
+    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(16));
     for (auto& e : ix.ev)
         if (!e) FCLSH_CUDA(cudaEventCreate(&e));
 
@@ -398,53 +579,69 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // S1: hash (point-major: key[q*T + t])
     if (nq) hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
     FCLSH_CUDA(cudaEventRecord(ix.ev[1], s));
-    // S2: probe + gather + per-query sort
-    FCLSH_CUDA(cudaMemsetAsync(coll, 0, (nq + 1) * 8, s));
-    FCLSH_CUDA(cudaMemsetAsync(fill, 0, (nq + 1) * 8, s));
-    if (pairs) {
-        k_probe<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, nq, uint32_t(T_), ix.dir.as<uint32_t>(), cells,
-                                                               ix.key_shift, ix.n,
-                                                               static_cast<const typename T::E*>(ix.entries.p), rs, rc, coll);
-        FCLSH_LAUNCHED();
+    // S2+S3 fused
+    FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 4, s));
+    if (nq) {
+        if (big)
+            launch_fused<T, 2048>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
+                                  tmp_dist, ovf, ovf_cnt, s);
+        else
+            launch_fused<T, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
+                                  tmp_dist, ovf, ovf_cnt, s);
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
-    size_t tmp_bytes = 0;
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, coll, coll_off, nq + 1, s));
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, coll, coll_off, nq + 1, s));
-    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
-    unsigned long long total_coll = 0;
-    FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + nq, 8, cudaMemcpyDeviceToHost, s));
+    unsigned int ns = 0;
+    FCLSH_CUDA(cudaMemcpyAsync(&ns, ovf_cnt, 4, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
-    uint32_t* cand = static_cast<uint32_t*>(ix.cand.ensure(std::max<uint64_t>(1, total_coll) * 4));
-    uint32_t* sorted = static_cast<uint32_t*>(ix.cand_sorted.ensure(std::max<uint64_t>(1, total_coll) * 4));
-    uint32_t* res_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
-    uint32_t* res_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
-    if (total_coll) {
-        k_gather<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(nq, uint32_t(T_), ix.n,
-                                                                static_cast<const typename T::E*>(ix.entries.p), rs, rc,
-                                                                coll_off, fill, cand);
+    uint32_t* tmp2_id = tmp_id;
+    uint32_t* tmp2_dist = tmp_dist;
+    if (ns) {
+        // general path for the overflowing queries
+        const uint64_t pairs = uint64_t(ns) * T_;
+        uint32_t* rs = static_cast<uint32_t*>(ix.r_start.ensure(pairs * 4));
+        uint32_t* rc = static_cast<uint32_t*>(ix.r_count.ensure(pairs * 4));
+        auto* coll_s = static_cast<unsigned long long*>(ix.coll_sel.ensure((ns + 1) * 8));
+        auto* coll_off = static_cast<unsigned long long*>(ix.coll_off.ensure((ns + 1) * 8));
+        auto* fill = static_cast<unsigned long long*>(ix.fill.ensure((ns + 1) * 8));
+        FCLSH_CUDA(cudaMemsetAsync(coll_s, 0, (ns + 1) * 8, s));
+        FCLSH_CUDA(cudaMemsetAsync(fill, 0, (ns + 1) * 8, s));
+        k_probe<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), ix.dir.as<uint32_t>(), cells,
+                                                               ix.key_shift, ix.n,
+                                                               static_cast<const typename T::E*>(ix.entries.p), rs, rc,
+                                                               coll_s);
+        FCLSH_LAUNCHED();
+        size_t tb = 0;
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, coll_s, coll_off, ns + 1, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tb), tb, coll_s, coll_off, ns + 1, s));
+        unsigned long long total_coll = 0;
+        FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + ns, 8, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaStreamSynchronize(s));
+        uint32_t* cand = static_cast<uint32_t*>(ix.cand.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        uint32_t* sorted = static_cast<uint32_t*>(ix.cand_sorted.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        tmp2_id = static_cast<uint32_t*>(ix.res2_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        tmp2_dist = static_cast<uint32_t*>(ix.res2_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        if (total_coll) {
+            k_gather<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(ns, uint32_t(T_), ix.n,
+                                                                    static_cast<const typename T::E*>(ix.entries.p), rs,
+                                                                    rc, coll_off, fill, cand);
+            FCLSH_LAUNCHED();
+            size_t sb = 0;
+            FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(ns),
+                                                          coll_off, coll_off + 1, s));
+            FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted,
+                                                          int64_t(total_coll), int64_t(ns), coll_off, coll_off + 1, s));
+        }
+        k_verify<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
+            ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap, tmp2_id,
+            tmp2_dist, coll_q, cand_q, found_q, src_pos);
         FCLSH_LAUNCHED();
     }
+    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
+    FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
+    size_t tmp_bytes = 0;
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found_q, res_off, nq + 1, s));
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found_q, res_off, nq + 1, s));
     FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
-    if (total_coll) {
-        size_t sb = 0;
-        FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(nq),
-                                                      coll_off, coll_off + 1, s));
-        FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted, int64_t(total_coll),
-                                                      int64_t(nq), coll_off, coll_off + 1, s));
-    }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
-    // S3: verify + compact
-    if (nq) {
-        k_verify<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, coll_off, sorted, ix.rows.as<uint64_t>(), d_q,
-                                                              ix.row_words, radius, res_id, res_dist, cand_cnt, found);
-        FCLSH_LAUNCHED();
-    }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
-    FCLSH_CUDA(cudaMemsetAsync(found + nq, 0, 8, s));
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found, res_off, nq + 1, s));
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found, res_off, nq + 1, s));
-    FCLSH_CUDA(cudaEventRecord(ix.ev[7], s));
     unsigned long long total = 0;
     FCLSH_CUDA(cudaMemcpyAsync(&total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
@@ -452,23 +649,23 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(std::max<uint64_t>(1, total) * 4));
     uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(std::max<uint64_t>(1, total) * 4));
     if (total) {
-        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, coll_off, res_off, res_id, res_dist, ix.id_offset,
-                                                               oq, oi, od);
+        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap,
+                                                               tmp2_id, tmp2_dist, ix.id_offset, oq, oi, od);
         FCLSH_LAUNCHED();
     }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[8], s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
     out.total = total;
     out.d_query = oq;
     out.d_id = oi;
     out.d_dist = od;
     out.d_offsets = reinterpret_cast<uint64_t*>(res_off);
-    out.d_coll = reinterpret_cast<uint64_t*>(coll);
-    out.d_cand = reinterpret_cast<uint64_t*>(cand_cnt);
-    out.d_found = reinterpret_cast<uint64_t*>(found);
+    out.d_coll = reinterpret_cast<uint64_t*>(coll_q);
+    out.d_cand = reinterpret_cast<uint64_t*>(cand_q);
+    out.d_found = reinterpret_cast<uint64_t*>(found_q);
     ix.last_total = total;
+    ix.last_overflow = ns;
     return out;
 }
-
 } // namespace
 
 DeviceIndex::~DeviceIndex() {
@@ -560,8 +757,8 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         ix.stage_ms[i] = ms;
     }
     ix.t_hash_ms = ix.stage_ms[0];
-    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2] + ix.stage_ms[3] + ix.stage_ms[4];
-    ix.t_verify_ms = ix.stage_ms[5] + ix.stage_ms[6] + ix.stage_ms[7];
+    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2]; // probe + dedup + verify are fused
+    ix.t_verify_ms = ix.stage_ms[3] + ix.stage_ms[4];
     return o;
 }
 

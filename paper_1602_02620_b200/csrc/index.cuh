@@ -38,13 +38,16 @@ struct DeviceIndex {
     DevBuf rows, entries, dir;
 
     // query workspace (grow-only)
-    DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, fill, cand, cand_sorted, cand_cnt,
-        found, res_off, res_tmp_id, res_tmp_dist, out_q, out_id, out_dist, cub_tmp;
+    DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, coll_sel, fill, cand, cand_sorted, cand_cnt,
+        found, res_off, src_pos, res_tmp_id, res_tmp_dist, res2_id, res2_dist, overflow, overflow_cnt, out_q, out_id,
+        out_dist, cub_tmp;
     uint64_t last_total = 0;
+    uint64_t last_overflow = 0; // queries that took the general path
     double t_hash_ms = 0, t_probe_ms = 0, t_verify_ms = 0;
-    // per-kernel device time of the last query: hash, probe, collision scan,
-    // gather, segmented sort, verify, found scan, compaction
-    static constexpr int kStages = 8;
+    // device time of the last query per stage: hash (S1), fused
+    // probe+dedup+verify (S2+S3), general path for overflowing queries,
+    // found scan, compaction
+    static constexpr int kStages = 5;
     double stage_ms[kStages] = {};
     cudaEvent_t ev[kStages + 1] = {};
 

@@ -358,7 +358,7 @@ class IndexSet:
             N.lib().fclsh_result_free(rp)
         return res
 
-    STAGES = ("hash", "probe", "collision_scan", "gather", "segment_sort", "verify", "found_scan", "compact")
+    STAGES = ("hash", "fused", "overflow", "found_scan", "compact")
 
     def stage_ms(self) -> dict:
         """Device time per stage of the last query (CUDA events)."""
