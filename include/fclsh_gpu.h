@@ -149,8 +149,18 @@ typedef struct {
     uint64_t table_budget;       /* IndexOptions::table_budget */
     int32_t device;              /* CUDA device ordinal */
     uint64_t id_offset;          /* added to every reported id (shards) */
-    int32_t directory_bits;      /* 0 = automatic */
+    int32_t directory_bits;      /* CSR layout: 0 = automatic */
+    int32_t layout;              /* FCLSH_TABLES_* */
 } fclsh_index_options;
+
+/* Device table layouts (same query results):
+ * BUCKETS  open-addressed buckets of four postings, one random 32-byte read
+ *          per probe, ~16 bytes per posting (default when it fits);
+ * CSR      the reference's sorted posting array + a key-cell directory, two
+ *          random reads per probe, ~10 bytes per posting. */
+#define FCLSH_TABLES_AUTO 0
+#define FCLSH_TABLES_CSR 1
+#define FCLSH_TABLES_BUCKETS 2
 
 void fclsh_index_options_default(fclsh_index_options* o);
 
@@ -169,6 +179,8 @@ typedef struct {
     uint32_t directory_bits;
     uint64_t device_bytes;
     double build_ms; /* device time of the last build, CUDA events */
+    int32_t layout;  /* FCLSH_TABLES_CSR or FCLSH_TABLES_BUCKETS */
+    uint64_t buckets_per_table;
 } fclsh_index_info;
 int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out);
 /* Part p's family (a new handle the caller destroys). */

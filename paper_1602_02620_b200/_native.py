@@ -35,13 +35,14 @@ class PlanInfo(C.Structure):
 
 class IndexOptions(C.Structure):
     _fields_ = [("prime", C.c_uint64), ("include_zero_column", C.c_int32), ("table_budget", C.c_uint64),
-                ("device", C.c_int32), ("id_offset", C.c_uint64), ("directory_bits", C.c_int32)]
+                ("device", C.c_int32), ("id_offset", C.c_uint64), ("directory_bits", C.c_int32),
+                ("layout", C.c_int32)]
 
 
 class IndexInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("dims", C.c_uint64), ("radius", C.c_uint32), ("table_count", C.c_uint64),
                 ("entry_count", C.c_uint64), ("directory_bits", C.c_uint32), ("device_bytes", C.c_uint64),
-                ("build_ms", C.c_double)]
+                ("build_ms", C.c_double), ("layout", C.c_int32), ("buckets_per_table", C.c_uint64)]
 
 
 class Result(C.Structure):

@@ -235,6 +235,7 @@ void fclsh_index_options_default(fclsh_index_options* o) {
     o->device = 0;
     o->id_offset = 0;
     o->directory_bits = 0;
+    o->layout = FCLSH_TABLES_AUTO;
 }
 
 int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint64_t dims, uint32_t radius,
@@ -253,6 +254,7 @@ int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint
         bo.device = o.device;
         bo.id_offset = o.id_offset;
         bo.directory_bits = o.directory_bits;
+        bo.layout = o.layout;
         auto h = std::make_unique<fclsh_index>();
         h->ix = build_index(rows, rows_on_device != 0, n, dims, radius, plan->p, rng_seed, bo);
         *out = h.release();
@@ -272,6 +274,8 @@ int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out) {
         out->directory_bits = d.dir_bits;
         out->device_bytes = d.device_bytes();
         out->build_ms = d.build_ms;
+        out->layout = d.layout;
+        out->buckets_per_table = d.nbuckets;
     });
 }
 

@@ -1,24 +1,39 @@
-// K2 (table build) and K3-K5 (probe, gather + dedup, verify) for sm_100a.
+// K2 (table build) and K3-K5 (probe, dedup, verify) for sm_100a.
 //
-// Build (reference: build_index index.cpp:49-119 + PostingTable::finalize
-// posting.cpp:9-12): for each part, K1 writes the part's L key columns
-// table-major; then per table a counting pass over the top key bits builds
-// the cell directory (CSR offsets), a scatter pass places (key, id) into the
-// cells, and a per-cell sort orders each cell by (key, id) -- so every table
-// ends up exactly as the reference's sorted posting array, plus O(1) cell
-// lookup instead of a binary search. Cells are tiny on i.i.d. data (about
-// two entries); long cells from clustered data go to a CTA-wide sort.
+// Every table of the reference is a PostingTable: (key, id) entries sorted by
+// (key, id), looked up by binary search (posting.cpp:9-21). query_r_nn walks
+// every table's bucket for the query key, counts every posting it touches
+// (`collisions`), keeps the first sighting of each id (`candidates`) and
+// verifies those on the full row (`found`, ids ascending) (index.cpp:157-188).
+// On the GPU the probe is bound by random DRAM accesses, so the device tables
+// are built for one random access per probe:
 //
-// Query (reference: query_r_nn index.cpp:157-188):
-//   S1  K1 hashes the query rows point-major.
-//   S2  K3 probes every (query, table): directory cell -> matching key run;
-//       counts are the reference's `collisions`. K4 gathers the ids of all
-//       runs per query and sorts each query's list (dedup = adjacent
-//       uniques, `candidates`).
-//   S3  K5 verifies each distinct candidate with XOR+popcount over the full
-//       row and keeps dist <= radius (`found`, ids ascending as the
-//       reference's std::sort leaves them); a compaction writes the sorted
-//       (query, id, distance) triples.
+//  kBuckets (default)  open-addressed bucket table per table: 2^bb buckets of
+//      four (key, id) slots, home bucket = key >> shift (keys are uniform in
+//      [0, P)), linear probing into the next bucket, filled slots always a
+//      prefix of the bucket. Load <= 50%, so a probe reads one 32-byte
+//      bucket (64 B for 8-byte keys) and almost never a second. Every
+//      posting with key k sits in the run of full buckets starting at
+//      home(k), so counts are exact.
+//  kCsr  (fallback when memory is tight)  the reference's sorted array plus a
+//      directory of 2^b key cells (CSR offsets): two random accesses per probe,
+//      ~10 bytes per posting instead of ~16.
+//
+// Build: K1 writes one part's L key columns table-major, then per table
+// kBuckets inserts every (key, id) with a CAS into the first free slot of its
+// run; kCsr counts cells, scans, scatters and sorts each cell by (key, id).
+//
+// Query (all queries of a batch at once):
+//   S1  K1 hashes the query rows point-major (key[q*T + t]).
+//   S2+S3  k_query_fused, one warp per query: lanes probe tables lane,
+//       lane+32, ... four at a time, append matching ids to a shared-memory
+//       list (its length = collisions), bitonic-sort it (adjacent uniques =
+//       candidates), verify with XOR+popcount (found, ids ascending) into the
+//       query's result slot.
+//   Queries whose list or result set overflows the fused kernel's capacity
+//   go through the general path (count, scan, gather, CUB segmented sort,
+//   verify); a scan of the per-query found counts and one compaction write
+//   the (query, id, distance) triples ordered by (query, id).
 
 #include "index.cuh"
 
@@ -27,32 +42,115 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace fclsh_b200 {
 
 namespace {
 
-struct NarrowEntry {
+struct NarrowEntry { // key < 2^32: one u64, (key << 32 | id) orders as (key, id)
     using E = unsigned long long;
     using K = uint32_t;
+    static constexpr int kBucketLoads = 2; // 32-byte bucket = 2 x 16 B
     __device__ __forceinline__ static uint64_t key(E e) { return e >> 32; }
     __device__ __forceinline__ static uint32_t id(E e) { return uint32_t(e); }
     __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return (E(k) << 32) | i; }
     __device__ __forceinline__ static bool less(E a, E b) { return a < b; }
-    __device__ __forceinline__ static E maxval() { return ~0ull; }
+    __device__ __forceinline__ static bool empty(E e) { return e == ~0ull; }
+    __host__ __device__ static constexpr unsigned char empty_byte() { return 0xFF; }
+    // claim slot p for e; true if this thread placed it
+    __device__ __forceinline__ static bool claim(E* p, E e) { return atomicCAS(p, ~0ull, e) == ~0ull; }
 };
 
-struct WideEntry {
-    using E = ulonglong2; // x = key, y = id
+struct WideEntry { // 8-byte keys: {key, id}
+    using E = ulonglong2;
     using K = uint64_t;
+    static constexpr int kBucketLoads = 4; // 64-byte bucket
     __device__ __forceinline__ static uint64_t key(E e) { return e.x; }
     __device__ __forceinline__ static uint32_t id(E e) { return uint32_t(e.y); }
     __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return make_ulonglong2(k, i); }
     __device__ __forceinline__ static bool less(E a, E b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
-    __device__ __forceinline__ static E maxval() { return make_ulonglong2(~0ull, ~0ull); }
+    __device__ __forceinline__ static bool empty(E e) { return e.x == ~0ull; }
+    __host__ __device__ static constexpr unsigned char empty_byte() { return 0xFF; }
+    __device__ __forceinline__ static bool claim(E* p, E e) {
+        if (atomicCAS(&p->x, ~0ull, e.x) != ~0ull) return false;
+        p->y = e.y; // the slot is ours; nobody reads it before the build ends
+        return true;
+    }
 };
 
+constexpr int kSlots = 4; // per bucket
+
+// Read-only view of one shard's tables, passed by value to the kernels.
+template <typename T>
+struct Tables {
+    const typename T::E* data; // entries (CSR) or buckets (kBuckets)
+    const uint32_t* dir;       // CSR only
+    uint64_t n;                // postings per table
+    uint64_t cells;            // CSR cells per table
+    uint64_t nbuckets;         // buckets per table
+    uint32_t shift;            // CSR: cell = key >> shift; buckets: home = key >> shift
+};
+
+// Calls on_id(id) for every posting of table t with this key; returns the count.
+template <typename T, int LAYOUT, typename F>
+__device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, uint64_t key, F&& on_id) {
+    using E = typename T::E;
+    uint32_t cnt = 0;
+    if constexpr (LAYOUT == kLayoutCsr) {
+        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key >> tb.shift);
+        uint32_t a = __ldg(d);
+        const uint32_t e = __ldg(d + 1);
+        const E* et = tb.data + uint64_t(t) * tb.n;
+        while (a < e && T::key(et[a]) < key) ++a;
+        while (a < e && T::key(et[a]) == key) {
+            on_id(T::id(et[a]));
+            ++a;
+            ++cnt;
+        }
+    } else {
+        uint64_t b = key >> tb.shift;
+        const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
+        for (;;) {
+            const E* bp = base + b * kSlots;
+            E s[kSlots];
+#pragma unroll
+            for (int j = 0; j < kSlots; ++j) s[j] = bp[j];
+#pragma unroll
+            for (int j = 0; j < kSlots; ++j)
+                if (!T::empty(s[j]) && T::key(s[j]) == key) {
+                    on_id(T::id(s[j]));
+                    ++cnt;
+                }
+            if (T::empty(s[kSlots - 1])) break;
+            b = (b + 1) & (tb.nbuckets - 1);
+        }
+    }
+    return cnt;
+}
+
 // ----------------------------------------------------------------- build
+
+template <typename T>
+__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t nbuckets,
+                                typename T::E* __restrict__ buckets) {
+    const uint32_t t = blockIdx.y;
+    const typename T::K* kt = keys + uint64_t(t) * n;
+    typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t key = kt[i];
+        const typename T::E e = T::make(key, uint32_t(i));
+        uint64_t b = key >> shift;
+        for (;;) {
+            typename T::E* bp = bt + b * kSlots;
+            bool done = false;
+#pragma unroll
+            for (int j = 0; j < kSlots && !done; ++j) done = T::claim(bp + j, e);
+            if (done) break;
+            b = (b + 1) & (nbuckets - 1);
+        }
+    }
+}
 
 template <typename K>
 __global__ void k_hist(const K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t cells,
@@ -211,20 +309,12 @@ __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ d
 
 // ----------------------------------------------------------------- query
 
-// K3+K4+K5 fused, one warp per query (the common path):
-//   probe   each lane probes tables lane, lane+32, ... four at a time (their
-//           key / directory / entry loads in flight together); matching ids
-//           are appended to the warp's shared-memory list; the list length
-//           is the reference's `collisions`;
-//   dedup   warp bitonic sort of the list, adjacent uniques = `candidates`;
-//   verify  XOR+popcount over the full row, dist <= radius = `found`, ids
-//           ascending; results go to the query's slot (slot_cap entries).
-// A query whose list exceeds CAP or whose results exceed slot_cap is queued
-// for the general multi-kernel path (overflow list) and written by it.
-template <typename T, int CAP>
+// K3+K4+K5 fused, one warp per query (the common path). A query whose list
+// exceeds CAP or whose results exceed slot_cap is queued for the general
+// path (overflow list), which then writes all of that query's outputs.
+template <typename T, int LAYOUT, int CAP>
 __global__ void __launch_bounds__(256) k_query_fused(
-    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const uint32_t* __restrict__ dir,
-    uint64_t cells, uint32_t shift, uint64_t n, const typename T::E* __restrict__ entries,
+    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
     unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
@@ -239,38 +329,69 @@ __global__ void __launch_bounds__(256) k_query_fused(
         if (lane == 0) cnt_s[warp] = 0;
         __syncwarp();
         const typename T::K* qk = qkeys + q * tables;
+        auto push = [&](uint32_t id) {
+            const uint32_t pos = atomicAdd(cnt_s + warp, 1u);
+            if (pos < CAP) ids[pos] = id;
+        };
         for (uint32_t t0 = 0; t0 < tables; t0 += 128) {
             uint64_t key[4];
-            uint32_t s[4], e[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t t = t0 + u * 32 + lane;
                 key[u] = t < tables ? uint64_t(qk[t]) : 0ull;
             }
+            if constexpr (LAYOUT == kLayoutCsr) {
+                uint32_t s[4], e[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t t = t0 + u * 32 + lane;
-                if (t < tables) {
-                    const uint32_t* d = dir + uint64_t(t) * (cells + 1) + (key[u] >> shift);
-                    s[u] = __ldg(d);
-                    e[u] = __ldg(d + 1);
-                } else {
-                    s[u] = e[u] = 0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (s[u] < e[u]) {
+                for (int u = 0; u < 4; ++u) { // four directory lookups in flight
                     const uint32_t t = t0 + u * 32 + lane;
-                    const E* et = entries + uint64_t(t) * n;
+                    if (t < tables) {
+                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key[u] >> tb.shift);
+                        s[u] = __ldg(d);
+                        e[u] = __ldg(d + 1);
+                    } else {
+                        s[u] = e[u] = 0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const E* et = tb.data + uint64_t(t0 + u * 32 + lane) * tb.n;
                     uint32_t a = s[u];
                     while (a < e[u] && T::key(et[a]) < key[u]) ++a;
-                    uint32_t b = a;
-                    while (b < e[u] && T::key(et[b]) == key[u]) ++b;
-                    if (b > a) {
-                        const uint32_t pos = atomicAdd(cnt_s + warp, b - a);
-                        for (uint32_t k = a; k < b; ++k)
-                            if (pos + (k - a) < CAP) ids[pos + (k - a)] = T::id(et[k]);
+                    while (a < e[u] && T::key(et[a]) == key[u]) push(T::id(et[a++]));
+                }
+            } else {
+                E sl[4][kSlots];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { // four home buckets in flight
+                    const uint32_t t = t0 + u * 32 + lane;
+                    if (t < tables) {
+                        const E* bp = tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots;
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j) sl[u][j] = bp[j];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t t = t0 + u * 32 + lane;
+                    if (t >= tables) continue;
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+                        if (!T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u]) push(T::id(sl[u][j]));
+                    if (!T::empty(sl[u][kSlots - 1])) { // run continues (rare)
+                        uint64_t b = key[u] >> tb.shift;
+                        const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
+                        for (;;) {
+                            b = (b + 1) & (tb.nbuckets - 1);
+                            const E* bp = base + b * kSlots;
+                            E x[kSlots];
+#pragma unroll
+                            for (int j = 0; j < kSlots; ++j) x[j] = bp[j];
+#pragma unroll
+                            for (int j = 0; j < kSlots; ++j)
+                                if (!T::empty(x[j]) && T::key(x[j]) == key[u]) push(T::id(x[j]));
+                            if (T::empty(x[kSlots - 1])) break;
+                        }
                     }
                 }
             }
@@ -353,58 +474,47 @@ __global__ void __launch_bounds__(256) k_query_fused(
     }
 }
 
-// General path, for the selected queries qsel[0..ns) (overflow of the fused
-// kernel): probe -> per-selection collision counts; scan; gather; CUB
-// segmented sort; verify.
-template <typename T>
-__global__ void k_probe(const typename T::K* __restrict__ qkeys, const uint32_t* __restrict__ qsel, uint64_t ns,
-                        uint32_t tables, const uint32_t* __restrict__ dir, uint64_t cells, uint32_t shift, uint64_t n,
-                        const typename T::E* __restrict__ entries, uint32_t* __restrict__ r_start,
-                        uint32_t* __restrict__ r_count, unsigned long long* __restrict__ coll) {
+// General path for the selected queries qsel[0..ns): per (query, table)
+// counts -> per-query collision totals; scan; gather the ids; CUB segmented
+// sort; verify.
+template <typename T, int LAYOUT>
+__global__ void k_count_sel(const typename T::K* __restrict__ qkeys, const uint32_t* __restrict__ qsel, uint64_t ns,
+                            uint32_t tables, const Tables<T> tb, unsigned long long* __restrict__ coll) {
     const uint64_t total = ns * tables;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t s_ = i / tables;
         const uint32_t t = uint32_t(i % tables);
         const uint64_t key = qkeys[uint64_t(qsel[s_]) * tables + t];
-        const uint32_t* d = dir + uint64_t(t) * (cells + 1);
-        const uint64_t c = key >> shift;
-        uint32_t s = __ldg(d + c);
-        const uint32_t e = __ldg(d + c + 1);
-        const typename T::E* et = entries + uint64_t(t) * n;
-        while (s < e && T::key(et[s]) < key) ++s;
-        uint32_t f = s;
-        while (f < e && T::key(et[f]) == key) ++f;
-        r_start[i] = s;
-        r_count[i] = f - s;
-        if (f > s) atomicAdd(coll + s_, (unsigned long long)(f - s));
+        const uint32_t c = probe_one<T, LAYOUT>(tb, t, key, [](uint32_t) {});
+        if (c) atomicAdd(coll + s_, (unsigned long long)c);
     }
 }
 
-template <typename T>
-__global__ void k_gather(uint64_t ns, uint32_t tables, uint64_t n, const typename T::E* __restrict__ entries,
-                         const uint32_t* __restrict__ r_start, const uint32_t* __restrict__ r_count,
-                         const unsigned long long* __restrict__ coll_off, unsigned long long* __restrict__ fill,
-                         uint32_t* __restrict__ cand) {
+template <typename T, int LAYOUT>
+__global__ void k_gather_sel(const typename T::K* __restrict__ qkeys, const uint32_t* __restrict__ qsel, uint64_t ns,
+                             uint32_t tables, const Tables<T> tb, const unsigned long long* __restrict__ coll_off,
+                             unsigned long long* __restrict__ fill, uint32_t* __restrict__ cand) {
     const uint64_t total = ns * tables;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t cnt = r_count[i];
-        if (cnt == 0) continue;
         const uint64_t s_ = i / tables;
         const uint32_t t = uint32_t(i % tables);
-        const uint64_t dst = coll_off[s_] + atomicAdd(fill + s_, (unsigned long long)cnt);
-        const typename T::E* et = entries + uint64_t(t) * n + r_start[i];
-        for (uint32_t k = 0; k < cnt; ++k) cand[dst + k] = T::id(et[k]);
+        const uint64_t key = qkeys[uint64_t(qsel[s_]) * tables + t];
+        probe_one<T, LAYOUT>(tb, t, key, [&](uint32_t id) {
+            const uint64_t dst = coll_off[s_] + atomicAdd(fill + s_, 1ull);
+            cand[dst] = id;
+        });
     }
 }
 
 // Warp per selected query over its sorted candidate list; writes the query's
-// counters and its results at base + coll_off[s].
-__global__ void k_verify(uint64_t ns, const uint32_t* __restrict__ qsel, const unsigned long long* __restrict__ coll_off,
-                         const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ rows,
-                         const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius, uint64_t base_pos,
-                         uint32_t* __restrict__ res_id, uint32_t* __restrict__ res_dist,
-                         unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
-                         unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos) {
+// counters and its results at base_pos + coll_off[s].
+__global__ void k_verify_sel(uint64_t ns, const uint32_t* __restrict__ qsel,
+                             const unsigned long long* __restrict__ coll_off, const uint32_t* __restrict__ sorted,
+                             const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words,
+                             uint32_t radius, uint64_t base_pos, uint32_t* __restrict__ res_id,
+                             uint32_t* __restrict__ res_dist, unsigned long long* __restrict__ coll_q,
+                             unsigned long long* __restrict__ cand_q, unsigned long long* __restrict__ found_q,
+                             unsigned long long* __restrict__ src_pos) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t s_ = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); s_ < ns; s_ += warps) {
@@ -478,8 +588,20 @@ unsigned grid_for(uint64_t work, int device, unsigned threads = 256, unsigned pe
 }
 
 template <typename T>
-void build_tables(DeviceIndex& ix, const void* keys, uint32_t t0, uint32_t count, DevBuf& cnt_buf,
-                  DevBuf& cur_buf, DevBuf& big_buf, DevBuf& big_cnt, cudaStream_t s) {
+Tables<T> view(const DeviceIndex& ix) {
+    Tables<T> tb;
+    tb.data = static_cast<const typename T::E*>(ix.entries.p);
+    tb.dir = ix.dir.as<uint32_t>();
+    tb.n = ix.n;
+    tb.cells = ix.cells();
+    tb.nbuckets = ix.nbuckets;
+    tb.shift = ix.key_shift;
+    return tb;
+}
+
+template <typename T>
+void build_csr_tables(DeviceIndex& ix, const void* keys, uint32_t t0, uint32_t count, DevBuf& cnt_buf,
+                      DevBuf& cur_buf, DevBuf& big_buf, DevBuf& big_cnt, cudaStream_t s) {
     using K = typename T::K;
     const uint64_t n = ix.n, cells = ix.cells();
     const uint64_t cbytes = uint64_t(count) * (cells + 1) * 4;
@@ -488,7 +610,7 @@ void build_tables(DeviceIndex& ix, const void* keys, uint32_t t0, uint32_t count
     uint32_t* dir = ix.dir.as<uint32_t>() + uint64_t(t0) * (cells + 1);
     auto* entries = static_cast<typename T::E*>(ix.entries.p) + uint64_t(t0) * n;
     FCLSH_CUDA(cudaMemsetAsync(cnt, 0, cbytes, s));
-    const dim3 g2(std::max<unsigned>(1, grid_for(n, ix.device, 256, 8) / count), count);
+    const dim3 g2(std::max<unsigned>(1, grid_for(n * count, ix.device, 256, 8) / count), count);
     k_hist<K><<<g2, 256, 0, s>>>(static_cast<const K*>(keys), n, ix.key_shift, cells, cnt);
     FCLSH_LAUNCHED();
     k_scan_cells<<<count, 1024, 0, s>>>(cnt, cells, dir, cur);
@@ -522,44 +644,53 @@ void build_all(DeviceIndex& ix) {
     cudaStream_t s = ix.stream;
     DevBuf keys, cnt, cur, big, bigc;
     keys.ensure(L * n * kb);
-    // tables per directory chunk: keep one chunk's working set near L2 size
-    const uint64_t per_table = n * (kb + ix.entry_bytes()) + (ix.cells() + 1) * 8;
-    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (64ull << 20) / per_table)));
+    if (ix.layout == kLayoutBuckets)
+        FCLSH_CUDA(cudaMemsetAsync(ix.entries.p, T::empty_byte(), ix.entries.bytes, s));
+    // CSR: tables per chunk bounded by ~1 GiB of cell counters
+    const uint64_t per_table = (ix.cells() + 1) * 8;
+    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (1ull << 30) / per_table)));
     for (uint32_t p = 0; p < ix.fs->parts; ++p) {
         hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, n, kLayoutTableMajor, s, p, 1);
-        for (uint32_t t = 0; t < L; t += chunk) {
-            const uint32_t c = uint32_t(std::min<uint64_t>(chunk, L - t));
-            build_tables<T>(ix, static_cast<const K*>(keys.p) + uint64_t(t) * n, uint32_t(p * L + t), c, cnt, cur,
-                            big, bigc, s);
+        if (ix.layout == kLayoutBuckets) {
+            const dim3 g(std::max<unsigned>(1, grid_for(n * L, ix.device, 256, 8) / unsigned(L)), unsigned(L));
+            auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
+            k_bucket_insert<T><<<g, 256, 0, s>>>(static_cast<const K*>(keys.p), n, ix.key_shift, ix.nbuckets, bk);
+            FCLSH_LAUNCHED();
+        } else {
+            for (uint32_t t = 0; t < L; t += chunk) {
+                const uint32_t c = uint32_t(std::min<uint64_t>(chunk, L - t));
+                build_csr_tables<T>(ix, static_cast<const K*>(keys.p) + uint64_t(t) * n, uint32_t(p * L + t), c, cnt,
+                                    cur, big, bigc, s);
+            }
         }
     }
     FCLSH_CUDA(cudaStreamSynchronize(s));
 }
 
-template <typename T, int CAP>
+template <typename T, int LAYOUT, int CAP>
 void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, cudaStream_t s) {
-    auto kern = k_query_fused<T, CAP>;
+    auto kern = k_query_fused<T, LAYOUT, CAP>;
     const size_t smem = (8 + size_t(8) * CAP) * 4;
     FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
     FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
-    kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), ix.dir.as<uint32_t>(), ix.cells(),
-                                           ix.key_shift, ix.n, static_cast<const typename T::E*>(ix.entries.p),
-                                           ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q,
-                                           found_q, src_pos, tmp_id, tmp_dist, ovf, ovf_cnt);
+    const uint64_t grid =
+        std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
+    kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
+                                           ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
+                                           tmp_dist, ovf, ovf_cnt);
     FCLSH_LAUNCHED();
 }
 
-template <typename T>
+template <typename T, int LAYOUT>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
     using K = typename T::K;
     QueryOutput out;
     out.nq = nq;
-    const uint64_t T_ = ix.tables, cells = ix.cells();
+    const uint64_t T_ = ix.tables;
     const bool big = T_ > 600;
     const uint32_t slot_cap = big ? 128 : 32;
     K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
@@ -583,11 +714,11 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 4, s));
     if (nq) {
         if (big)
-            launch_fused<T, 2048>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                  tmp_dist, ovf, ovf_cnt, s);
+            launch_fused<T, LAYOUT, 2048>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
         else
-            launch_fused<T, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                  tmp_dist, ovf, ovf_cnt, s);
+            launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
     unsigned int ns = 0;
@@ -598,21 +729,17 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     if (ns) {
         // general path for the overflowing queries
         const uint64_t pairs = uint64_t(ns) * T_;
-        uint32_t* rs = static_cast<uint32_t*>(ix.r_start.ensure(pairs * 4));
-        uint32_t* rc = static_cast<uint32_t*>(ix.r_count.ensure(pairs * 4));
+        const Tables<T> tb = view<T>(ix);
         auto* coll_s = static_cast<unsigned long long*>(ix.coll_sel.ensure((ns + 1) * 8));
         auto* coll_off = static_cast<unsigned long long*>(ix.coll_off.ensure((ns + 1) * 8));
         auto* fill = static_cast<unsigned long long*>(ix.fill.ensure((ns + 1) * 8));
         FCLSH_CUDA(cudaMemsetAsync(coll_s, 0, (ns + 1) * 8, s));
         FCLSH_CUDA(cudaMemsetAsync(fill, 0, (ns + 1) * 8, s));
-        k_probe<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), ix.dir.as<uint32_t>(), cells,
-                                                               ix.key_shift, ix.n,
-                                                               static_cast<const typename T::E*>(ix.entries.p), rs, rc,
-                                                               coll_s);
+        k_count_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), tb, coll_s);
         FCLSH_LAUNCHED();
-        size_t tb = 0;
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, coll_s, coll_off, ns + 1, s));
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tb), tb, coll_s, coll_off, ns + 1, s));
+        size_t tb_bytes = 0;
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb_bytes, coll_s, coll_off, ns + 1, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tb_bytes), tb_bytes, coll_s, coll_off, ns + 1, s));
         unsigned long long total_coll = 0;
         FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + ns, 8, cudaMemcpyDeviceToHost, s));
         FCLSH_CUDA(cudaStreamSynchronize(s));
@@ -621,9 +748,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         tmp2_id = static_cast<uint32_t*>(ix.res2_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
         tmp2_dist = static_cast<uint32_t*>(ix.res2_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
         if (total_coll) {
-            k_gather<T><<<grid_for(pairs, ix.device), 256, 0, s>>>(ns, uint32_t(T_), ix.n,
-                                                                    static_cast<const typename T::E*>(ix.entries.p), rs,
-                                                                    rc, coll_off, fill, cand);
+            k_gather_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), tb,
+                                                                                coll_off, fill, cand);
             FCLSH_LAUNCHED();
             size_t sb = 0;
             FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(ns),
@@ -631,7 +757,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted,
                                                           int64_t(total_coll), int64_t(ns), coll_off, coll_off + 1, s));
         }
-        k_verify<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
+        k_verify_sel<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
             ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap, tmp2_id,
             tmp2_dist, coll_q, cand_q, found_q, src_pos);
         FCLSH_LAUNCHED();
@@ -666,6 +792,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     ix.last_overflow = ns;
     return out;
 }
+
 } // namespace
 
 DeviceIndex::~DeviceIndex() {
@@ -683,6 +810,7 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     if (radius != plan.radius) throw UsageError("index: radius does not match the plan");
     if (plan.table_count() > opt.table_budget) throw ResourceError("index: table count exceeds the budget");
     if (n + opt.id_offset > (uint64_t(1) << 32)) throw UsageError("index: ids must fit 32 bits");
+    if (opt.layout < 0 || opt.layout > 2) throw UsageError("index: unknown table layout");
 
     auto ix = std::make_unique<DeviceIndex>();
     ix->device = opt.device;
@@ -708,17 +836,45 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     ix->tables = ix->fs->total_tables();
 
     const uint32_t kbits = bit_length(opt.prime - 1);
+    const uint64_t W = ix->row_words;
+    const uint64_t eb = ix->entry_bytes();
+    // bucket table: 2^bb >= n/2 buckets of 4 slots (load <= 50%), home = key >> (kbits - bb)
+    uint32_t bb = bit_length(std::max<uint64_t>(2, (n + 1) / 2) - 1);
+    if (bb < 1) bb = 1;
+    const bool bkt_ok = bb <= kbits && (uint64_t(kSlots) << bb) > n;
+    const uint64_t bkt_bytes = ix->tables * (uint64_t(1) << bb) * kSlots * eb;
+    // CSR directory: 2^b cells, about two postings per cell
     uint32_t b = opt.directory_bits > 0 ? uint32_t(opt.directory_bits)
                                         : std::max<uint32_t>(1, bit_length(n - 1) > 1 ? bit_length(n - 1) - 1 : 1);
     b = std::min<uint32_t>({b, kbits, 30u});
-    ix->dir_bits = b;
-    ix->key_shift = kbits - b;
+    const uint64_t csr_bytes = ix->tables * (n * eb + ((uint64_t(1) << b) + 1) * 4);
+    int layout = opt.layout;
+    if (layout == kLayoutAuto) {
+        size_t free_b = 0, total_b = 0;
+        FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * (ix->wide ? 8 : 4) + (uint64_t(2) << 30);
+        layout = (bkt_ok && bkt_bytes + need_extra <= free_b) ? kLayoutBuckets : kLayoutCsr;
+    }
+    if (layout == kLayoutBuckets && !bkt_ok)
+        throw UsageError("index: bucket layout needs a key field wider than the bucket count");
+    ix->layout = layout;
+    if (layout == kLayoutBuckets) {
+        ix->nbuckets = uint64_t(1) << bb;
+        ix->key_shift = kbits - bb;
+        ix->dir_bits = 0;
+    } else {
+        ix->dir_bits = b;
+        ix->key_shift = kbits - b;
+    }
 
-    const uint64_t W = ix->row_words;
     try {
         ix->rows.ensure(n * W * 8);
-        ix->entries.ensure(ix->tables * n * ix->entry_bytes());
-        ix->dir.ensure(ix->tables * (ix->cells() + 1) * 4);
+        if (layout == kLayoutBuckets) {
+            ix->entries.ensure(bkt_bytes);
+        } else {
+            ix->entries.ensure(ix->tables * n * eb);
+            ix->dir.ensure(ix->tables * (ix->cells() + 1) * 4);
+        }
     } catch (const CudaError& e) {
         throw ResourceError(std::string("index: device memory exhausted (") + e.what() + ")");
     }
@@ -748,8 +904,13 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
                          std::to_string(ix.radius));
     FCLSH_CUDA(cudaSetDevice(ix.device));
     cudaStream_t s = stream ? stream : ix.stream;
-    QueryOutput o = ix.wide ? query_impl<WideEntry>(ix, d_q, nq, radius, s)
-                            : query_impl<NarrowEntry>(ix, d_q, nq, radius, s);
+    QueryOutput o;
+    if (ix.wide)
+        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
+                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s);
+    else
+        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
+                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s);
     FCLSH_CUDA(cudaEventSynchronize(ix.ev[DeviceIndex::kStages]));
     for (int i = 0; i < DeviceIndex::kStages; ++i) {
         float ms = 0;

@@ -12,14 +12,21 @@
 
 namespace fclsh_b200 {
 
-// Device layout of one shard's index:
-//   rows     n x W u64            the shard's points (verify reads them)
-//   entries  T x n                per table, (key, id) sorted by (key, id):
-//                                 u64 (key << 32 | id) when prime < 2^32,
-//                                 else {u64 key, u64 id} pairs
-//   dir      T x (D + 1) u32      per table, CSR offsets of D = 2^b key
-//                                 cells (cell = key >> shift): the entries
-//                                 with key in cell c are [dir[c], dir[c+1])
+constexpr int kLayoutAuto = 0;
+constexpr int kLayoutCsr = 1;
+constexpr int kLayoutBuckets = 2;
+
+// Device layout of one shard's index. An entry is
+// u64 (key << 32 | id) when prime < 2^32, else {u64 key, u64 id}.
+//   rows     n x W u64          the shard's points (verify reads them)
+//   kLayoutBuckets (default):
+//     entries  T x 2^bb x 4     per table, open-addressed buckets of four
+//                               entries, home bucket key >> shift, linear
+//                               probing, load <= 50%, empty = all-ones
+//   kLayoutCsr (memory-tight):
+//     entries  T x n            per table, (key, id) sorted by (key, id)
+//     dir      T x (D + 1) u32  CSR offsets of D = 2^b key cells
+//                               (cell = key >> shift)
 struct DeviceIndex {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -30,8 +37,10 @@ struct DeviceIndex {
     uint64_t prime = 0;
     bool wide = false;        // 16-byte entries (prime >= 2^32)
     uint64_t tables = 0;      // T
-    uint32_t dir_bits = 0;    // b
-    uint32_t key_shift = 0;   // cell = key >> key_shift
+    int layout = 0;           // kLayoutCsr or kLayoutBuckets
+    uint64_t nbuckets = 0;    // buckets per table (kLayoutBuckets)
+    uint32_t dir_bits = 0;    // b (kLayoutCsr)
+    uint32_t key_shift = 0;   // cell / home bucket = key >> key_shift
     uint64_t id_offset = 0;
     double build_ms = 0;
     std::unique_ptr<DeviceFamilySet> fs;
@@ -64,6 +73,7 @@ struct IndexBuildOptions {
     int device = 0;
     uint64_t id_offset = 0;
     int directory_bits = 0;
+    int layout = kLayoutAuto;
 };
 
 // build_index(data, covering_batch, radius, plan, Rng(rng_seed), opt).

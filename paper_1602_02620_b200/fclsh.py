@@ -313,6 +313,8 @@ class IndexSet:
         self.directory_bits = int(info.directory_bits)
         self.device_bytes = int(info.device_bytes)
         self.build_ms = float(info.build_ms)
+        self.layout = {1: "csr", 2: "buckets"}.get(int(info.layout), "?")
+        self.buckets_per_table = int(info.buckets_per_table)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -380,9 +382,11 @@ class IndexSet:
 
 def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, prime: int = M61,
                 include_zero_column: bool = False, table_budget: int = DEFAULT_TABLE_BUDGET, device: int = 0,
-                id_offset: int = 0, directory_bits: int = 0, dims: int | None = None) -> IndexSet:
+                id_offset: int = 0, directory_bits: int = 0, dims: int | None = None,
+                layout: str = "auto") -> IndexSet:
     """build_index(data, Method::covering_batch, radius, plan, Rng(rng_seed), IndexOptions{...})
-    (index.cpp:49-119). data_rows: numpy uint64 [n, W] or a CUDA tensor."""
+    (index.cpp:49-119). data_rows: numpy uint64 [n, W] or a CUDA tensor.
+    layout: "auto" | "csr" | "buckets" (device table layout; same results)."""
     opt = N.IndexOptions()
     N.lib().fclsh_index_options_default(C.byref(opt))
     opt.prime = prime
@@ -391,6 +395,7 @@ def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, 
     opt.device = device
     opt.id_offset = id_offset
     opt.directory_bits = directory_bits
+    opt.layout = {"auto": 0, "csr": 1, "buckets": 2}[layout]
     d = plan.dims if dims is None else dims
     h = C.c_void_p()
     if hasattr(data_rows, "data_ptr"):  # torch tensor on the device

@@ -13,12 +13,24 @@ pytestmark = pytest.mark.gpu
 M31, M61 = F.M31, F.M61
 
 
+LAYOUTS = ("buckets", "csr")
+
+
 def check_against_oracle(oracle, rows, q, d, radius, override, prime, plan_seed=11, index_seed=22, qradius=None,
-                         directory_bits=0):
+                         directory_bits=0, layouts=LAYOUTS):
+    res = None
+    for layout in layouts:
+        res = _check_one(oracle, rows, q, d, radius, override, prime, plan_seed, index_seed, qradius, directory_bits,
+                         layout)
+    return res
+
+
+def _check_one(oracle, rows, q, d, radius, override, prime, plan_seed, index_seed, qradius, directory_bits, layout):
     qradius = radius if qradius is None else qradius
     force = F.PlanOverride(F.PlanKind(override[0]), override[1])
     plan = F.make_plan(d, radius, 1.0, rows.shape[0], plan_seed, force)
-    ix = F.build_index(rows, radius, plan, index_seed, prime=prime, directory_bits=directory_bits)
+    ix = F.build_index(rows, radius, plan, index_seed, prime=prime, directory_bits=directory_bits, layout=layout)
+    assert ix.layout == layout
     assert ix.table_count() == plan.table_count()
     assert ix.entry_count() == plan.table_count() * rows.shape[0]
     res = ix.query_r_nn(q, qradius)
@@ -60,7 +72,11 @@ def test_m61_and_small_prime_indexes(oracle):
     q = planted_queries(rng, rows, 96, 60, 5)
     check_against_oracle(oracle, rows, q, 96, 4, (0, 1), M61)
     check_against_oracle(oracle, rows, q, 96, 4, (2, 2), M61)
-    check_against_oracle(oracle, rows, q, 96, 3, (0, 1), 101)
+    check_against_oracle(oracle, rows, q, 96, 3, (0, 1), 101, layouts=("csr",))
+    plan = F.make_plan(96, 3, 1.0, 1500, 11, F.PlanOverride(F.PlanKind.identity, 1))
+    with pytest.raises(F.UsageError, match="bucket layout"):
+        F.build_index(rows, 3, plan, 22, prime=101, layout="buckets")
+    assert F.build_index(rows, 3, plan, 22, prime=101).layout == "csr"  # auto falls back
 
 
 def test_clustered_data_long_cells(oracle):
@@ -79,7 +95,7 @@ def test_directory_extremes(oracle):
     rows = random_rows(rng, 2500, 64)
     q = planted_queries(rng, rows, 64, 40, 4)
     for bits in (1, 4, 18):
-        check_against_oracle(oracle, rows, q, 64, 3, (0, 1), M31, directory_bits=bits)
+        check_against_oracle(oracle, rows, q, 64, 3, (0, 1), M31, directory_bits=bits, layouts=("csr",))
 
 
 def test_edge_queries(oracle):
