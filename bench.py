@@ -12,7 +12,7 @@ out, copies inside the timed region). The step's results are checked against
 the reference CPU path (oracle/_ref) in the same run (`parity`).
 
 Also reported: the fcLSH hash-evaluation microbenchmark (configs[4], "cfg5":
-8M x 1024-bit rows, r = 10, 2047 keys/row written table-major in 1M-row
+8M x 1024-bit rows, r = 10, 2047 keys/row written point-major in 1M-row
 chunks) as `hash`, and the index build time as `build`.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
@@ -359,7 +359,7 @@ def main():
 
 
 def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
-    """cfg5: 8M x 1024-bit rows, r = 10 -> 2047 keys per row, table-major in
+    """cfg5: 8M x 1024-bit rows, r = 10 -> 2047 keys per row, point-major in
     1M-row chunks. Step = all chunks. Algorithmic bytes = rows read once +
     every key written once = n * (d/8 + L*4)."""
     import torch
@@ -369,12 +369,12 @@ def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
     fam = F.build_covering_family(cfg5.dims, cfg5.radius, cfg5.index_seed(), prime=F.M31)
     L = fam.table_count()
     d_rows = torch.from_numpy(rows.view(np.int64)).to(f"cuda:{dev}")
-    keys = torch.empty((L, chunk), dtype=torch.int32, device=f"cuda:{dev}")
+    keys = torch.empty((chunk, L), dtype=torch.int32, device=f"cuda:{dev}")  # point-major chunk
 
     def step():
         for c0 in range(0, n, chunk):
             m = min(chunk, n - c0)
-            F.hash_batch_device(fam, d_rows[c0:c0 + m], keys, layout=0, key_stride=chunk, stream=stream)
+            F.hash_batch_device(fam, d_rows[c0:c0 + m], keys, layout=1, key_stride=L, stream=stream)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -397,16 +397,16 @@ def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
         from oracle import oracle as O
         orc = O.best()
         m0 = 64
-        F.hash_batch_device(fam, d_rows[:chunk], keys, layout=0, key_stride=chunk, stream=stream)
+        F.hash_batch_device(fam, d_rows[:chunk], keys, layout=1, key_stride=L, stream=stream)
         torch.cuda.synchronize()
-        got = keys[:, :m0].cpu().numpy().T.astype(np.uint64)
+        got = keys[:m0].cpu().numpy().astype(np.uint64)
         want = orc.hash_batch(fam.mapping, fam.seeds, cfg5.dims, cfg5.radius, F.M31, rows[:m0], kind=int(fam.kind))
         check = bool((got == want).all())
     except Exception as e:  # noqa: BLE001
         check = str(e)
     return {"metric": "fcLSH hash keys/sec (cfg5: 8M x 1024-bit rows, r=10, L=2047, 32-bit keys)",
             "value": n * L / (avg / 1e3), "unit": "keys/s", "ms_per_step": avg, "points": n, "chunk": chunk,
-            "roofline": {"bound": "hbm", "kernel": "k_hash_m31<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": "k_hash_m31_pm<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "traffic": None, "peak_source": peak_src,
                          "algorithmic_bytes_per_step": algo_bytes},
             "keys_match_oracle_sample": check}

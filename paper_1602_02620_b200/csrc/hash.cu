@@ -393,6 +393,191 @@ __global__ void __launch_bounds__(256) k_hash_generic(const GenericParams p) {
     }
 }
 
+// (O_lo + 2^16 * O_hi) mod (2^31-1) from D = 2*O per plane (D even).
+__device__ __forceinline__ uint32_t finish_from_d(uint32_t Dlo, uint32_t Dhi) {
+    const uint32_t slo = Dlo >> 1;
+    const uint32_t shi = Dhi >> 1;
+    uint32_t s = slo + (shi >> 15) + ((shi & 0x7FFFu) << 16); // < 2^32
+    s = (s & kP31) + (s >> 31);                               // <= 2^31
+    const uint32_t s1 = s + 1;
+    return (s1 & kP31) + (s1 >> 31) - 1;                      // canonical in [0, P)
+}
+
+// Point-major variant (keys[row*stride + part*L + v-1]) for G > 1: every warp
+// owns 32/G rows end to end -- row fetch, sketch, both butterfly phases, the
+// final reduction and the key stores go straight from registers to HBM (a
+// lane's consecutive keys are contiguous across the warp), so there is no
+// output staging and no CTA-wide barrier after the family is staged. The
+// plane totals T = F[0] come from a lane reduction of the phase-1 block
+// totals, which lets the last butterfly stage produce D = T - F directly.
+template <int LOGN, bool DIRECT>
+__global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = lanes_for(LOGN);
+    constexpr int E = N / G;
+    constexpr int EG = E / G;
+    constexpr int SPW = 32 / G; // rows per warp
+    static_assert(G > 1 && (EG == 1 || EG == 2), "phase-2 layout");
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* xbuf = reinterpret_cast<uint64_t*>(smem);    // 8 warps x 32*E u64
+    uint64_t* rows_s = xbuf + 256 * E;                      // 8 warps x SPW x row_words u64
+    uint2* fam_s = reinterpret_cast<uint2*>(rows_s + 8 * SPW * p.row_words);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int slot = lane / G; // row within the warp
+    const int g = lane % G;
+
+    for (uint32_t i = tid; i < p.parts * p.part_words; i += 256) fam_s[i] = p.fam[i];
+    __syncthreads();
+
+    uint64_t* xw = xbuf + warp * 32 * E;                    // this warp's transpose region
+    uint64_t* rw = rows_s + warp * SPW * p.row_words;       // this warp's rows
+    const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rw + slot * p.row_words);
+    uint64_t* xs = xw + slot * N;                           // this row's transpose region
+
+    const uint64_t groups = (p.n + SPW - 1) / SPW;
+    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+    for (uint64_t grp = uint64_t(blockIdx.x) * 8 + warp; grp < groups; grp += nwarps) {
+        const uint64_t p0 = grp * SPW;
+        {
+            const uint64_t base = p0 * p.row_words;
+            const uint64_t lim = p.n * p.row_words;
+            for (uint32_t i = lane; i < SPW * p.row_words; i += 32)
+                rw[i] = (base + i < lim) ? __ldg(p.rows + base + i) : 0ull;
+        }
+        __syncwarp();
+        const uint64_t my_point = p0 + slot;
+
+        for (uint32_t part = 0; part < p.parts; ++part) {
+            const uint2* fam = fam_s + part * p.part_words;
+            uint32_t lo[E], hi[E];
+            if constexpr (DIRECT) {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint2 e = fam[j * G + g];
+                    const uint32_t m = 0u - row_bit(myrow, e.x);
+                    lo[j] = e.y & m & 0xFFFFu;
+                    hi[j] = (e.y >> 16) & m;
+                }
+            } else {
+                uint64_t* sk = xw; // sk[col][lane], conflict-free for any col
+#pragma unroll
+                for (int j = 0; j < E; ++j) sk[j * 32 + lane] = 0ull;
+                const uint2* le = fam + g;
+                uint32_t cur = le[0].x >> 24;
+                uint64_t acc = 0;
+                for (uint32_t k = 0; k < p.lane_entries; ++k) {
+                    const uint2 e = le[k * G];
+                    const uint32_t col = e.x >> 24;
+                    if (col != cur) {
+                        sk[cur * 32 + lane] = acc;
+                        acc = 0;
+                        cur = col;
+                    }
+                    const uint64_t packed = (uint64_t(e.y >> 16) << 32) | (e.y & 0xFFFFu);
+                    acc += row_bit(myrow, e.x & 0xFFFFFFu) ? packed : 0ull;
+                }
+                sk[cur * 32 + lane] = acc;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint64_t v = sk[j * 32 + lane];
+                    lo[j] = uint32_t(v);
+                    hi[j] = uint32_t(v >> 32);
+                }
+                __syncwarp();
+            }
+
+            // phase 1
+            fht_signed<E>(lo);
+            fht_signed<E>(hi);
+            // plane totals: sum of the G block totals (register 0 of each lane)
+            uint32_t Tlo = lo[0], Thi = hi[0];
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                Tlo += __shfl_xor_sync(0xffffffffu, Tlo, o);
+                Thi += __shfl_xor_sync(0xffffffffu, Thi, o);
+            }
+            // transpose (warp-local)
+#pragma unroll
+            for (int j = 0; j < E; j += 2) {
+                const int idx = g * E + (j ^ ((2 * g) & (E - 1)));
+                *reinterpret_cast<uint4*>(xs + idx) = make_uint4(lo[j], hi[j], lo[j + 1], hi[j + 1]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                const int idx = h * E + ((g * EG) ^ ((2 * h) & (E - 1)));
+                if constexpr (EG == 2) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(xs + idx);
+                    lo[h] = v.x;
+                    hi[h] = v.y;
+                    lo[G + h] = v.z;
+                    hi[G + h] = v.w;
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2*>(xs + idx);
+                    lo[h] = v.x;
+                    hi[h] = v.y;
+                }
+            }
+            __syncwarp();
+            // phase 2: all but the last stage, then the last stage emits D = T - F
+#pragma unroll
+            for (int k = 0; k < EG; ++k) {
+                uint32_t* xl = lo + k * G;
+                uint32_t* xh = hi + k * G;
+#pragma unroll
+                for (int hs = 1; hs < G / 2; hs <<= 1) {
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        if ((i & hs) == 0) {
+                            uint32_t a = xl[i], b = xl[i + hs];
+                            xl[i] = a + b;
+                            xl[i + hs] = a - b;
+                            a = xh[i];
+                            b = xh[i + hs];
+                            xh[i] = a + b;
+                            xh[i + hs] = a - b;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < G / 2; ++i) {
+                    uint32_t a = xl[i], b = xl[i + G / 2];
+                    xl[i] = Tlo - a - b;
+                    xl[i + G / 2] = Tlo - a + b;
+                    a = xh[i];
+                    b = xh[i + G / 2];
+                    xh[i] = Thi - a - b;
+                    xh[i + G / 2] = Thi - a + b;
+                }
+            }
+            // keys straight to HBM: element (k, h) is code v = h*E + g*EG + k
+            if (my_point < p.n) {
+                uint32_t* out = static_cast<uint32_t*>(p.keys) + my_point * p.key_stride + part * p.L;
+                uint64_t* out64 = static_cast<uint64_t*>(p.keys) + my_point * p.key_stride + part * p.L;
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+#pragma unroll
+                    for (int k = 0; k < EG; ++k) {
+                        const int v = h * E + g * EG + k;
+                        const uint32_t key = finish_from_d(lo[k * G + h], hi[k * G + h]);
+                        if (v != 0) {
+                            if (p.key_bytes == 4)
+                                out[v - 1] = key;
+                            else
+                                out64[v - 1] = key;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <int LOGN, bool DIRECT>
 size_t fast_smem_bytes(const DeviceFamilySet& fs) {
     constexpr int G = lanes_for(LOGN);
@@ -406,6 +591,20 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
     constexpr int G = lanes_for(LOGN);
     constexpr int PT = 256 / G;
     const size_t smem = fast_smem_bytes<LOGN, DIRECT>(fs);
+    if constexpr (G > 1) {
+        if (prm.layout == kLayoutPointMajor) {
+            auto kern = k_hash_m31_pm<LOGN, DIRECT>;
+            FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            int per_sm = 0;
+            FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+            if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
+            const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
+            const uint64_t grid = std::min<uint64_t>((groups + 7) / 8, uint64_t(per_sm) * sm_count(fs.device));
+            kern<<<unsigned(std::max<uint64_t>(grid, 1)), 256, smem, stream>>>(prm);
+            FCLSH_LAUNCHED();
+            return;
+        }
+    }
     auto kern = k_hash_m31<LOGN, DIRECT>;
     FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;

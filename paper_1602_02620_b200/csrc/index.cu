@@ -131,14 +131,16 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
 
 // ----------------------------------------------------------------- build
 
+// keys are point-major for one part: key of (row i, table t) at keys[i*L + t]
 template <typename T>
-__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t nbuckets,
-                                typename T::E* __restrict__ buckets) {
-    const uint32_t t = blockIdx.y;
-    const typename T::K* kt = keys + uint64_t(t) * n;
-    typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t key = kt[i];
+__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t shift,
+                                uint64_t nbuckets, typename T::E* __restrict__ buckets) {
+    const uint64_t total = n * L;
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = x / L;
+        const uint32_t t = uint32_t(x % L);
+        typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
+        const uint64_t key = keys[x];
         const typename T::E e = T::make(key, uint32_t(i));
         uint64_t b = key >> shift;
         for (;;) {
@@ -152,14 +154,16 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
     }
 }
 
+// CSR build over tables [t0, t0+c) of one part; keys point-major (stride L).
 template <typename K>
-__global__ void k_hist(const K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t cells,
-                       uint32_t* __restrict__ cnt) {
-    const uint32_t t = blockIdx.y;
-    const K* kt = keys + uint64_t(t) * n;
-    uint32_t* ct = cnt + uint64_t(t) * (cells + 1);
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        atomicAdd(ct + (uint64_t(kt[i]) >> shift), 1u);
+__global__ void k_hist(const K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0, uint32_t c, uint32_t shift,
+                       uint64_t cells, uint32_t* __restrict__ cnt) {
+    const uint64_t total = n * c;
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = x / c;
+        const uint32_t t = uint32_t(x % c);
+        atomicAdd(cnt + uint64_t(t) * (cells + 1) + (uint64_t(keys[i * L + t0 + t]) >> shift), 1u);
+    }
 }
 
 // One CTA per table: exclusive scan of cnt[0..cells] -> dir and cursor.
@@ -199,16 +203,15 @@ __global__ void __launch_bounds__(1024) k_scan_cells(const uint32_t* __restrict_
 }
 
 template <typename T, typename K>
-__global__ void k_scatter(const K* __restrict__ keys, uint64_t n, uint32_t shift, uint64_t cells,
-                          uint32_t* __restrict__ cursor, typename T::E* __restrict__ entries) {
-    const uint32_t t = blockIdx.y;
-    const K* kt = keys + uint64_t(t) * n;
-    uint32_t* ut = cursor + uint64_t(t) * (cells + 1);
-    typename T::E* et = entries + uint64_t(t) * n;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t key = kt[i];
-        const uint32_t pos = atomicAdd(ut + (key >> shift), 1u);
-        et[pos] = T::make(key, uint32_t(i));
+__global__ void k_scatter(const K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0, uint32_t c, uint32_t shift,
+                          uint64_t cells, uint32_t* __restrict__ cursor, typename T::E* __restrict__ entries) {
+    const uint64_t total = n * c;
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = x / c;
+        const uint32_t t = uint32_t(x % c);
+        const uint64_t key = keys[i * L + t0 + t];
+        const uint32_t pos = atomicAdd(cursor + uint64_t(t) * (cells + 1) + (key >> shift), 1u);
+        entries[uint64_t(t) * n + pos] = T::make(key, uint32_t(i));
     }
 }
 
@@ -599,23 +602,25 @@ Tables<T> view(const DeviceIndex& ix) {
     return tb;
 }
 
+// keys: one part's point-major keys (stride L); builds global tables
+// [tg0, tg0 + count) from the part's local tables [t0, t0 + count).
 template <typename T>
-void build_csr_tables(DeviceIndex& ix, const void* keys, uint32_t t0, uint32_t count, DevBuf& cnt_buf,
-                      DevBuf& cur_buf, DevBuf& big_buf, DevBuf& big_cnt, cudaStream_t s) {
+void build_csr_tables(DeviceIndex& ix, const void* keys, uint32_t L, uint32_t t0, uint32_t tg0, uint32_t count,
+                      DevBuf& cnt_buf, DevBuf& cur_buf, DevBuf& big_buf, DevBuf& big_cnt, cudaStream_t s) {
     using K = typename T::K;
     const uint64_t n = ix.n, cells = ix.cells();
     const uint64_t cbytes = uint64_t(count) * (cells + 1) * 4;
     uint32_t* cnt = static_cast<uint32_t*>(cnt_buf.ensure(cbytes));
     uint32_t* cur = static_cast<uint32_t*>(cur_buf.ensure(cbytes));
-    uint32_t* dir = ix.dir.as<uint32_t>() + uint64_t(t0) * (cells + 1);
-    auto* entries = static_cast<typename T::E*>(ix.entries.p) + uint64_t(t0) * n;
+    uint32_t* dir = ix.dir.as<uint32_t>() + uint64_t(tg0) * (cells + 1);
+    auto* entries = static_cast<typename T::E*>(ix.entries.p) + uint64_t(tg0) * n;
     FCLSH_CUDA(cudaMemsetAsync(cnt, 0, cbytes, s));
-    const dim3 g2(std::max<unsigned>(1, grid_for(n * count, ix.device, 256, 8) / count), count);
-    k_hist<K><<<g2, 256, 0, s>>>(static_cast<const K*>(keys), n, ix.key_shift, cells, cnt);
+    const unsigned g = grid_for(n * count, ix.device, 256, 8);
+    k_hist<K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, cells, cnt);
     FCLSH_LAUNCHED();
     k_scan_cells<<<count, 1024, 0, s>>>(cnt, cells, dir, cur);
     FCLSH_LAUNCHED();
-    k_scatter<T, K><<<g2, 256, 0, s>>>(static_cast<const K*>(keys), n, ix.key_shift, cells, cur, entries);
+    k_scatter<T, K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, cells, cur, entries);
     FCLSH_LAUNCHED();
     // cells longer than kSmallCell: at most n / (kSmallCell+1) per table
     const uint64_t max_big = uint64_t(count) * (n / (kSmallCell + 1) + 1);
@@ -650,17 +655,17 @@ void build_all(DeviceIndex& ix) {
     const uint64_t per_table = (ix.cells() + 1) * 8;
     const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (1ull << 30) / per_table)));
     for (uint32_t p = 0; p < ix.fs->parts; ++p) {
-        hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, n, kLayoutTableMajor, s, p, 1);
+        // K1, point-major: key of (row i, local table t) at keys[i*L + t]
+        hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, L, kLayoutPointMajor, s, p, 1);
         if (ix.layout == kLayoutBuckets) {
-            const dim3 g(std::max<unsigned>(1, grid_for(n * L, ix.device, 256, 8) / unsigned(L)), unsigned(L));
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
-            k_bucket_insert<T><<<g, 256, 0, s>>>(static_cast<const K*>(keys.p), n, ix.key_shift, ix.nbuckets, bk);
+            k_bucket_insert<T><<<grid_for(n * L, ix.device, 256, 8), 256, 0, s>>>(
+                static_cast<const K*>(keys.p), n, uint32_t(L), ix.key_shift, ix.nbuckets, bk);
             FCLSH_LAUNCHED();
         } else {
             for (uint32_t t = 0; t < L; t += chunk) {
                 const uint32_t c = uint32_t(std::min<uint64_t>(chunk, L - t));
-                build_csr_tables<T>(ix, static_cast<const K*>(keys.p) + uint64_t(t) * n, uint32_t(p * L + t), c, cnt,
-                                    cur, big, bigc, s);
+                build_csr_tables<T>(ix, keys.p, uint32_t(L), t, uint32_t(p * L + t), c, cnt, cur, big, bigc, s);
             }
         }
     }
