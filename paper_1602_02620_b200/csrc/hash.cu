@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_hash_m31(const FastParams p) {
             if constexpr (DIRECT) {
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
-                    const uint2 e = fam[j * G + g]; // lane-fastest: conflict-free
+                    const uint2 e = fam[(j / 2) * 2 * G + 2 * g + (j & 1)]; // column pairs, lane-fastest
                     const uint32_t m = 0u - row_bit(myrow, e.x);
                     lo[j] = e.y & m & 0xFFFFu;
                     hi[j] = (e.y >> 16) & m;
@@ -393,14 +393,17 @@ __global__ void __launch_bounds__(256) k_hash_generic(const GenericParams p) {
     }
 }
 
-// (O_lo + 2^16 * O_hi) mod (2^31-1) from D = 2*O per plane (D even).
+// (O_lo + 2^16 * O_hi) mod (2^31-1) from D = 2*O per plane (D even, Dlo <
+// 2^32, Dhi < 2^31): s = O_lo + 2^16 O_hi (mod P, lazily) + 1 < 2^32, then
+// two Mersenne folds; the +1 makes the second fold land on the canonical
+// residue (P -> 0, 2^31 -> 1).
 __device__ __forceinline__ uint32_t finish_from_d(uint32_t Dlo, uint32_t Dhi) {
     const uint32_t slo = Dlo >> 1;
-    const uint32_t shi = Dhi >> 1;
-    uint32_t s = slo + (shi >> 15) + ((shi & 0x7FFFu) << 16); // < 2^32
-    s = (s & kP31) + (s >> 31);                               // <= 2^31
-    const uint32_t s1 = s + 1;
-    return (s1 & kP31) + (s1 >> 31) - 1;                      // canonical in [0, P)
+    const uint32_t a = Dhi >> 16;                               // (O_hi >> 15) * 2^31 == (O_hi >> 15)
+    const uint32_t b = ((Dhi << 15) & 0x7FFF0000u) | 1u;        // (O_hi & 0x7fff) << 16, plus 1
+    const uint32_t s1 = slo + a + b;                            // s + 1, s < 2^32 - 1
+    const uint32_t y = (s1 & kP31) + (s1 >> 31);                // fold
+    return (y & kP31) + (y >> 31) - 1;                          // canonical in [0, P)
 }
 
 // Point-major variant (keys[row*stride + part*L + v-1]) for G > 1: every warp
@@ -410,19 +413,29 @@ __device__ __forceinline__ uint32_t finish_from_d(uint32_t Dlo, uint32_t Dhi) {
 // output staging and no CTA-wide barrier after the family is staged. The
 // plane totals T = F[0] come from a lane reduction of the phase-1 block
 // totals, which lets the last butterfly stage produce D = T - F directly.
+// The transpose rows are padded by one 16-byte unit (E+2 u64) instead of
+// XOR-swizzled: conflict-free, and every access is [base + immediate].
+template <int LOGN>
+__host__ __device__ constexpr int pm_warps() {
+    return LOGN == 11 ? 12 : 8; // N = 2048 needs ~200 registers: 12 warps fit the register file
+}
+
 template <int LOGN, bool DIRECT>
-__global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
+__global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_m31_pm(const FastParams p) {
     constexpr int N = 1 << LOGN;
     constexpr int G = lanes_for(LOGN);
     constexpr int E = N / G;
+    constexpr int EP = E + 2; // padded transpose row (u64)
     constexpr int EG = E / G;
     constexpr int SPW = 32 / G; // rows per warp
+    constexpr int WARPS = pm_warps<LOGN>();
+    constexpr int NT = 32 * WARPS;
     static_assert(G > 1 && (EG == 1 || EG == 2), "phase-2 layout");
 
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* xbuf = reinterpret_cast<uint64_t*>(smem);    // 8 warps x 32*E u64
-    uint64_t* rows_s = xbuf + 256 * E;                      // 8 warps x SPW x row_words u64
-    uint2* fam_s = reinterpret_cast<uint2*>(rows_s + 8 * SPW * p.row_words);
+    uint64_t* xbuf = reinterpret_cast<uint64_t*>(smem);    // WARPS x 32*EP u64
+    uint64_t* rows_s = xbuf + WARPS * 32 * EP;              // WARPS x SPW x row_words u64
+    uint2* fam_s = reinterpret_cast<uint2*>(rows_s + WARPS * SPW * p.row_words);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -430,17 +443,19 @@ __global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
     const int slot = lane / G; // row within the warp
     const int g = lane % G;
 
-    for (uint32_t i = tid; i < p.parts * p.part_words; i += 256) fam_s[i] = p.fam[i];
+    for (uint32_t i = tid; i < p.parts * p.part_words; i += NT) fam_s[i] = p.fam[i];
     __syncthreads();
 
-    uint64_t* xw = xbuf + warp * 32 * E;                    // this warp's transpose region
+    uint64_t* xw = xbuf + warp * 32 * EP;                   // this warp's transpose region
     uint64_t* rw = rows_s + warp * SPW * p.row_words;       // this warp's rows
     const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rw + slot * p.row_words);
-    uint64_t* xs = xw + slot * N;                           // this row's transpose region
+    uint64_t* xs = xw + slot * G * EP;                      // this row's transpose region
+    uint64_t* xs_w = xs + g * EP;                           // phase-1 row of this lane
+    const uint64_t* xs_r = xs + g * EG;                     // phase-2 column of this lane
 
     const uint64_t groups = (p.n + SPW - 1) / SPW;
-    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
-    for (uint64_t grp = uint64_t(blockIdx.x) * 8 + warp; grp < groups; grp += nwarps) {
+    const uint64_t nwarps = uint64_t(gridDim.x) * WARPS;
+    for (uint64_t grp = uint64_t(blockIdx.x) * WARPS + warp; grp < groups; grp += nwarps) {
         const uint64_t p0 = grp * SPW;
         {
             const uint64_t base = p0 * p.row_words;
@@ -455,12 +470,17 @@ __global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
             const uint2* fam = fam_s + part * p.part_words;
             uint32_t lo[E], hi[E];
             if constexpr (DIRECT) {
+                // entries of columns (j, j+1) of lane g are adjacent: one 16-byte load
+                const uint4* fam4 = reinterpret_cast<const uint4*>(fam) + g;
 #pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    const uint2 e = fam[j * G + g];
-                    const uint32_t m = 0u - row_bit(myrow, e.x);
-                    lo[j] = e.y & m & 0xFFFFu;
-                    hi[j] = (e.y >> 16) & m;
+                for (int j = 0; j < E; j += 2) {
+                    const uint4 e = fam4[(j / 2) * G];
+                    const uint32_t m0 = 0u - row_bit(myrow, e.x);
+                    const uint32_t m1 = 0u - row_bit(myrow, e.z);
+                    lo[j] = e.y & m0 & 0xFFFFu;
+                    hi[j] = (e.y >> 16) & m0;
+                    lo[j + 1] = e.w & m1 & 0xFFFFu;
+                    hi[j + 1] = (e.w >> 16) & m1;
                 }
             } else {
                 uint64_t* sk = xw; // sk[col][lane], conflict-free for any col
@@ -500,24 +520,21 @@ __global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
                 Tlo += __shfl_xor_sync(0xffffffffu, Tlo, o);
                 Thi += __shfl_xor_sync(0xffffffffu, Thi, o);
             }
-            // transpose (warp-local)
+            // transpose (warp-local): element c = hb*E + j lives at xs[hb*EP + j]
 #pragma unroll
-            for (int j = 0; j < E; j += 2) {
-                const int idx = g * E + (j ^ ((2 * g) & (E - 1)));
-                *reinterpret_cast<uint4*>(xs + idx) = make_uint4(lo[j], hi[j], lo[j + 1], hi[j + 1]);
-            }
+            for (int j = 0; j < E; j += 2)
+                *reinterpret_cast<uint4*>(xs_w + j) = make_uint4(lo[j], hi[j], lo[j + 1], hi[j + 1]);
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < G; ++h) {
-                const int idx = h * E + ((g * EG) ^ ((2 * h) & (E - 1)));
                 if constexpr (EG == 2) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(xs + idx);
+                    const uint4 v = *reinterpret_cast<const uint4*>(xs_r + h * EP);
                     lo[h] = v.x;
                     hi[h] = v.y;
                     lo[G + h] = v.z;
                     hi[G + h] = v.w;
                 } else {
-                    const uint2 v = *reinterpret_cast<const uint2*>(xs + idx);
+                    const uint2 v = *reinterpret_cast<const uint2*>(xs_r + h * EP);
                     lo[h] = v.x;
                     hi[h] = v.y;
                 }
@@ -556,21 +573,22 @@ __global__ void __launch_bounds__(256) k_hash_m31_pm(const FastParams p) {
             }
             // keys straight to HBM: element (k, h) is code v = h*E + g*EG + k
             if (my_point < p.n) {
-                uint32_t* out = static_cast<uint32_t*>(p.keys) + my_point * p.key_stride + part * p.L;
-                uint64_t* out64 = static_cast<uint64_t*>(p.keys) + my_point * p.key_stride + part * p.L;
+                if (p.key_bytes == 4) {
+                    uint32_t* out = static_cast<uint32_t*>(p.keys) + my_point * p.key_stride + part * p.L +
+                                    (g * EG - 1);
 #pragma unroll
-                for (int h = 0; h < G; ++h) {
+                    for (int h = 0; h < G; ++h)
 #pragma unroll
-                    for (int k = 0; k < EG; ++k) {
-                        const int v = h * E + g * EG + k;
-                        const uint32_t key = finish_from_d(lo[k * G + h], hi[k * G + h]);
-                        if (v != 0) {
-                            if (p.key_bytes == 4)
-                                out[v - 1] = key;
-                            else
-                                out64[v - 1] = key;
-                        }
-                    }
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + g * EG + k != 0) out[h * E + k] = finish_from_d(lo[k * G + h], hi[k * G + h]);
+                } else {
+                    uint64_t* out = static_cast<uint64_t*>(p.keys) + my_point * p.key_stride + part * p.L +
+                                    (g * EG - 1);
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + g * EG + k != 0) out[h * E + k] = finish_from_d(lo[k * G + h], hi[k * G + h]);
                 }
             }
         }
@@ -592,15 +610,20 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
     constexpr int PT = 256 / G;
     const size_t smem = fast_smem_bytes<LOGN, DIRECT>(fs);
     if constexpr (G > 1) {
-        if (prm.layout == kLayoutPointMajor) {
+        constexpr int WARPS = pm_warps<LOGN>();
+        constexpr int E = (1 << LOGN) / G;
+        const size_t smem_pm = size_t(WARPS) * 32 * (E + 2) * 8 + size_t(WARPS) * (32 / G) * fs.row_words * 8 +
+                               size_t(fs.parts) * fs.part_words * 8;
+        // (a family table too large for the 12-warp layout falls back to the staged kernel)
+        if (prm.layout == kLayoutPointMajor && smem_pm <= 227 * 1024) {
             auto kern = k_hash_m31_pm<LOGN, DIRECT>;
-            FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_pm)));
             int per_sm = 0;
-            FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+            FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WARPS, smem_pm));
             if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
             const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
-            const uint64_t grid = std::min<uint64_t>((groups + 7) / 8, uint64_t(per_sm) * sm_count(fs.device));
-            kern<<<unsigned(std::max<uint64_t>(grid, 1)), 256, smem, stream>>>(prm);
+            const uint64_t grid = std::min<uint64_t>((groups + WARPS - 1) / WARPS, uint64_t(per_sm) * sm_count(fs.device));
+            kern<<<unsigned(std::max<uint64_t>(grid, 1)), 32 * WARPS, smem_pm, stream>>>(prm);
             FCLSH_LAUNCHED();
             return;
         }
@@ -703,7 +726,9 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
                 const Family& f = families[p];
                 for (uint64_t j = 0; j < f.dims; ++j)
                     if (f.mapping[j] != 0)
-                        blob[size_t(p) * N + (f.mapping[j] % E) * G + f.mapping[j] / E] =
+                        // column c = g*E + j -> pair (j/2) of lane g, lanes fastest (16-byte loads)
+                        blob[size_t(p) * N + ((f.mapping[j] % E) / 2) * 2 * G + 2 * (f.mapping[j] / E) +
+                             (f.mapping[j] % E) % 2] =
                             make_uint2(uint32_t(plan.source_bit(p, j)), uint32_t(f.seeds[j]));
             }
         } else {

@@ -1,6 +1,7 @@
 """Small, ncu-friendly workload: cfg2 index + two query batches, and two
-1M-row chunks of the cfg5 hash. Used for the launch list and the
-`ncu --set full` captures under profiles/ (never a bench number)."""
+1M-row chunks of the cfg5 hash (point-major, as the bench). Used for the
+launch list and the `ncu --set full` captures under profiles/ (never a bench
+number)."""
 import os
 import sys
 
@@ -30,8 +31,8 @@ if what in ("all", "hash"):
     rows = F.gen_bernoulli(cfg5.root(), n, cfg5.dims)
     fam = F.build_covering_family(cfg5.dims, cfg5.radius, cfg5.index_seed(), prime=F.M31)
     d = torch.from_numpy(rows.view(np.int64)).cuda()
-    keys = torch.empty((fam.table_count(), n), dtype=torch.int32, device="cuda")
+    keys = torch.empty((n, fam.table_count()), dtype=torch.int32, device="cuda")
     for _ in range(2):
-        F.hash_batch_device(fam, d, keys, layout=0, key_stride=n)
+        F.hash_batch_device(fam, d, keys, layout=1, key_stride=fam.table_count())
     torch.cuda.synchronize()
 print("done")
