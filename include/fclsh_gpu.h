@@ -228,6 +228,22 @@ typedef struct {
 int fclsh_query_device(fclsh_index* ix, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
                        void* stream, fclsh_device_result* out);
 
+/* Copies a device result into caller device buffers (all on `device`):
+ * d_triples [3][cap] (rows: query, id, distance; cap >= r->total),
+ * d_offsets [nq+1], d_counters [3][nq] (rows: collisions, candidates, found).
+ * Any output pointer may be NULL. Asynchronous on `stream`. */
+int fclsh_result_copy_device(const fclsh_device_result* r, uint32_t* d_triples, uint64_t cap,
+                             uint64_t* d_offsets, uint64_t* d_counters, int device, void* stream);
+
+/* Multi-GPU result assembly (points sharded by contiguous id ranges in rank
+ * order): given every rank's offsets [world][nq+1] and triples
+ * [world][3][cap], writes the merged triples, ordered by (query, id), to
+ * d_out [3][out_cap] and their per-query offsets to d_out_offsets [nq+1].
+ * out_cap >= total over ranks. Asynchronous on `stream`. */
+int fclsh_merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, const uint32_t* d_triples,
+                       uint64_t cap, uint32_t* d_out, uint64_t out_cap, uint64_t* d_out_offsets, int device,
+                       void* stream);
+
 /* Device time (CUDA events, ms) of each stage of the last query on ix:
  * [0] hash (S1) [1] fused probe + dedup + verify (S2+S3, warp per query)
  * [2] general path for queries that overflowed the fused kernel

@@ -25,6 +25,9 @@ void gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, d
 void gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
                  uint64_t* qrows, uint32_t* src_out);
 
+void merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, const uint32_t* d_triples, uint64_t cap,
+                  uint32_t* d_out, uint64_t out_cap, uint64_t* d_out_offsets, cudaStream_t s, int device);
+
 uint64_t& launch_counter() {
     static thread_local uint64_t c = 0;
     return c;
@@ -367,6 +370,40 @@ int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, 
         out->d_collisions = o.d_coll;
         out->d_candidates = o.d_cand;
         out->d_found = o.d_found;
+    });
+}
+
+int fclsh_result_copy_device(const fclsh_device_result* r, uint32_t* d_triples, uint64_t cap, uint64_t* d_offsets,
+                             uint64_t* d_counters, int device, void* stream) {
+    return guarded([&] {
+        need(r, "result");
+        if (d_triples && cap < r->total) throw UsageError("result copy: cap below the triple count");
+        FCLSH_CUDA(cudaSetDevice(device));
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const uint64_t t = r->total, nq = r->nq;
+        if (d_triples && t) {
+            FCLSH_CUDA(cudaMemcpyAsync(d_triples, r->d_query, t * 4, cudaMemcpyDeviceToDevice, s));
+            FCLSH_CUDA(cudaMemcpyAsync(d_triples + cap, r->d_id, t * 4, cudaMemcpyDeviceToDevice, s));
+            FCLSH_CUDA(cudaMemcpyAsync(d_triples + 2 * cap, r->d_distance, t * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        if (d_offsets) FCLSH_CUDA(cudaMemcpyAsync(d_offsets, r->d_offsets, (nq + 1) * 8, cudaMemcpyDeviceToDevice, s));
+        if (d_counters && nq) {
+            FCLSH_CUDA(cudaMemcpyAsync(d_counters, r->d_collisions, nq * 8, cudaMemcpyDeviceToDevice, s));
+            FCLSH_CUDA(cudaMemcpyAsync(d_counters + nq, r->d_candidates, nq * 8, cudaMemcpyDeviceToDevice, s));
+            FCLSH_CUDA(cudaMemcpyAsync(d_counters + 2 * nq, r->d_found, nq * 8, cudaMemcpyDeviceToDevice, s));
+        }
+    });
+}
+
+int fclsh_merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, const uint32_t* d_triples, uint64_t cap,
+                       uint32_t* d_out, uint64_t out_cap, uint64_t* d_out_offsets, int device, void* stream) {
+    return guarded([&] {
+        if (world == 0) throw UsageError("merge: world must be >= 1");
+        need(d_offsets, "d_offsets");
+        need(d_out_offsets, "d_out_offsets");
+        FCLSH_CUDA(cudaSetDevice(device));
+        merge_shards(world, nq, d_offsets, d_triples, cap, d_out, out_cap, d_out_offsets,
+                     static_cast<cudaStream_t>(stream), device);
     });
 }
 

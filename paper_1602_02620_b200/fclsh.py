@@ -295,6 +295,27 @@ class DeviceQueryResults:
     d_collisions: int
     d_candidates: int
     d_found: int
+    raw: object = None  # the C struct (for fclsh_result_copy_device)
+
+    def copy_to(self, triples=None, offsets=None, counters=None, device: int = 0, stream=None) -> None:
+        """Copy into caller CUDA tensors: triples int32 [3, cap], offsets int64 [nq+1],
+        counters int64 [3, nq] (collisions, candidates, found)."""
+        cap = triples.shape[1] if triples is not None else 0
+        _check(N.lib().fclsh_result_copy_device(
+            C.byref(self.raw), C.c_void_p(triples.data_ptr() if triples is not None else 0), cap,
+            C.c_void_p(offsets.data_ptr() if offsets is not None else 0),
+            C.c_void_p(counters.data_ptr() if counters is not None else 0), device, _stream_ptr(stream)))
+
+
+def merge_shards(offsets_all, triples_all, out_triples, out_offsets, device: int = 0, stream=None) -> None:
+    """fclsh_merge_shards over CUDA tensors: offsets_all int64 [world, nq+1],
+    triples_all int32 [world, 3, cap] -> out_triples int32 [3, out_cap],
+    out_offsets int64 [nq+1] (rank runs in rank order = (query, id) order)."""
+    world, nq1 = offsets_all.shape
+    _check(N.lib().fclsh_merge_shards(world, nq1 - 1, C.c_void_p(offsets_all.data_ptr()),
+                                      C.c_void_p(triples_all.data_ptr()), triples_all.shape[2],
+                                      C.c_void_p(out_triples.data_ptr()), out_triples.shape[1],
+                                      C.c_void_p(out_offsets.data_ptr()), device, _stream_ptr(stream)))
 
 
 class IndexSet:
@@ -377,7 +398,7 @@ class IndexSet:
                                           _stream_ptr(stream), C.byref(out)))
         return DeviceQueryResults(int(out.nq), int(out.total), out.d_query or 0, out.d_id or 0,
                                   out.d_distance or 0, out.d_offsets or 0, out.d_collisions or 0,
-                                  out.d_candidates or 0, out.d_found or 0)
+                                  out.d_candidates or 0, out.d_found or 0, out)
 
 
 def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, prime: int = M61,
