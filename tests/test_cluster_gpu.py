@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def test_merge_shards_equals_single_index(shards):
     rng = np.random.default_rng(shards)
     n, d, r = 6000, 256, 8
-    rows = F.gen_clustered(shards, 40, n, d, 0.04)  # dense neighbourhoods: many results per query
+    rows = F.gen_clustered(shards, 40, n, d, 0.01)  # dense neighbourhoods: many results per query
     q = planted_queries(rng, rows, d, 200, 10)
     plan = F.make_plan(d, r, 1.0, n, 5, F.PlanOverride(F.PlanKind.partition, 2))
     full = F.build_index(rows, r, plan, 6, prime=F.M31).query_r_nn(q, r)
