@@ -41,6 +41,20 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 
 
+def measured_traffic(prefix: str):
+    """DRAM bytes per launch (read + write) of a kernel from the newest
+    committed ncu --set full capture (profiles/rNN/traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            for k, v in json.load(open(path)).items():
+                if k.startswith(prefix):
+                    return int(v["dram_read_bytes"] + v["dram_write_bytes"]), os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def hbm_peak():
     try:
         p = json.load(open(PEAKS_PATH))
@@ -50,59 +64,62 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed regions (the
+    same fields as the nvidia-smi clocks line of the profiling recipe), via
+    NVML polled every ~1 ms from a thread: the timed regions here are
+    milliseconds long, too short for nvidia-smi's 200-ms loop. Reentrant:
+    `with sampler:` around each timed region accumulates samples."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, const in self.REASONS.items():
+                    if r & getattr(nv, const):
+                        self.reasons.add(name)
+            except Exception:
+                return
+            time.sleep(0.001)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        if self.nv is not None:
+            self._stop.clear()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self._t is not None:
+            self._stop.set()
+            self._t.join()
+            self._t = None
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "NVML, 1 ms polling during the timed regions"}
 
 
 def dist_setup(args):
@@ -255,7 +272,8 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev) as clocks:
+    clocks = ClockSampler(dev)
+    with clocks:
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)
@@ -292,9 +310,11 @@ def main():
     roofline = None
     if dom_bytes is not None:
         ach = dom_bytes / (stage_avg[dominant] / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "peak_source": peak_src,
-                    "algorithmic_bytes_per_launch": dom_bytes}
+        traffic, tsrc = measured_traffic("k_query_fused") if dominant == "fused" else (None, None)
+        roofline = {"bound": "hbm", "kernel": "k_query_fused" if dominant == "fused" else dominant,
+                    "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                    "traffic_source": tsrc, "peak_source": peak_src, "algorithmic_bytes_per_launch": dom_bytes,
+                    "duration_ms": stage_avg[dominant]}
     stage_rooflines = {k: {"ms": stage_avg[k], "GB/s": algo[k] / (stage_avg[k] / 1e3) / 1e9,
                            "frac": algo[k] / (stage_avg[k] / 1e3) / 1e9 / hbm}
                        for k in algo if stage_avg.get(k, 0) > 0}
@@ -334,7 +354,7 @@ def main():
     # ---------------- hash microbenchmark (cfg5)
     hash_block = None
     if not args.no_hash:
-        hash_block = bench_hash(F, CONFIGS[5], dev, args, hbm, peak_src, flush, stream, threads)
+        hash_block = bench_hash(F, CONFIGS[5], dev, args, hbm, peak_src, flush, stream, threads, clocks)
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -344,7 +364,7 @@ def main():
         "config": config_block(cfg, world),
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
         "gpu_launches_note": "own kernels only; CUB scan/segmented-sort launches are not counted",
-        "clocks": clocks.summary(), "parity_vs_reference": parity,
+        "clocks": None, "parity_vs_reference": parity,
         "stages_ms": stage_avg, "stage_rooflines": stage_rooflines,
         "counters": {"collisions_mean": float(coll.mean()), "candidates_mean": float(cand.mean()),
                      "found_total": int(found.sum())},
@@ -352,13 +372,14 @@ def main():
                   "device_bytes": ix.device_bytes},
         "hash": hash_block,
     }
+    line["clocks"] = clocks.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
+def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads, clocks):
     """cfg5: 8M x 1024-bit rows, r = 10 -> 2047 keys per row, point-major in
     1M-row chunks. Step = all chunks. Algorithmic bytes = rows read once +
     every key written once = n * (d/8 + L*4)."""
@@ -383,10 +404,11 @@ def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
     for _ in range(args.steps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b.record(stream)
-        torch.cuda.synchronize()
+        with clocks:
+            a.record(stream)
+            step()
+            b.record(stream)
+            torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
     avg = statistics.mean(ms)
     algo_bytes = n * (cfg5.dims / 8 + L * 4)
@@ -407,8 +429,11 @@ def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads):
     return {"metric": "fcLSH hash keys/sec (cfg5: 8M x 1024-bit rows, r=10, L=2047, 32-bit keys)",
             "value": n * L / (avg / 1e3), "unit": "keys/s", "ms_per_step": avg, "points": n, "chunk": chunk,
             "roofline": {"bound": "hbm", "kernel": "k_hash_m31_pm<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": None, "peak_source": peak_src,
-                         "algorithmic_bytes_per_step": algo_bytes},
+                         "frac": ach / hbm, "traffic": measured_traffic("k_hash_m31_pm<11")[0],
+                         "traffic_unit": "bytes per launch (one 1M-row chunk)",
+                         "traffic_source": measured_traffic("k_hash_m31_pm<11")[1], "peak_source": peak_src,
+                         "algorithmic_bytes_per_step": algo_bytes,
+                         "algorithmic_bytes_per_launch": chunk * (cfg5.dims / 8 + L * 4)},
             "keys_match_oracle_sample": check}
 
 

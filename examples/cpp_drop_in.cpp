@@ -1,0 +1,45 @@
+// Reference-style C++ caller of the B200 engine through include/fclsh_gpu.hpp.
+// Mirrors the reference CLI `build` seed chain (tools/fclsh.cpp:248-263):
+// plan seed = Rng(seed).stream("run",0).stream("plan"), index seed = ...("index").
+// Usage: cpp_drop_in [--host-only]
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "fclsh_gpu.hpp"
+
+int main(int argc, char** argv) {
+    namespace G = fclsh::gpu;
+    const bool host_only = argc > 1 && std::strcmp(argv[1], "--host-only") == 0;
+    const uint64_t seed = 42, n = 20000, d = 128;
+    const uint32_t r = 4;
+    const uint64_t run = fclsh_rng_stream_index(seed, "run", 0);
+    const uint64_t plan_seed = fclsh_rng_stream(run, "plan"), index_seed = fclsh_rng_stream(run, "index");
+    try {
+        auto fam = G::build_covering_family(d, r, fclsh_rng_stream_index(index_seed, "family", 0), G::kMersenne31);
+        auto m = fam.mapping();
+        auto s = fam.seeds();
+        std::printf("family tables=%llu mapping0=%u seed0=%llu\n", (unsigned long long)fam.table_count(), m[0],
+                    (unsigned long long)s[0]);
+        fclsh_plan_override ov{FCLSH_PLAN_IDENTITY, 1};
+        auto plan = G::make_plan(d, r, 1.0, n, plan_seed, &ov);
+        std::printf("plan tables=%llu\n", (unsigned long long)plan.info().table_count);
+        try {
+            G::make_plan(d, 0, 1.0, n, plan_seed);
+        } catch (const G::UsageError& e) {
+            std::printf("usage error ok: %s\n", e.what());
+        }
+        if (host_only) return 0;
+        std::vector<uint64_t> rows(n * (d / 64));
+        fclsh_gen_bernoulli(seed, n, d, rows.data(), 4);
+        std::vector<uint64_t> q(rows.begin(), rows.begin() + 10 * (d / 64)); // 10 queries = data rows
+        auto ix = G::build_index(rows.data(), n, d, r, plan, index_seed, G::kMersenne31);
+        auto res = ix.query_r_nn(q.data(), 10, r);
+        std::printf("index tables=%llu found0=%llu first_id=%u total=%zu\n", (unsigned long long)ix.table_count(),
+                    (unsigned long long)res.found[0], res.id.empty() ? 0u : res.id[0], res.id.size());
+        return (res.found[0] >= 1 && res.id[0] == 0) ? 0 : 1;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 2;
+    }
+}
