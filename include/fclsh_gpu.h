@@ -246,8 +246,9 @@ int fclsh_merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, c
 
 /* Device time (CUDA events, ms) of each stage of the last query on ix:
  * [0] hash (S1) [1] fused probe + dedup + verify (S2+S3, warp per query)
- * [2] general path for queries that overflowed the fused kernel
- * [3] found scan [4] compaction. Writes min(n, 5) values; returns the number
+ * [2] found scan [3] compaction [4] general path for queries that
+ * overflowed the fused kernel (with its rescan/recompaction; includes the
+ * host round trip that discovers them). Writes min(n, 5) values; returns the number
  * written (negative on error). */
 int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n);
 

@@ -402,7 +402,11 @@ __global__ void __launch_bounds__(256) k_query_fused(
         __syncwarp();
         const uint32_t m = cnt_s[warp];
         if (m > CAP) {
-            if (lane == 0) overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+            if (lane == 0) {
+                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                found_q[q] = 0; // written by the general path later
+                src_pos[q] = 0;
+            }
             continue;
         }
         // dedup: ascending-only bitonic sort of the list (padding = +inf)
@@ -465,7 +469,11 @@ __global__ void __launch_bounds__(256) k_query_fused(
             nfound += __popc(bp);
         }
         if (nfound > slot_cap) {
-            if (lane == 0) overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+            if (lane == 0) {
+                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                found_q[q] = 0; // written by the general path later
+                src_pos[q] = 0;
+            }
             continue;
         }
         if (lane == 0) {
@@ -726,11 +734,42 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                           tmp_id, tmp_dist, ovf, ovf_cnt, s);
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
-    unsigned int ns = 0;
-    FCLSH_CUDA(cudaMemcpyAsync(&ns, ovf_cnt, 4, cudaMemcpyDeviceToHost, s));
-    FCLSH_CUDA(cudaStreamSynchronize(s));
+    // Common path, one host sync: scan the per-query found counts (overflowing
+    // queries count 0 here) and compact into buffers sized for the fused
+    // results (<= nq * slot_cap), then read the overflow count and the total.
+    auto scan_found = [&] {
+        FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
+        size_t tmp_bytes = 0;
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found_q, res_off, nq + 1, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found_q, res_off, nq + 1, s));
+    };
     uint32_t* tmp2_id = tmp_id;
     uint32_t* tmp2_dist = tmp_dist;
+    uint64_t out_cap = std::max<uint64_t>(1, nq * slot_cap);
+    auto compact = [&] {
+        uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
+        uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
+        uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
+        if (nq) {
+            k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist,
+                                                                   nq * slot_cap, tmp2_id, tmp2_dist, ix.id_offset,
+                                                                   oq, oi, od);
+            FCLSH_LAUNCHED();
+        }
+    };
+    scan_found();
+    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
+    compact();
+    FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
+    struct {
+        unsigned long long total;
+        unsigned int ns;
+    } hs{0, 0};
+    FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaMemcpyAsync(&hs.ns, ovf_cnt, 4, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    const unsigned int ns = hs.ns;
+    unsigned long long total = hs.total;
     if (ns) {
         // general path for the overflowing queries
         const uint64_t pairs = uint64_t(ns) * T_;
@@ -766,29 +805,19 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap, tmp2_id,
             tmp2_dist, coll_q, cand_q, found_q, src_pos);
         FCLSH_LAUNCHED();
-    }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
-    FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
-    size_t tmp_bytes = 0;
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found_q, res_off, nq + 1, s));
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found_q, res_off, nq + 1, s));
-    FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
-    unsigned long long total = 0;
-    FCLSH_CUDA(cudaMemcpyAsync(&total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
-    FCLSH_CUDA(cudaStreamSynchronize(s));
-    uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(std::max<uint64_t>(1, total) * 4));
-    uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(std::max<uint64_t>(1, total) * 4));
-    uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(std::max<uint64_t>(1, total) * 4));
-    if (total) {
-        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap,
-                                                               tmp2_id, tmp2_dist, ix.id_offset, oq, oi, od);
-        FCLSH_LAUNCHED();
+        // the overflowing queries' counts are in now: scan and compact again
+        scan_found();
+        FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaStreamSynchronize(s));
+        total = hs.total;
+        out_cap = std::max<uint64_t>(out_cap, total);
+        compact();
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
     out.total = total;
-    out.d_query = oq;
-    out.d_id = oi;
-    out.d_dist = od;
+    out.d_query = ix.out_q.as<uint32_t>();
+    out.d_id = ix.out_id.as<uint32_t>();
+    out.d_dist = ix.out_dist.as<uint32_t>();
     out.d_offsets = reinterpret_cast<uint64_t*>(res_off);
     out.d_coll = reinterpret_cast<uint64_t*>(coll_q);
     out.d_cand = reinterpret_cast<uint64_t*>(cand_q);
@@ -923,8 +952,8 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         ix.stage_ms[i] = ms;
     }
     ix.t_hash_ms = ix.stage_ms[0];
-    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2]; // probe + dedup + verify are fused
-    ix.t_verify_ms = ix.stage_ms[3] + ix.stage_ms[4];
+    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[4]; // probe + dedup + verify are fused
+    ix.t_verify_ms = ix.stage_ms[2] + ix.stage_ms[3]; // result assembly
     return o;
 }
 

@@ -54,8 +54,8 @@ struct DeviceIndex {
     uint64_t last_overflow = 0; // queries that took the general path
     double t_hash_ms = 0, t_probe_ms = 0, t_verify_ms = 0;
     // device time of the last query per stage: hash (S1), fused
-    // probe+dedup+verify (S2+S3), general path for overflowing queries,
-    // found scan, compaction
+    // probe+dedup+verify (S2+S3), found scan, compaction, general path for
+    // overflowing queries (+ its rescan / recompaction; includes one host sync)
     static constexpr int kStages = 5;
     double stage_ms[kStages] = {};
     cudaEvent_t ev[kStages + 1] = {};

@@ -381,7 +381,7 @@ class IndexSet:
             N.lib().fclsh_result_free(rp)
         return res
 
-    STAGES = ("hash", "fused", "overflow", "found_scan", "compact")
+    STAGES = ("hash", "fused", "found_scan", "compact", "overflow")
 
     def stage_ms(self) -> dict:
         """Device time per stage of the last query (CUDA events)."""
