@@ -213,6 +213,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-hash", action="store_true", help="skip the cfg5 hash microbenchmark")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1/3/4 query measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--hash-points", type=int, default=8_000_000)
     ap.add_argument("--ref-sample", type=int, default=2000)
@@ -356,6 +357,23 @@ def main():
     if not args.no_hash:
         hash_block = bench_hash(F, CONFIGS[5], dev, args, hbm, peak_src, flush, stream, threads, clocks)
 
+    # ---------------- the other BASELINE query configs (1, 3, 4), same step definition
+    others = None
+    if not args.no_configs and world == 1:
+        build_info = {"device_ms": ix.build_ms, "wall_s": build_wall, "entries": ix.entry_count(),
+                      "device_bytes": ix.device_bytes, "layout": ix.layout}
+        del ix
+        torch.cuda.empty_cache()
+        others = {}
+        for cid in (1, 3, 4):
+            try:
+                others[f"cfg{cid}"] = bench_query_config(F, CONFIGS[cid], dev, args, flush, stream, threads, clocks)
+            except Exception as e:  # noqa: BLE001
+                others[f"cfg{cid}"] = {"error": str(e)}
+    else:
+        build_info = {"device_ms": ix.build_ms, "wall_s": build_wall, "entries": ix.entry_count(),
+                      "device_bytes": ix.device_bytes, "layout": ix.layout}
+
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -368,15 +386,79 @@ def main():
         "stages_ms": stage_avg, "stage_rooflines": stage_rooflines,
         "counters": {"collisions_mean": float(coll.mean()), "candidates_mean": float(cand.mean()),
                      "found_total": int(found.sum())},
-        "build": {"device_ms": ix.build_ms, "wall_s": build_wall, "entries": ix.entry_count(),
-                  "device_bytes": ix.device_bytes},
+        "build": build_info,
         "hash": hash_block,
+        "configs": others,
     }
     line["clocks"] = clocks.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _time_queries(ix, qd, radius, args, flush, stream, clocks):
+    import torch
+    for _ in range(2):
+        ix.query_device(qd, radius, stream)
+    ms, stages = [], []
+    for _ in range(max(3, args.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with clocks:
+            a.record(stream)
+            ix.query_device(qd, radius, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+        stages.append(ix.stage_ms())
+    return statistics.mean(ms), {k: statistics.mean(s[k] for s in stages) for k in stages[0]}
+
+
+def bench_query_config(F, cfg, dev, args, flush, stream, threads, clocks):
+    """cfg1 / cfg3 / cfg4 with the headline step definition (one query_r_nn
+    pass over the config's whole query set, rows in HBM). cfg4 is measured as
+    one 10M-point index on this GPU (the CSR layout when buckets do not fit)
+    and as the 8-shard layout of BASELINE cfg4, shard by shard: the 8-GPU
+    critical path is the slowest shard plus the device merge (the NCCL
+    exchange is not in that figure)."""
+    import torch
+
+    from paper_1602_02620_b200 import cluster
+    from paper_1602_02620_b200.configs import make_data, make_queries
+    data = make_data(cfg, threads)
+    q = make_queries(cfg, data, threads)
+    nq = q.shape[0]
+    qd = torch.from_numpy(q.view(np.int64)).to(f"cuda:{dev}")
+    plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg.plan_seed(), cfg.override())
+    out = {"n": cfg.n, "d": cfg.dims, "r": cfg.radius, "plan": cfg.plan_kind.name, "t": cfg.t, "tables": cfg.tables,
+           "queries": nq}
+    ix = F.build_index(data, cfg.radius, plan, cfg.index_seed(), prime=F.M31, device=dev)
+    ms, stages = _time_queries(ix, qd, cfg.radius, args, flush, stream, clocks)
+    paths = ix.path_counts()
+    res = ix.query_r_nn(q, cfg.radius)
+    out.update({"queries_per_s": nq / (ms / 1e3), "ms_per_step": ms, "stages_ms": stages, "query_paths": paths,
+                "build_device_ms": ix.build_ms, "layout": ix.layout, "device_bytes": ix.device_bytes,
+                "collisions_mean": float(res.collisions.mean()), "candidates_mean": float(res.candidates.mean()),
+                "found_mean": float(res.found.mean())})
+    del ix
+    torch.cuda.empty_cache()
+    if cfg.shards > 1:
+        shard_ms, shard_build = [], []
+        for r in range(cfg.shards):
+            b, e = cluster.shard_range(cfg.n, cfg.shards, r)
+            six = F.build_index(data[b:e], cfg.radius, plan, cfg.index_seed(), prime=F.M31, device=dev, id_offset=b)
+            m, _ = _time_queries(six, qd, cfg.radius, args, flush, stream, clocks)
+            shard_ms.append(m)
+            shard_build.append(six.build_ms)
+            del six
+            torch.cuda.empty_cache()
+        out["sharded"] = {"shards": cfg.shards, "shard_query_ms": shard_ms, "shard_build_ms": shard_build,
+                          "critical_path_ms": max(shard_ms),
+                          "queries_per_s_8gpu_estimate": nq / (max(shard_ms) / 1e3),
+                          "note": "shards run one after another on this GPU; NCCL exchange not included"}
+    return out
 
 
 def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads, clocks):

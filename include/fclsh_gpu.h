@@ -246,11 +246,18 @@ int fclsh_merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, c
 
 /* Device time (CUDA events, ms) of each stage of the last query on ix:
  * [0] hash (S1) [1] fused probe + dedup + verify (S2+S3, warp per query)
- * [2] found scan [3] compaction [4] general path for queries that
- * overflowed the fused kernel (with its rescan/recompaction; includes the
- * host round trip that discovers them). Writes min(n, 5) values; returns the number
+ * [2] the same fused, CTA per query, for the dense queries [1] handed over
+ * [3] found scan [4] compaction [5] general path for queries that
+ * overflowed both (with its rescan/recompaction; includes the host round
+ * trip that discovers them). Writes min(n, 6) values; returns the number
  * written (negative on error). */
 int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n);
+
+/* How the last query on ix was served: *dense = queries handed from the
+ * warp-per-query kernel to the CTA-per-query kernel, *general = queries
+ * that went on to the general (sort-based) path. Either pointer may be
+ * NULL. Returns 0 or a negative error code. */
+int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* general);
 
 /* Number of kernels the library launched on this thread since the last
  * reset (launch accounting for the bench). */

@@ -417,6 +417,16 @@ int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n) {
     return k;
 }
 
+int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* general) {
+    if (!ix) {
+        g_err = "fclsh_query_path_counts: NULL index";
+        return -FCLSH_ERR_USAGE;
+    }
+    if (dense) *dense = ix->ix->last_dense;
+    if (general) *general = ix->ix->last_overflow;
+    return 0;
+}
+
 uint64_t fclsh_launch_count(void) { return launch_counter(); }
 void fclsh_launch_count_reset(void) { launch_counter() = 0; }
 

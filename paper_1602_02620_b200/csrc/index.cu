@@ -81,6 +81,24 @@ struct WideEntry { // 8-byte keys: {key, id}
 
 constexpr int kSlots = 4; // per bucket
 
+// One bucket (4 slots) with 256-bit loads: a random probe is one L1 request
+// for the narrow layout (two for wide) instead of four 64-bit ones; the
+// tables are read-only while queries run (.nc). tools/rand_bench.cu measures
+// the random-access ceiling this targets.
+__device__ __forceinline__ void load_bucket(const unsigned long long* bp, unsigned long long (&x)[kSlots]) {
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3])
+        : "l"(bp));
+}
+__device__ __forceinline__ void load_bucket(const ulonglong2* bp, ulonglong2 (&x)[kSlots]) {
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(x[0].x), "=l"(x[0].y), "=l"(x[1].x), "=l"(x[1].y)
+        : "l"(bp));
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(x[2].x), "=l"(x[2].y), "=l"(x[3].x), "=l"(x[3].y)
+        : "l"(bp + 2));
+}
+
 // Read-only view of one shard's tables, passed by value to the kernels.
 template <typename T>
 struct Tables {
@@ -112,10 +130,8 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
         uint64_t b = key >> tb.shift;
         const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
         for (;;) {
-            const E* bp = base + b * kSlots;
             E s[kSlots];
-#pragma unroll
-            for (int j = 0; j < kSlots; ++j) s[j] = bp[j];
+            load_bucket(base + b * kSlots, s);
 #pragma unroll
             for (int j = 0; j < kSlots; ++j)
                 if (!T::empty(s[j]) && T::key(s[j]) == key) {
@@ -315,7 +331,7 @@ __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ d
 // K3+K4+K5 fused, one warp per query (the common path). A query whose list
 // exceeds CAP or whose results exceed slot_cap is queued for the general
 // path (overflow list), which then writes all of that query's outputs.
-template <typename T, int LAYOUT, int CAP>
+template <typename T, int LAYOUT, int CAP, int U>
 __global__ void __launch_bounds__(256) k_query_fused(
     const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -336,17 +352,17 @@ __global__ void __launch_bounds__(256) k_query_fused(
             const uint32_t pos = atomicAdd(cnt_s + warp, 1u);
             if (pos < CAP) ids[pos] = id;
         };
-        for (uint32_t t0 = 0; t0 < tables; t0 += 128) {
-            uint64_t key[4];
+        for (uint32_t t0 = 0; t0 < tables; t0 += 32 * U) {
+            uint64_t key[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const uint32_t t = t0 + u * 32 + lane;
                 key[u] = t < tables ? uint64_t(qk[t]) : 0ull;
             }
             if constexpr (LAYOUT == kLayoutCsr) {
-                uint32_t s[4], e[4];
+                uint32_t s[U], e[U];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) { // four directory lookups in flight
+                for (int u = 0; u < U; ++u) { // U directory lookups in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t < tables) {
                         const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key[u] >> tb.shift);
@@ -357,25 +373,23 @@ __global__ void __launch_bounds__(256) k_query_fused(
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const E* et = tb.data + uint64_t(t0 + u * 32 + lane) * tb.n;
                     uint32_t a = s[u];
                     while (a < e[u] && T::key(et[a]) < key[u]) ++a;
                     while (a < e[u] && T::key(et[a]) == key[u]) push(T::id(et[a++]));
                 }
             } else {
-                E sl[4][kSlots];
+                E sl[U][kSlots];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) { // four home buckets in flight
+                for (int u = 0; u < U; ++u) { // U home buckets in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t < tables) {
-                        const E* bp = tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots;
-#pragma unroll
-                        for (int j = 0; j < kSlots; ++j) sl[u][j] = bp[j];
+                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t >= tables) continue;
 #pragma unroll
@@ -386,10 +400,8 @@ __global__ void __launch_bounds__(256) k_query_fused(
                         const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
                         for (;;) {
                             b = (b + 1) & (tb.nbuckets - 1);
-                            const E* bp = base + b * kSlots;
                             E x[kSlots];
-#pragma unroll
-                            for (int j = 0; j < kSlots; ++j) x[j] = bp[j];
+                            load_bucket(base + b * kSlots, x);
 #pragma unroll
                             for (int j = 0; j < kSlots; ++j)
                                 if (!T::empty(x[j]) && T::key(x[j]) == key[u]) push(T::id(x[j]));
@@ -398,6 +410,8 @@ __global__ void __launch_bounds__(256) k_query_fused(
                     }
                 }
             }
+            __syncwarp();
+            if (cnt_s[warp] > CAP) break; // overflowing: the dense kernel redoes it
         }
         __syncwarp();
         const uint32_t m = cnt_s[warp];
@@ -485,6 +499,128 @@ __global__ void __launch_bounds__(256) k_query_fused(
     }
 }
 
+// Dense queries (clustered data, cfg4): one CTA per query. Dedup is a
+// shared-memory open-addressing id set instead of a sort of the collision
+// list, so the cost follows the distinct candidates (cfg4: ~480) rather than
+// the collisions (~1900). Phase 1 probes (thread per table) and inserts into
+// the set; phase 2 walks the set, verifying four candidates per thread at a
+// time (independent row loads in flight), and appends (id << 32 | dist) to a
+// shared found list; only that list is sorted (ascending ids,
+// index.cpp:171-186). Queries: ovf[0 .. *ovf_cnt) (the warp kernel's
+// hand-over, count read on the device), or every query 0 .. direct_n when
+// ovf is null. A query with 3/4 * HS or more distinct candidates or more
+// than FCAP results, or whose results do not fit the region, goes to the
+// general path (ovf2), which recomputes all its outputs.
+template <typename T, int LAYOUT, int HS, int FCAP>
+__global__ void __launch_bounds__(512) k_query_dense(
+    const typename T::K* __restrict__ qkeys, uint32_t tables, const Tables<T> tb, const uint64_t* __restrict__ rows,
+    const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius, const uint32_t* __restrict__ ovf,
+    const unsigned int* __restrict__ ovf_cnt, uint32_t direct_n, unsigned long long* __restrict__ coll_q,
+    unsigned long long* __restrict__ cand_q, unsigned long long* __restrict__ found_q,
+    unsigned long long* __restrict__ src_pos, uint64_t src_base, uint32_t* __restrict__ res_id,
+    uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
+    uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
+    uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
+    __shared__ unsigned int coll_s, cand_s, found_s;
+    __shared__ volatile int bad_s;
+    __shared__ unsigned long long base_s;
+    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+    constexpr uint32_t kMaxDistinct = HS / 4 * 3;
+    constexpr int kV = 4; // candidates verified per thread at a time (one LDS.128)
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const unsigned int ns = ovf ? *ovf_cnt : direct_n;
+    for (uint32_t s_ = blockIdx.x; s_ < ns; s_ += gridDim.x) {
+        const uint64_t q = ovf ? ovf[s_] : s_;
+        for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
+        if (tid == 0) {
+            coll_s = cand_s = found_s = 0;
+            bad_s = 0;
+        }
+        __syncthreads();
+        // phase 1: probe, dedup into the set
+        const typename T::K* qk = qkeys + q * tables;
+        uint32_t coll = 0;
+        for (uint32_t t = tid; t < tables; t += nt) {
+            if (bad_s) break;
+            coll += probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), [&](uint32_t id) {
+                if (bad_s) return; // the set holds at most kMaxDistinct + nt ids
+                uint32_t h = (id * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
+                for (;;) {
+                    const uint32_t old = atomicCAS(set + h, kEmpty, id);
+                    if (old == id) return; // seen
+                    if (old == kEmpty) break;
+                    h = (h + 1) & (HS - 1);
+                }
+                if (atomicAdd(&cand_s, 1u) >= kMaxDistinct) bad_s = 1;
+            });
+        }
+        atomicAdd(&coll_s, coll);
+        __syncthreads();
+        // phase 2: verify the distinct candidates
+        if (!bad_s) {
+            const uint64_t* qr = qrows + q * words;
+            for (uint32_t i0 = tid * kV; i0 < HS; i0 += nt * kV) {
+                const uint4 v = *reinterpret_cast<const uint4*>(set + i0);
+                uint32_t id[kV] = {v.x, v.y, v.z, v.w}, d[kV] = {0, 0, 0, 0};
+                for (uint32_t w = 0; w < words; ++w) {
+                    const uint64_t qw = __ldg(qr + w);
+#pragma unroll
+                    for (int u = 0; u < kV; ++u)
+                        if (id[u] != kEmpty) d[u] += __popcll(__ldg(rows + uint64_t(id[u]) * words + w) ^ qw);
+                }
+#pragma unroll
+                for (int u = 0; u < kV; ++u)
+                    if (id[u] != kEmpty && d[u] <= radius) {
+                        const uint32_t pos = atomicAdd(&found_s, 1u);
+                        if (pos < FCAP)
+                            fl[pos] = (static_cast<unsigned long long>(id[u]) << 32) | d[u];
+                        else
+                            bad_s = 1;
+                    }
+            }
+        }
+        __syncthreads();
+        const uint32_t nf = found_s;
+        if (tid == 0) {
+            bool bad = bad_s;
+            base_s = 0;
+            if (!bad && nf) {
+                base_s = atomicAdd(res_cursor, (unsigned long long)nf);
+                bad = base_s + nf > res_cap; // region full
+            }
+            if (bad) {
+                ovf2[atomicAdd(ovf2_cnt, 1u)] = uint32_t(q);
+                found_q[q] = 0; // written by the general path later
+                src_pos[q] = 0;
+                bad_s = 1;
+            } else {
+                coll_q[q] = coll_s;
+                cand_q[q] = cand_s;
+                found_q[q] = nf;
+                src_pos[q] = src_base + base_s;
+            }
+        }
+        __syncthreads();
+        if (!bad_s && nf) {
+            uint32_t P = 1;
+            while (P < nf) P <<= 1;
+            for (uint32_t i = nf + tid; i < P; i += nt) fl[i] = ~0ull;
+            __syncthreads();
+            bitonic_sort<NarrowEntry>(fl, P, P);
+            const uint64_t base = base_s;
+            for (uint32_t k = tid; k < nf; k += nt) {
+                const unsigned long long e = fl[k];
+                res_id[base + k] = uint32_t(e >> 32);
+                res_dist[base + k] = uint32_t(e);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+
 // General path for the selected queries qsel[0..ns): per (query, table)
 // counts -> per-query collision totals; scan; gather the ids; CUB segmented
 // sort; verify.
@@ -565,9 +701,12 @@ __global__ void k_verify_sel(uint64_t ns, const uint32_t* __restrict__ qsel,
 
 // Copies every query's results (slot of the fused path, or region of the
 // general path) to its place in the (query, id) ordered output.
+// Result sources by src_pos: [0, tmp_len) warp-kernel slots, [tmp_len,
+// tmp_len + cta_len) the CTA kernel's region, beyond: the general path.
 __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ src_pos,
                           const unsigned long long* __restrict__ res_off, const uint32_t* __restrict__ tmp_id,
-                          const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len, const uint32_t* __restrict__ tmp2_id,
+                          const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len, const uint32_t* __restrict__ cta_id,
+                          const uint32_t* __restrict__ cta_dist, uint64_t cta_len, const uint32_t* __restrict__ tmp2_id,
                           const uint32_t* __restrict__ tmp2_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
                           uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist) {
     const uint32_t lane = threadIdx.x & 31;
@@ -578,10 +717,14 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
         uint64_t src = src_pos[q];
         const uint32_t* ti = tmp_id;
         const uint32_t* td = tmp_dist;
-        if (src >= tmp_len) {
-            src -= tmp_len;
+        if (src >= tmp_len + cta_len) {
+            src -= tmp_len + cta_len;
             ti = tmp2_id;
             td = tmp2_dist;
+        } else if (src >= tmp_len) {
+            src -= tmp_len;
+            ti = cta_id;
+            td = cta_dist;
         }
         for (uint64_t k = lane; k < cnt; k += 32) {
             out_q[dst + k] = uint32_t(q);
@@ -685,7 +828,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, cudaStream_t s) {
-    auto kern = k_query_fused<T, LAYOUT, CAP>;
+    auto kern = k_query_fused<T, LAYOUT, CAP, 4>;
     const size_t smem = (8 + size_t(8) * CAP) * 4;
     FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
@@ -698,6 +841,30 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     FCLSH_LAUNCHED();
 }
 
+constexpr int kDenseSet = 8192;   // id-set slots per dense query (< 6144 distinct candidates)
+constexpr int kDenseFound = 2048; // results per dense query
+constexpr int kDenseThreads = 512;
+
+template <typename T, int LAYOUT>
+void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint32_t radius,
+                const uint32_t* ovf, const unsigned int* ovf_cnt, uint64_t direct_n, unsigned long long* coll_q,
+                unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
+                uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
+                unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, cudaStream_t s) {
+    auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
+    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4;
+    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem));
+    // persistent grid: the overflow count is only known on the device
+    uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
+    if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
+    kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
+                                                     d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
+                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt);
+    FCLSH_LAUNCHED();
+}
+
 template <typename T, int LAYOUT>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
     using K = typename T::K;
@@ -705,7 +872,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     out.nq = nq;
     const uint64_t T_ = ix.tables;
     const bool big = T_ > 600;
-    const uint32_t slot_cap = big ? 128 : 32;
+    const uint32_t slot_cap = 32; // results per query in the warp kernel's slots
     K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
     auto* coll_q = static_cast<unsigned long long*>(ix.coll.ensure((nq + 1) * 8));
     auto* cand_q = static_cast<unsigned long long*>(ix.cand_cnt.ensure((nq + 1) * 8));
@@ -715,7 +882,15 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* tmp_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
     uint32_t* tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
     uint32_t* ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
+    uint32_t* ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
+    // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
+    // count, bytes 8..15: the CTA kernel's result cursor
     auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(16));
+    auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
+    // CTA-kernel result region; queries that do not fit go on to the general path
+    const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
+    uint32_t* cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(cta_cap * 4));
+    uint32_t* cta_dist = static_cast<uint32_t*>(ix.res_cta_dist.ensure(cta_cap * 4));
     for (auto& e : ix.ev)
         if (!e) FCLSH_CUDA(cudaEventCreate(&e));
 
@@ -723,17 +898,21 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // S1: hash (point-major: key[q*T + t])
     if (nq) hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
     FCLSH_CUDA(cudaEventRecord(ix.ev[1], s));
-    // S2+S3 fused
-    FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 4, s));
-    if (nq) {
-        if (big)
-            launch_fused<T, LAYOUT, 2048>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
-        else
-            launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
-    }
+    // S2+S3 fused, warp per query
+    FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 16, s));
+    // Many tables (cfg4: 1022): CTA per query for every query (measured
+    // faster than the warp kernel there, clustered or sharded).
+    const bool dense_all = big;
+    if (nq && !dense_all)
+        launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
+                                      tmp_dist, ovf, ovf_cnt, s);
     FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
+    // the dense queries it handed over (count read on the device), or all, CTA per query
+    if (nq)
+        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
+                                found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
+                                ovf_cnt + 1, s);
+    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
     // Common path, one host sync: scan the per-query found counts (overflowing
     // queries count 0 here) and compact into buffers sized for the fused
     // results (<= nq * slot_cap), then read the overflow count and the total.
@@ -752,23 +931,26 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
         if (nq) {
             k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist,
-                                                                   nq * slot_cap, tmp2_id, tmp2_dist, ix.id_offset,
-                                                                   oq, oi, od);
+                                                                   nq * slot_cap, cta_id, cta_dist, cta_cap, tmp2_id,
+                                                                   tmp2_dist, ix.id_offset, oq, oi, od);
             FCLSH_LAUNCHED();
         }
     };
     scan_found();
-    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
-    compact();
     FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
+    // the CTA kernel's results are bounded by cta_cap
+    out_cap = std::max<uint64_t>(1, nq * slot_cap + cta_cap);
+    compact();
+    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
     struct {
         unsigned long long total;
-        unsigned int ns;
-    } hs{0, 0};
+        unsigned int cnt[2];
+    } hs{0, {0, 0}};
     FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
-    FCLSH_CUDA(cudaMemcpyAsync(&hs.ns, ovf_cnt, 4, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaMemcpyAsync(hs.cnt, ovf_cnt, 8, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
-    const unsigned int ns = hs.ns;
+    const unsigned int ns = hs.cnt[1];
+    ovf = ovf2; // what the CTA kernel could not take
     unsigned long long total = hs.total;
     if (ns) {
         // general path for the overflowing queries
@@ -802,8 +984,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                                           int64_t(total_coll), int64_t(ns), coll_off, coll_off + 1, s));
         }
         k_verify_sel<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
-            ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap, tmp2_id,
-            tmp2_dist, coll_q, cand_q, found_q, src_pos);
+            ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap + cta_cap,
+            tmp2_id, tmp2_dist, coll_q, cand_q, found_q, src_pos);
         FCLSH_LAUNCHED();
         // the overflowing queries' counts are in now: scan and compact again
         scan_found();
@@ -813,7 +995,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         out_cap = std::max<uint64_t>(out_cap, total);
         compact();
     }
-    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
+    FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
     out.total = total;
     out.d_query = ix.out_q.as<uint32_t>();
     out.d_id = ix.out_id.as<uint32_t>();
@@ -823,6 +1005,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     out.d_cand = reinterpret_cast<uint64_t*>(cand_q);
     out.d_found = reinterpret_cast<uint64_t*>(found_q);
     ix.last_total = total;
+    ix.last_dense = dense_all ? nq : hs.cnt[0];
     ix.last_overflow = ns;
     return out;
 }
@@ -952,8 +1135,8 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         ix.stage_ms[i] = ms;
     }
     ix.t_hash_ms = ix.stage_ms[0];
-    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[4]; // probe + dedup + verify are fused
-    ix.t_verify_ms = ix.stage_ms[2] + ix.stage_ms[3]; // result assembly
+    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2] + ix.stage_ms[5]; // probe + dedup + verify are fused
+    ix.t_verify_ms = ix.stage_ms[3] + ix.stage_ms[4];                 // result assembly
     return o;
 }
 

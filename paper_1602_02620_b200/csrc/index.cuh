@@ -48,15 +48,17 @@ struct DeviceIndex {
 
     // query workspace (grow-only)
     DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, coll_sel, fill, cand, cand_sorted, cand_cnt,
-        found, res_off, src_pos, res_tmp_id, res_tmp_dist, res2_id, res2_dist, overflow, overflow_cnt, out_q, out_id,
-        out_dist, cub_tmp;
+        found, res_off, src_pos, res_tmp_id, res_tmp_dist, res2_id, res2_dist, res_cta_id, res_cta_dist, overflow,
+        overflow2, overflow_cnt, out_q, out_id, out_dist, cub_tmp;
     uint64_t last_total = 0;
+    uint64_t last_dense = 0;    // queries the CTA-per-query kernel served
     uint64_t last_overflow = 0; // queries that took the general path
     double t_hash_ms = 0, t_probe_ms = 0, t_verify_ms = 0;
-    // device time of the last query per stage: hash (S1), fused
-    // probe+dedup+verify (S2+S3), found scan, compaction, general path for
-    // overflowing queries (+ its rescan / recompaction; includes one host sync)
-    static constexpr int kStages = 5;
+    // device time of the last query per stage: hash (S1), fused warp-per-query
+    // probe+dedup+verify (S2+S3), the CTA-per-query kernel for the dense
+    // queries the warp kernel hands over, found scan, compaction, general path
+    // for what is left (+ its rescan / recompaction; includes one host sync)
+    static constexpr int kStages = 6;
     double stage_ms[kStages] = {};
     cudaEvent_t ev[kStages + 1] = {};
 

@@ -59,6 +59,19 @@ def _check(rc: int) -> None:
         raise _ERRORS.get(rc, FclshError)(msg)
 
 
+def _release(obj, destroy: str) -> None:
+    """__del__ helper: frees the handle; a no-op once interpreter shutdown has
+    torn the module globals down."""
+    h = getattr(obj, "_h", None)
+    if h is None or not h.value or N is None:
+        return
+    try:
+        getattr(N.lib(), destroy)(h)
+    except (AttributeError, TypeError):  # pragma: no cover - shutdown order
+        return
+    obj._h = None
+
+
 def _u64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.uint64)
 
@@ -129,10 +142,7 @@ class CoveringFamily:
         self._seeds = None
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            N.lib().fclsh_family_destroy(h)
-            self._h = None
+        _release(self, "fclsh_family_destroy")
 
     def code_order(self) -> int:
         return 1 << (self.radius + 1)
@@ -234,10 +244,7 @@ class PreprocessPlan:
             self.parts = []
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            N.lib().fclsh_plan_destroy(h)
-            self._h = None
+        _release(self, "fclsh_plan_destroy")
 
     def part_count(self) -> int:
         return self._part_count
@@ -338,10 +345,7 @@ class IndexSet:
         self.buckets_per_table = int(info.buckets_per_table)
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            N.lib().fclsh_index_destroy(h)
-            self._h = None
+        _release(self, "fclsh_index_destroy")
 
     def table_count(self) -> int:
         return self._tables
@@ -381,7 +385,7 @@ class IndexSet:
             N.lib().fclsh_result_free(rp)
         return res
 
-    STAGES = ("hash", "fused", "found_scan", "compact", "overflow")
+    STAGES = ("hash", "fused", "dense", "found_scan", "compact", "overflow")
 
     def stage_ms(self) -> dict:
         """Device time per stage of the last query (CUDA events)."""
@@ -390,6 +394,12 @@ class IndexSet:
         if k < 0:
             _check(-k)
         return {name: float(buf[i]) for i, name in enumerate(self.STAGES[:k])}
+
+    def path_counts(self) -> dict:
+        """Queries of the last batch served by the dense (CTA) kernel and by the general path."""
+        dense, general = C.c_uint64(0), C.c_uint64(0)
+        _check(N.lib().fclsh_query_path_counts(self._h, C.byref(dense), C.byref(general)))
+        return {"dense": int(dense.value), "general": int(general.value)}
 
     def query_device(self, q_rows, radius: int, stream=None) -> DeviceQueryResults:
         """Device rows in (CUDA tensor), device results out (index-owned buffers)."""

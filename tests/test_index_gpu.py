@@ -89,6 +89,46 @@ def test_clustered_data_long_cells(oracle):
     assert res.found.max() >= 500
 
 
+def test_three_query_paths(oracle):
+    """One batch that needs all three query kernels: warp per query (sparse),
+    CTA per query (more than 1024 collisions; more such queries than the
+    persistent grid has CTAs) and the general sort path (more than 2048
+    results)."""
+    rng = np.random.default_rng(33)
+    d, radius = 128, 6
+    base = random_rows(rng, 700, d)
+    rows = random_rows(rng, 12000, d)
+    rows[:7000] = np.repeat(base, 10, axis=0)  # 700 values x 10 copies
+    rows[7000:9100] = base[0]  # base[0]: 2110 copies, more results than the CTA kernel holds
+    q = np.concatenate([base, random_rows(rng, 200, d), planted_queries(rng, rows[9100:], d, 100, radius)])
+    for layout in LAYOUTS:
+        force = F.PlanOverride(F.PlanKind.identity, 1)
+        plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, force)
+        ix = F.build_index(rows, radius, plan, 22, prime=M31, layout=layout)
+        ix.query_r_nn(q, radius)
+        paths = ix.path_counts()
+        assert paths["dense"] >= 600 and paths["general"] >= 1, paths
+    res = check_against_oracle(oracle, rows, q, d, radius, (0, 1), M31)
+    assert res.found[0] >= 2110
+
+
+def test_many_tables_cta_per_query(oracle):
+    """More than 600 tables (cfg4 has 1022): every query takes the CTA kernel
+    directly; duplicates push one query to the general path."""
+    rng = np.random.default_rng(77)
+    d, radius = 96, 9
+    rows = random_rows(rng, 3000, d)
+    rows[100:2300] = rows[0]  # 2201 copies: more results than the CTA kernel holds
+    q = np.concatenate([rows[:1], planted_queries(rng, rows[2300:], d, 150, radius)])
+    res = check_against_oracle(oracle, rows, q, d, radius, (0, 1), M31)
+    assert res.found[0] >= 2201
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, F.PlanOverride(F.PlanKind.identity, 1))
+    assert plan.table_count() > 600
+    ix = F.build_index(rows, radius, plan, 22, prime=M31)
+    ix.query_r_nn(q, radius)
+    assert ix.path_counts() == {"dense": q.shape[0], "general": 1}
+
+
 def test_directory_extremes(oracle):
     """A 2-cell directory (long scans) and a fine one give the same answers."""
     rng = np.random.default_rng(9)

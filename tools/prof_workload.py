@@ -25,6 +25,20 @@ if what in ("all", "query"):
     for _ in range(2):
         ix.query_device(qd, cfg.radius)
     torch.cuda.synchronize()
+if what in ("cfg4shard", "cfg4"):
+    # cfg4: shard 0 of the 8-shard layout (buckets), or the whole 10M index (CSR)
+    from paper_1602_02620_b200 import cluster
+    cfg = CONFIGS[4]
+    data = make_data(cfg, 16)
+    q = make_queries(cfg, data, 16)
+    b, e = cluster.shard_range(cfg.n, cfg.shards, 0) if what == "cfg4shard" else (0, cfg.n)
+    plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg.plan_seed(), cfg.override())
+    ix = F.build_index(data[b:e], cfg.radius, plan, cfg.index_seed(), prime=F.M31, id_offset=b)
+    qd = torch.from_numpy(q.view(np.int64)).cuda()
+    for _ in range(2):
+        ix.query_device(qd, cfg.radius)
+    torch.cuda.synchronize()
+    print(what, ix.layout, ix.stage_ms(), ix.path_counts())
 if what in ("all", "hash"):
     cfg5 = CONFIGS[5]
     n = 1_000_000
