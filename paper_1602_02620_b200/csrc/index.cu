@@ -41,6 +41,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -708,8 +709,19 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
                           const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len, const uint32_t* __restrict__ cta_id,
                           const uint32_t* __restrict__ cta_dist, uint64_t cta_len, const uint32_t* __restrict__ tmp2_id,
                           const uint32_t* __restrict__ tmp2_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
-                          uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist) {
+                          uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist,
+                          unsigned long long* __restrict__ pub, unsigned long long seq,
+                          const unsigned int* __restrict__ cnts) {
     const uint32_t lane = threadIdx.x & 31;
+    if (pub && blockIdx.x == 0 && threadIdx.x == 0) {
+        // the batch's total and hand-over counts to mapped host memory, then
+        // the sequence number the host spins on (no memcpy + stream sync)
+        pub[0] = res_off[nq];
+        pub[1] = cnts[0];
+        pub[2] = cnts[1];
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
+    }
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
         const uint64_t dst = res_off[q], cnt = res_off[q + 1] - dst;
@@ -865,6 +877,21 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     FCLSH_LAUNCHED();
 }
 
+// Spins until k_compact has published this batch's sequence number in mapped
+// host memory (lower latency than a D2H copy + cudaStreamSynchronize). Polls
+// the stream now and then so a device fault surfaces instead of hanging.
+void wait_published(const unsigned long long* h_pub, unsigned long long seq, cudaStream_t s) {
+    const volatile unsigned long long* flag = h_pub + 3;
+    for (uint64_t it = 1; *flag != seq; ++it) {
+        if ((it & 4095) == 0) {
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e == cudaSuccess && *flag != seq) throw CudaError("query: batch results were not published");
+            if (e != cudaSuccess && e != cudaErrorNotReady) FCLSH_CUDA(e);
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 template <typename T, int LAYOUT>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
     using K = typename T::K;
@@ -925,14 +952,14 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* tmp2_id = tmp_id;
     uint32_t* tmp2_dist = tmp_dist;
     uint64_t out_cap = std::max<uint64_t>(1, nq * slot_cap);
-    auto compact = [&] {
+    auto compact = [&](unsigned long long* pub, unsigned long long seq) {
         uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
         uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
         uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
         if (nq) {
-            k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist,
-                                                                   nq * slot_cap, cta_id, cta_dist, cta_cap, tmp2_id,
-                                                                   tmp2_dist, ix.id_offset, oq, oi, od);
+            k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(
+                nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap, cta_id, cta_dist, cta_cap, tmp2_id, tmp2_dist,
+                ix.id_offset, oq, oi, od, pub, seq, ovf_cnt);
             FCLSH_LAUNCHED();
         }
     };
@@ -940,15 +967,23 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
     // the CTA kernel's results are bounded by cta_cap
     out_cap = std::max<uint64_t>(1, nq * slot_cap + cta_cap);
-    compact();
+    if (!ix.h_pub) {
+        FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 64, cudaHostAllocMapped));
+        FCLSH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ix.d_pub), ix.h_pub, 0));
+    }
+    const unsigned long long seq = ++ix.pub_seq;
+    compact(ix.d_pub, seq);
     FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
     struct {
         unsigned long long total;
         unsigned int cnt[2];
     } hs{0, {0, 0}};
-    FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
-    FCLSH_CUDA(cudaMemcpyAsync(hs.cnt, ovf_cnt, 8, cudaMemcpyDeviceToHost, s));
-    FCLSH_CUDA(cudaStreamSynchronize(s));
+    if (nq) {
+        wait_published(ix.h_pub, seq, s);
+        hs.total = ix.h_pub[0];
+        hs.cnt[0] = unsigned(ix.h_pub[1]);
+        hs.cnt[1] = unsigned(ix.h_pub[2]);
+    }
     const unsigned int ns = hs.cnt[1];
     ovf = ovf2; // what the CTA kernel could not take
     unsigned long long total = hs.total;
@@ -993,7 +1028,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         FCLSH_CUDA(cudaStreamSynchronize(s));
         total = hs.total;
         out_cap = std::max<uint64_t>(out_cap, total);
-        compact();
+        compact(nullptr, 0);
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
     out.total = total;
@@ -1013,6 +1048,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
 } // namespace
 
 DeviceIndex::~DeviceIndex() {
+    if (h_pub) cudaFreeHost(h_pub);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);

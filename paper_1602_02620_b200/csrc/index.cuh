@@ -50,6 +50,10 @@ struct DeviceIndex {
     DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, coll_sel, fill, cand, cand_sorted, cand_cnt,
         found, res_off, src_pos, res_tmp_id, res_tmp_dist, res2_id, res2_dist, res_cta_id, res_cta_dist, overflow,
         overflow2, overflow_cnt, out_q, out_id, out_dist, cub_tmp;
+    // mapped pinned words k_compact publishes {total, hand-over counts, seq} to
+    unsigned long long* h_pub = nullptr;
+    unsigned long long* d_pub = nullptr;
+    unsigned long long pub_seq = 0;
     uint64_t last_total = 0;
     uint64_t last_dense = 0;    // queries the CTA-per-query kernel served
     uint64_t last_overflow = 0; // queries that took the general path
