@@ -248,7 +248,10 @@ def main():
     ix = F.build_index(data, cfg.radius, plan, cfg0.index_seed(), prime=F.M31, device=dev,
                        id_offset=rank * cfg.n)
     build_wall = time.perf_counter() - t0
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for everything timed: the L2 flush, the CUDA events
+    # and the library's work are all ordered on it
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     q_dev = torch.from_numpy(queries.view(np.int64)).to(f"cuda:{dev}")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=f"cuda:{dev}")  # 256 MiB > 126 MB L2
 

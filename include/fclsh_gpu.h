@@ -212,8 +212,12 @@ void fclsh_result_free(fclsh_result* r);
 
 /* Device-resident variant: q rows already on the device, results stay in
  * index-owned device buffers that live until the next query on `ix`.
- * Pointers returned are device pointers; *total is read back to the host
- * (one 8-byte D2H). All work is enqueued on `stream`. */
+ * Pointers returned are device pointers. The work runs on the index's own
+ * stream, ordered after the work already queued on `stream` and before
+ * anything queued on `stream` afterwards (event fork/join; NULL = no join).
+ * The call returns once `total` is known (the device publishes it to mapped
+ * host memory); the output arrays complete in `stream` order. A batch shape
+ * seen twice in a row is replayed as one CUDA graph. */
 typedef struct {
     uint64_t nq;
     uint64_t total;

@@ -32,6 +32,39 @@ uint64_t& launch_counter() {
     static thread_local uint64_t c = 0;
     return c;
 }
+
+int resident_ctas_impl(const void* kern, int threads, size_t smem, int device) {
+    struct Key {
+        const void* k;
+        int threads;
+        size_t smem;
+        int device;
+        bool operator<(const Key& o) const {
+            if (k != o.k) return k < o.k;
+            if (threads != o.threads) return threads < o.threads;
+            if (smem != o.smem) return smem < o.smem;
+            return device < o.device;
+        }
+    };
+    static std::mutex mu;
+    static std::map<Key, int> cache;
+    static std::map<std::pair<const void*, int>, size_t> limit; // dynamic-smem limit set so far
+    const Key key{kern, threads, smem, device};
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    // the limit only ever grows: a smaller launch must not lower it under a
+    // larger one that is already cached
+    size_t& lim = limit[{kern, device}];
+    if (smem > lim) {
+        FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        lim = smem;
+    }
+    int per_sm = 0;
+    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    cache[key] = per_sm;
+    return per_sm;
+}
 } // namespace fclsh_b200
 
 using namespace fclsh_b200;
@@ -335,6 +368,7 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
             FCLSH_CUDA(cudaMemcpyAsync(r->found, o.d_found, nq * 8, cudaMemcpyDeviceToHost, s));
         }
         FCLSH_CUDA(cudaStreamSynchronize(s));
+        ix.collect_stages();
         r->time_hash_ms = ix.t_hash_ms;
         r->time_probe_ms = ix.t_probe_ms;
         r->time_verify_ms = ix.t_verify_ms;
@@ -413,6 +447,8 @@ int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n) {
         return -FCLSH_ERR_USAGE;
     }
     const int k = std::min(n, DeviceIndex::kStages);
+    const int rc = guarded([&] { ix->ix->collect_stages(); });
+    if (rc != FCLSH_OK) return -rc;
     for (int i = 0; i < k; ++i) ms[i] = ix->ix->stage_ms[i];
     return k;
 }

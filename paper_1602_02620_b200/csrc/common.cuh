@@ -25,16 +25,29 @@ uint64_t& launch_counter();
         ::fclsh_b200::launch_counter()++;                                                    \
         cudaError_t _e = cudaGetLastError();                                                 \
         if (_e != cudaSuccess)                                                               \
-            throw ::fclsh_b200::CudaError(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            throw ::fclsh_b200::CudaError(std::string("kernel launch (") + __FILE__ + ":" +            \
+                                          std::to_string(__LINE__) + "): " + cudaGetErrorString(_e));  \
     } while (0)
 
 constexpr int kNumSMs = 148; // B200
 
 inline int sm_count(int device) {
+    static int cache[64] = {};
+    if (device >= 0 && device < 64 && cache[device] > 0) return cache[device];
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
         return kNumSMs;
+    if (device >= 0 && device < 64) cache[device] = v;
     return v;
+}
+
+// Resident CTAs per SM of kern at (threads, dynamic smem) on device, raising
+// the kernel's dynamic-smem limit first. Cached: the attribute call and the
+// occupancy query cost host microseconds on every query batch otherwise.
+int resident_ctas_impl(const void* kern, int threads, size_t smem, int device);
+template <typename F>
+int resident_ctas(F* kern, int threads, size_t smem, int device) {
+    return resident_ctas_impl(reinterpret_cast<const void*>(kern), threads, smem, device);
 }
 
 // RAII device buffer (grow-only when reused as a workspace).

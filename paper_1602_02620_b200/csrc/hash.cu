@@ -617,9 +617,7 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
         // (a family table too large for the 12-warp layout falls back to the staged kernel)
         if (prm.layout == kLayoutPointMajor && smem_pm <= 227 * 1024) {
             auto kern = k_hash_m31_pm<LOGN, DIRECT>;
-            FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_pm)));
-            int per_sm = 0;
-            FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WARPS, smem_pm));
+            const int per_sm = resident_ctas(kern, 32 * WARPS, smem_pm, fs.device);
             if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
             const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
             const uint64_t grid = std::min<uint64_t>((groups + WARPS - 1) / WARPS, uint64_t(per_sm) * sm_count(fs.device));
@@ -629,9 +627,7 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
         }
     }
     auto kern = k_hash_m31<LOGN, DIRECT>;
-    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    const int per_sm = resident_ctas(kern, 256, smem, fs.device);
     if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
     const uint64_t tiles = (prm.n + PT - 1) / PT;
     const uint64_t grid = std::min<uint64_t>(tiles, uint64_t(per_sm) * sm_count(fs.device));

@@ -710,12 +710,14 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
                           const uint32_t* __restrict__ cta_dist, uint64_t cta_len, const uint32_t* __restrict__ tmp2_id,
                           const uint32_t* __restrict__ tmp2_dist, uint64_t id_offset, uint32_t* __restrict__ out_q,
                           uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist,
-                          unsigned long long* __restrict__ pub, unsigned long long seq,
+                          unsigned long long* __restrict__ pub, unsigned long long* __restrict__ dseq,
                           const unsigned int* __restrict__ cnts) {
     const uint32_t lane = threadIdx.x & 31;
     if (pub && blockIdx.x == 0 && threadIdx.x == 0) {
         // the batch's total and hand-over counts to mapped host memory, then
         // the sequence number the host spins on (no memcpy + stream sync)
+        const unsigned long long seq = *dseq + 1; // batch number (graph replays need no parameter)
+        *dseq = seq;
         pub[0] = res_off[nq];
         pub[1] = cnts[0];
         pub[2] = cnts[1];
@@ -842,9 +844,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   uint32_t* ovf, unsigned int* ovf_cnt, cudaStream_t s) {
     auto kern = k_query_fused<T, LAYOUT, CAP, 4>;
     const size_t smem = (8 + size_t(8) * CAP) * 4;
-    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    const int per_sm = resident_ctas(kern, 256, smem, ix.device);
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
     kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
@@ -865,9 +865,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4;
-    FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    FCLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem));
+    const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
     // persistent grid: the overflow count is only known on the device
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
     if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
@@ -920,69 +918,116 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* cta_dist = static_cast<uint32_t*>(ix.res_cta_dist.ensure(cta_cap * 4));
     for (auto& e : ix.ev)
         if (!e) FCLSH_CUDA(cudaEventCreate(&e));
-
-    FCLSH_CUDA(cudaEventRecord(ix.ev[0], s));
-    // S1: hash (point-major: key[q*T + t])
-    if (nq) hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
-    FCLSH_CUDA(cudaEventRecord(ix.ev[1], s));
-    // S2+S3 fused, warp per query
-    FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 16, s));
     // Many tables (cfg4: 1022): CTA per query for every query (measured
     // faster than the warp kernel there, clustered or sharded).
     const bool dense_all = big;
-    if (nq && !dense_all)
-        launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                      tmp_dist, ovf, ovf_cnt, s);
-    FCLSH_CUDA(cudaEventRecord(ix.ev[2], s));
-    // the dense queries it handed over (count read on the device), or all, CTA per query
-    if (nq)
-        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
-                                found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, s);
-    FCLSH_CUDA(cudaEventRecord(ix.ev[3], s));
-    // Common path, one host sync: scan the per-query found counts (overflowing
-    // queries count 0 here) and compact into buffers sized for the fused
-    // results (<= nq * slot_cap), then read the overflow count and the total.
-    auto scan_found = [&] {
-        FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
-        size_t tmp_bytes = 0;
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, found_q, res_off, nq + 1, s));
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tmp_bytes), tmp_bytes, found_q, res_off, nq + 1, s));
-    };
-    uint32_t* tmp2_id = tmp_id;
-    uint32_t* tmp2_dist = tmp_dist;
-    uint64_t out_cap = std::max<uint64_t>(1, nq * slot_cap);
-    auto compact = [&](unsigned long long* pub, unsigned long long seq) {
-        uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
-        uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
-        uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
-        if (nq) {
-            k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(
-                nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap, cta_id, cta_dist, cta_cap, tmp2_id, tmp2_dist,
-                ix.id_offset, oq, oi, od, pub, seq, ovf_cnt);
-            FCLSH_LAUNCHED();
-        }
-    };
-    scan_found();
-    FCLSH_CUDA(cudaEventRecord(ix.ev[4], s));
-    // the CTA kernel's results are bounded by cta_cap
-    out_cap = std::max<uint64_t>(1, nq * slot_cap + cta_cap);
+    // Everything the common path touches is sized here, before any launch, so
+    // a captured graph never needs a reallocation.
+    uint64_t out_cap = std::max<uint64_t>(1, nq * slot_cap + cta_cap); // CTA results <= cta_cap
+    uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
+    uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
+    uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
+    size_t scan_bytes = 0;
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, found_q, res_off, nq + 1, s));
+    void* scan_tmp = ix.cub_tmp.ensure(scan_bytes);
     if (!ix.h_pub) {
         FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 64, cudaHostAllocMapped));
         FCLSH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ix.d_pub), ix.h_pub, 0));
+        ix.h_pub[3] = 0;
+        FCLSH_CUDA(cudaMemset(ix.pub_seq_dev.ensure(8), 0, 8));
+        ix.pub_seq = 0;
     }
-    const unsigned long long seq = ++ix.pub_seq;
-    compact(ix.d_pub, seq);
-    FCLSH_CUDA(cudaEventRecord(ix.ev[5], s));
+    auto* d_seq = ix.pub_seq_dev.as<unsigned long long>();
+    uint32_t* tmp2_id = tmp_id;
+    uint32_t* tmp2_dist = tmp_dist;
+    auto scan_found = [&](void* tmp, size_t bytes) {
+        FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, found_q, res_off, nq + 1, s));
+    };
+    auto compact = [&](unsigned long long* pub) {
+        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap,
+                                                               cta_id, cta_dist, cta_cap, tmp2_id, tmp2_dist,
+                                                               ix.id_offset, oq, oi, od, pub, d_seq, ovf_cnt);
+        FCLSH_LAUNCHED();
+    };
+    // The common path: S1 hash (point-major key[q*T + t]), S2+S3 fused warp
+    // per query, the CTA-per-query kernel for what it hands over (count read
+    // on the device) or for every query, found scan, compaction + publish.
+    bool capturing = false;
+    auto rec = [&](int k) { // stage events; inside a capture they must be external record nodes
+        FCLSH_CUDA(capturing ? cudaEventRecordWithFlags(ix.ev[k], s, cudaEventRecordExternal)
+                             : cudaEventRecord(ix.ev[k], s));
+    };
+    auto enqueue_common = [&] {
+        rec(0);
+        hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
+        rec(1);
+        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 16, s));
+        if (!dense_all)
+            launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
+        rec(2);
+        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
+                                found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
+                                ovf_cnt + 1, s);
+        rec(3);
+        scan_found(scan_tmp, scan_bytes);
+        rec(4);
+        compact(ix.d_pub);
+        rec(5);
+    };
     struct {
         unsigned long long total;
         unsigned int cnt[2];
     } hs{0, {0, 0}};
     if (nq) {
-        wait_published(ix.h_pub, seq, s);
+        // A shape seen twice in a row (same rows pointer, batch size, radius,
+        // stream and workspace) is captured once into a CUDA graph and
+        // relaunched: one host call instead of ~10 launches per batch.
+        const std::vector<const void*> key = {d_q, reinterpret_cast<const void*>(nq),
+                                              reinterpret_cast<const void*>(uintptr_t(radius)), s, qkeys, coll_q,
+                                              cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
+                                              ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq};
+        if (ix.gexec && key == ix.gkey) {
+            FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
+            launch_counter() += ix.gkernels;
+        } else if (key == ix.gpending) {
+            const uint64_t before = launch_counter();
+            cudaGraph_t g = nullptr;
+            FCLSH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
+            try {
+                enqueue_common();
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            capturing = false;
+            FCLSH_CUDA(cudaStreamEndCapture(s, &g));
+            ix.gkernels = launch_counter() - before;
+            launch_counter() = before;
+            if (ix.gexec) {
+                cudaGraphExecDestroy(ix.gexec);
+                ix.gexec = nullptr;
+            }
+            const cudaError_t ie = cudaGraphInstantiate(&ix.gexec, g, 0);
+            cudaGraphDestroy(g);
+            FCLSH_CUDA(ie);
+            ix.gkey = key;
+            FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
+            launch_counter() += ix.gkernels;
+        } else {
+            enqueue_common();
+            ix.gpending = key;
+        }
+        wait_published(ix.h_pub, ++ix.pub_seq, s);
         hs.total = ix.h_pub[0];
         hs.cnt[0] = unsigned(ix.h_pub[1]);
         hs.cnt[1] = unsigned(ix.h_pub[2]);
+    } else {
+        FCLSH_CUDA(cudaMemsetAsync(res_off, 0, 8, s)); // offsets = [0]
+        for (int e = 0; e < 6; ++e) FCLSH_CUDA(cudaEventRecord(ix.ev[e], s));
     }
     const unsigned int ns = hs.cnt[1];
     ovf = ovf2; // what the CTA kernel could not take
@@ -1000,7 +1045,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         FCLSH_LAUNCHED();
         size_t tb_bytes = 0;
         FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb_bytes, coll_s, coll_off, ns + 1, s));
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp.ensure(tb_bytes), tb_bytes, coll_s, coll_off, ns + 1, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(ix.cub_tmp2.ensure(tb_bytes), tb_bytes, coll_s, coll_off, ns + 1, s));
         unsigned long long total_coll = 0;
         FCLSH_CUDA(cudaMemcpyAsync(&total_coll, coll_off + ns, 8, cudaMemcpyDeviceToHost, s));
         FCLSH_CUDA(cudaStreamSynchronize(s));
@@ -1015,7 +1060,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             size_t sb = 0;
             FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, cand, sorted, int64_t(total_coll), int64_t(ns),
                                                           coll_off, coll_off + 1, s));
-            FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp.ensure(sb), sb, cand, sorted,
+            FCLSH_CUDA(cub::DeviceSegmentedSort::SortKeys(ix.cub_tmp2.ensure(sb), sb, cand, sorted,
                                                           int64_t(total_coll), int64_t(ns), coll_off, coll_off + 1, s));
         }
         k_verify_sel<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
@@ -1023,12 +1068,17 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             tmp2_id, tmp2_dist, coll_q, cand_q, found_q, src_pos);
         FCLSH_LAUNCHED();
         // the overflowing queries' counts are in now: scan and compact again
-        scan_found();
+        scan_found(scan_tmp, scan_bytes);
         FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
         FCLSH_CUDA(cudaStreamSynchronize(s));
         total = hs.total;
-        out_cap = std::max<uint64_t>(out_cap, total);
-        compact(nullptr, 0);
+        if (total > out_cap) {
+            out_cap = total;
+            oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
+            oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
+            od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
+        }
+        compact(nullptr);
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
     out.total = total;
@@ -1048,6 +1098,9 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
 } // namespace
 
 DeviceIndex::~DeviceIndex() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
     if (h_pub) cudaFreeHost(h_pub);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
@@ -1156,7 +1209,15 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
     FCLSH_CUDA(cudaSetDevice(ix.device));
-    cudaStream_t s = stream ? stream : ix.stream;
+    // Work runs on the index's stream, ordered after / before the caller's.
+    cudaStream_t s = ix.stream;
+    const bool join = stream && stream != s;
+    if (join) {
+        for (auto* e : {&ix.ev_in, &ix.ev_out})
+            if (!*e) FCLSH_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        FCLSH_CUDA(cudaEventRecord(ix.ev_in, stream));
+        FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_in, 0));
+    }
     QueryOutput o;
     if (ix.wide)
         o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
@@ -1164,16 +1225,26 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
     else
         o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
                                         : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s);
-    FCLSH_CUDA(cudaEventSynchronize(ix.ev[DeviceIndex::kStages]));
-    for (int i = 0; i < DeviceIndex::kStages; ++i) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, ix.ev[i], ix.ev[i + 1]);
-        ix.stage_ms[i] = ms;
+    if (join) {
+        FCLSH_CUDA(cudaEventRecord(ix.ev_out, s));
+        FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));
     }
-    ix.t_hash_ms = ix.stage_ms[0];
-    ix.t_probe_ms = ix.stage_ms[1] + ix.stage_ms[2] + ix.stage_ms[5]; // probe + dedup + verify are fused
-    ix.t_verify_ms = ix.stage_ms[3] + ix.stage_ms[4];                 // result assembly
+    ix.stages_pending = true;
     return o;
+}
+
+void DeviceIndex::collect_stages() {
+    if (!stages_pending) return;
+    FCLSH_CUDA(cudaEventSynchronize(ev[kStages]));
+    for (int i = 0; i < kStages; ++i) {
+        float ms = 0;
+        FCLSH_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        stage_ms[i] = ms;
+    }
+    t_hash_ms = stage_ms[0];
+    t_probe_ms = stage_ms[1] + stage_ms[2] + stage_ms[5]; // probe + dedup + verify are fused
+    t_verify_ms = stage_ms[3] + stage_ms[4];              // result assembly
+    stages_pending = false;
 }
 
 } // namespace fclsh_b200

@@ -50,10 +50,17 @@ struct DeviceIndex {
     DevBuf q_rows, q_keys, r_start, r_count, coll, coll_off, coll_sel, fill, cand, cand_sorted, cand_cnt,
         found, res_off, src_pos, res_tmp_id, res_tmp_dist, res2_id, res2_dist, res_cta_id, res_cta_dist, overflow,
         overflow2, overflow_cnt, out_q, out_id, out_dist, cub_tmp;
-    // mapped pinned words k_compact publishes {total, hand-over counts, seq} to
+    // mapped pinned words k_compact publishes {total, hand-over counts, seq} to;
+    // the batch sequence number is counted on the device (pub_seq_dev)
     unsigned long long* h_pub = nullptr;
     unsigned long long* d_pub = nullptr;
     unsigned long long pub_seq = 0;
+    DevBuf pub_seq_dev, cub_tmp2;
+    // the common path as a CUDA graph, keyed by shape + buffers (index.cu)
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<const void*> gkey, gpending;
+    uint64_t gkernels = 0;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr; // caller-stream fork / join
     uint64_t last_total = 0;
     uint64_t last_dense = 0;    // queries the CTA-per-query kernel served
     uint64_t last_overflow = 0; // queries that took the general path
@@ -65,6 +72,8 @@ struct DeviceIndex {
     static constexpr int kStages = 6;
     double stage_ms[kStages] = {};
     cudaEvent_t ev[kStages + 1] = {};
+    bool stages_pending = false;
+    void collect_stages(); // waits for the last batch, fills stage_ms / t_*_ms
 
     ~DeviceIndex();
     uint64_t cells() const { return uint64_t(1) << dir_bits; }

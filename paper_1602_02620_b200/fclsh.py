@@ -115,16 +115,23 @@ class PlanOverride:  # transform.hpp:46-50
     t: int = 1
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: torch's default stream, passed so the C side joins it
+
+
 def _stream_ptr(stream):
+    """cudaStream_t for the C-ABI. A torch stream (None = torch's current one)
+    is passed as itself; torch's default stream (handle 0) as cudaStreamLegacy,
+    because NULL means the library's own stream, which is not ordered with the
+    caller's work. A plain int is passed through unchanged."""
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
     if stream is None:
         try:
             import torch
-            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            stream = torch.cuda.current_stream()
         except Exception:  # pragma: no cover - torch is always present in this image
             return C.c_void_p(0)
-    if isinstance(stream, int):
-        return C.c_void_p(stream)
-    return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(stream.cuda_stream or _CUDA_STREAM_LEGACY)
 
 
 class CoveringFamily:
@@ -141,8 +148,8 @@ class CoveringFamily:
         self._mapping = None
         self._seeds = None
 
-    def __del__(self):
-        _release(self, "fclsh_family_destroy")
+    def __del__(self, _free=_release):  # bound at definition: module globals may be gone at exit
+        _free(self, "fclsh_family_destroy")
 
     def code_order(self) -> int:
         return 1 << (self.radius + 1)
@@ -243,8 +250,8 @@ class PreprocessPlan:
             self.permutation = np.zeros(0, np.uint32)
             self.parts = []
 
-    def __del__(self):
-        _release(self, "fclsh_plan_destroy")
+    def __del__(self, _free=_release):  # bound at definition: module globals may be gone at exit
+        _free(self, "fclsh_plan_destroy")
 
     def part_count(self) -> int:
         return self._part_count
@@ -344,8 +351,8 @@ class IndexSet:
         self.layout = {1: "csr", 2: "buckets"}.get(int(info.layout), "?")
         self.buckets_per_table = int(info.buckets_per_table)
 
-    def __del__(self):
-        _release(self, "fclsh_index_destroy")
+    def __del__(self, _free=_release):  # bound at definition: module globals may be gone at exit
+        _free(self, "fclsh_index_destroy")
 
     def table_count(self) -> int:
         return self._tables

@@ -129,6 +129,42 @@ def test_many_tables_cta_per_query(oracle):
     assert ix.path_counts() == {"dense": q.shape[0], "general": 1}
 
 
+def _device_triples(r):
+    import torch
+    tri = torch.zeros((3, max(r.total, 1)), dtype=torch.int32, device="cuda")
+    off = torch.zeros(r.nq + 1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros((3, r.nq), dtype=torch.int64, device="cuda")
+    r.copy_to(tri, off, cnt)
+    torch.cuda.synchronize()
+    return tri[:, :r.total].cpu().numpy(), off.cpu().numpy(), cnt.cpu().numpy()
+
+
+def test_repeated_device_queries_replay_graph(oracle):
+    """The second identical batch is captured into a CUDA graph and later ones
+    replay it: results must equal the eager ones, follow new contents of the
+    same query buffer, and stay ordered with the caller's side stream."""
+    import torch
+    rng = np.random.default_rng(5)
+    rows = random_rows(rng, 4000, 128)
+    qa = planted_queries(rng, rows, 128, 300, 5)
+    qb = planted_queries(rng, rows, 128, 300, 5)
+    plan = F.make_plan(128, 4, 1.0, 4000, 1, F.PlanOverride(F.PlanKind.identity, 1))
+    ix = F.build_index(rows, 4, plan, 2, prime=M31)
+    want_a, want_b = ix.query_r_nn(qa, 4), ix.query_r_nn(qb, 4)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        qd = torch.from_numpy(qa.view(np.int64)).cuda()
+        for k in range(5):
+            if k == 3:  # same buffer, new contents: the replayed graph must read them
+                qd.copy_(torch.from_numpy(qb.view(np.int64)))
+            want = want_b if k >= 3 else want_a
+            tri, off, cnt = _device_triples(ix.query_device(qd, 4, side))
+            assert (off == want.offsets.astype(np.int64)).all(), k
+            assert (tri[1] == want.id.astype(np.int32)).all(), k
+            assert (cnt[2] == want.found.astype(np.int64)).all(), k
+            assert set(ix.stage_ms()) == set(F.IndexSet.STAGES)
+
+
 def test_directory_extremes(oracle):
     """A 2-cell directory (long scans) and a fine one give the same answers."""
     rng = np.random.default_rng(9)
