@@ -295,6 +295,7 @@ def main():
         total_ms = float(t.item())
     value = nq * args.steps / (total_ms / 1e3)
     stage_avg = {k: statistics.mean(s[k] for s in stages) for k in stages[0]}
+    paths = ix.path_counts()
 
     # ---------------- counters of the timed batch (for algorithmic bytes) + parity
     res = ix.query_r_nn(queries, cfg.radius)
@@ -386,7 +387,7 @@ def main():
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
         "gpu_launches_note": "own kernels only; CUB scan/segmented-sort launches are not counted",
         "clocks": None, "parity_vs_reference": parity,
-        "stages_ms": stage_avg, "stage_rooflines": stage_rooflines,
+        "stages_ms": stage_avg, "stage_rooflines": stage_rooflines, "query_paths": paths,
         "counters": {"collisions_mean": float(coll.mean()), "candidates_mean": float(cand.mean()),
                      "found_total": int(found.sum())},
         "build": build_info,

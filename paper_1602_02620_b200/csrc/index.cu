@@ -338,14 +338,21 @@ __global__ void __launch_bounds__(256) k_query_fused(
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
     unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
-    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count) {
+    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
+    unsigned int* __restrict__ qnext) {
     using E = typename T::E;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* cnt_s = reinterpret_cast<uint32_t*>(smem);
     uint32_t* ids = reinterpret_cast<uint32_t*>(smem) + 8 + warp * CAP;
-    const uint64_t nwarps = uint64_t(gridDim.x) * 8;
-    for (uint64_t q = uint64_t(blockIdx.x) * 8 + warp; q < nq; q += nwarps) {
+    // queries are handed out one at a time (a warp that finishes early takes
+    // the next), so the last wave does not leave most warps idle
+    auto fetch = [&]() -> uint64_t {
+        unsigned int v = 0;
+        if (lane == 0) v = atomicAdd(qnext, 1u);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint64_t q = fetch(); q < nq; q = fetch()) {
         if (lane == 0) cnt_s[warp] = 0;
         __syncwarp();
         const typename T::K* qk = qkeys + q * tables;
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(512) k_query_dense(
     unsigned long long* __restrict__ cand_q, unsigned long long* __restrict__ found_q,
     unsigned long long* __restrict__ src_pos, uint64_t src_base, uint32_t* __restrict__ res_id,
     uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
-    uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt) {
+    uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
     uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
@@ -532,7 +539,13 @@ __global__ void __launch_bounds__(512) k_query_dense(
     constexpr int kV = 4; // candidates verified per thread at a time (one LDS.128)
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
-    for (uint32_t s_ = blockIdx.x; s_ < ns; s_ += gridDim.x) {
+    __shared__ unsigned int next_s;
+    auto fetch = [&]() -> uint32_t { // dynamic hand-out: query costs vary widely on clustered data
+        if (tid == 0) next_s = atomicAdd(qnext, 1u);
+        __syncthreads();
+        return next_s; // rewritten only after the body's barriers
+    };
+    for (uint32_t s_ = fetch(); s_ < ns; s_ = fetch()) {
         const uint64_t q = ovf ? ovf[s_] : s_;
         for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
         if (tid == 0) {
@@ -841,7 +854,7 @@ template <typename T, int LAYOUT, int CAP>
 void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
-                  uint32_t* ovf, unsigned int* ovf_cnt, cudaStream_t s) {
+                  uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, cudaStream_t s) {
     auto kern = k_query_fused<T, LAYOUT, CAP, 4>;
     const size_t smem = (8 + size_t(8) * CAP) * 4;
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
@@ -849,7 +862,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
     kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
                                            ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                           tmp_dist, ovf, ovf_cnt);
+                                           tmp_dist, ovf, ovf_cnt, qnext);
     FCLSH_LAUNCHED();
 }
 
@@ -862,7 +875,8 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 const uint32_t* ovf, const unsigned int* ovf_cnt, uint64_t direct_n, unsigned long long* coll_q,
                 unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
                 uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
-                unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, cudaStream_t s) {
+                unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
+                cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
@@ -871,7 +885,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
     kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
                                                      d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
-                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt);
+                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext);
     FCLSH_LAUNCHED();
 }
 
@@ -909,8 +923,9 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
     uint32_t* ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
-    // count, bytes 8..15: the CTA kernel's result cursor
-    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(16));
+    // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
+    // query to hand out in the warp / CTA kernel
+    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32));
     auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
     // CTA-kernel result region; queries that do not fit go on to the general path
     const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
@@ -962,14 +977,14 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(0);
         hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
         rec(1);
-        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 16, s));
+        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32, s));
         if (!dense_all)
             launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, s);
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, s);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
                                 found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, s);
+                                ovf_cnt + 1, ovf_cnt + 5, s);
         rec(3);
         scan_found(scan_tmp, scan_bytes);
         rec(4);

@@ -24,8 +24,30 @@ __device__ __forceinline__ uint4 ld256_lo(const uint4* p, uint4& hi) {
     return lo;
 }
 
-// WIDE: 32-byte (256-bit) load instructions instead of 16-byte ones
-template <int B, int INFLIGHT, bool WIDE = false>
+__device__ __forceinline__ uint4 ld_noalloc(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint4 ld256_nc_na(const uint4* p, uint4& hi) {
+    uint4 lo;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+    return lo;
+}
+__device__ __forceinline__ uint4 ld256_cg(const uint4* p, uint4& hi) {
+    uint4 lo;
+    asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+    return lo;
+}
+
+// WIDE: 4 = 256-bit .nc.L1::no_allocate, 5 = 256-bit .cg; 1 = 32-byte (256-bit) .nc loads, 2 = ld.global.cg (__ldcg: L2 only),
+// 3 = ld.global.L1::no_allocate; 0 = __ldg (.nc, 16-byte)
+template <int B, int INFLIGHT, int WIDE = 0>
 __global__ void k_rand(const uint4* __restrict__ buf, uint64_t units, uint64_t iters, unsigned long long* sink) {
     constexpr int V = B / 16 > 0 ? B / 16 : 1;
     const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -36,9 +58,21 @@ __global__ void k_rand(const uint4* __restrict__ buf, uint64_t units, uint64_t i
         for (int k = 0; k < INFLIGHT; ++k) {
             const uint64_t u = mix(tid * 1315423911ull + it * INFLIGHT + k) % units;
             const uint4* p = buf + u * V;
-            if constexpr (WIDE) {
+            if constexpr (WIDE == 1) {
 #pragma unroll
                 for (int j = 0; j < V; j += 2) v[k][j] = ld256_lo(p + j, v[k][j + 1]);
+            } else if constexpr (WIDE == 4) {
+#pragma unroll
+                for (int j = 0; j < V; j += 2) v[k][j] = ld256_nc_na(p + j, v[k][j + 1]);
+            } else if constexpr (WIDE == 5) {
+#pragma unroll
+                for (int j = 0; j < V; j += 2) v[k][j] = ld256_cg(p + j, v[k][j + 1]);
+            } else if constexpr (WIDE == 2) {
+#pragma unroll
+                for (int j = 0; j < V; ++j) v[k][j] = __ldcg(p + j);
+            } else if constexpr (WIDE == 3) {
+#pragma unroll
+                for (int j = 0; j < V; ++j) v[k][j] = ld_noalloc(p + j);
             } else if constexpr (B == 8) {
                 const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
                 v[k][0] = make_uint4(x.x, x.y, 0, 0);
@@ -55,23 +89,27 @@ __global__ void k_rand(const uint4* __restrict__ buf, uint64_t units, uint64_t i
     if (acc == 0x12345) atomicAdd(sink, acc);
 }
 
-template <int B, int INFLIGHT, bool WIDE = false>
-void run(const uint4* buf, uint64_t bytes, unsigned long long* sink, int sms) {
+// smem_kb: dynamic shared memory per block (4 blocks per SM), shrinking the
+// L1 share of the unified L1/shared array as a probe kernel's working set does
+template <int B, int INFLIGHT, int WIDE = 0>
+void run(const uint4* buf, uint64_t bytes, unsigned long long* sink, int sms, int smem_kb = 0) {
     const uint64_t units = bytes / (B < 16 ? 16 : B);
-    const int threads = 256, blocks = sms * 8;
+    const int threads = 256, blocks = sms * (smem_kb ? 4 : 8);
     const uint64_t iters = 64;
-    k_rand<B, INFLIGHT, WIDE><<<blocks, threads>>>(buf, units, 4, sink);
+    const size_t smem = size_t(smem_kb) * 1024;
+    cudaFuncSetAttribute(k_rand<B, INFLIGHT, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_rand<B, INFLIGHT, WIDE><<<blocks, threads, smem>>>(buf, units, 4, sink);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    k_rand<B, INFLIGHT, WIDE><<<blocks, threads>>>(buf, units, iters, sink);
+    k_rand<B, INFLIGHT, WIDE><<<blocks, threads, smem>>>(buf, units, iters, sink);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     const double acc = double(blocks) * threads * iters * INFLIGHT;
-    printf("B=%3d inflight=%d%s: %.2f G accesses/s, %.0f GB/s useful\n", B, INFLIGHT, WIDE ? " (256-bit loads)" : "", acc / ms / 1e6,
+    printf("B=%3d inflight=%d smem=%3dKBx4%s: %.2f G accesses/s, %.0f GB/s useful\n", B, INFLIGHT, smem_kb, WIDE == 1 ? " (256-bit .nc)" : WIDE == 2 ? " (ld.cg)" : WIDE == 3 ? " (L1::no_allocate)" : WIDE == 4 ? " (256 nc.no_allocate)" : WIDE == 5 ? " (256 cg)" : "", acc / ms / 1e6,
            acc * B / ms / 1e6);
 }
 
@@ -84,17 +122,15 @@ int main() {
     cudaMemset(buf, 1, bytes);
     unsigned long long* sink;
     cudaMalloc(&sink, 8);
-    run<8, 4>(buf, bytes, sink, sms);
-    run<8, 8>(buf, bytes, sink, sms);
-    run<32, 4>(buf, bytes, sink, sms);
-    run<32, 8>(buf, bytes, sink, sms);
-    run<64, 4>(buf, bytes, sink, sms);
-    run<128, 2>(buf, bytes, sink, sms);
-    run<128, 4>(buf, bytes, sink, sms);
-    run<32, 4, true>(buf, bytes, sink, sms);
-    run<32, 8, true>(buf, bytes, sink, sms);
-    run<64, 4, true>(buf, bytes, sink, sms);
-    run<128, 4, true>(buf, bytes, sink, sms);
+    run<32, 8, 1>(buf, bytes, sink, sms, 0);
+    run<32, 8, 4>(buf, bytes, sink, sms, 0);
+    run<32, 8, 5>(buf, bytes, sink, sms, 0);
+    run<32, 8, 1>(buf, bytes, sink, sms, 32);
+    run<32, 8, 4>(buf, bytes, sink, sms, 32);
+    run<32, 8, 5>(buf, bytes, sink, sms, 32);
+    run<32, 8, 1>(buf, bytes, sink, sms, 48);
+    run<32, 8, 4>(buf, bytes, sink, sms, 48);
+    run<32, 8, 5>(buf, bytes, sink, sms, 48);
     cudaError_t e = cudaDeviceSynchronize();
     printf("%s\n", cudaGetErrorString(e));
     return e != cudaSuccess;
