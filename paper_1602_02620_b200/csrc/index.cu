@@ -510,15 +510,16 @@ __global__ void __launch_bounds__(256) k_query_fused(
 // Dense queries (clustered data, cfg4): one CTA per query. Dedup is a
 // shared-memory open-addressing id set instead of a sort of the collision
 // list, so the cost follows the distinct candidates (cfg4: ~480) rather than
-// the collisions (~1900). Phase 1 probes (thread per table) and inserts into
-// the set; phase 2 walks the set, verifying four candidates per thread at a
-// time (independent row loads in flight), and appends (id << 32 | dist) to a
-// shared found list; only that list is sorted (ascending ids,
-// index.cpp:171-186). Queries: ovf[0 .. *ovf_cnt) (the warp kernel's
-// hand-over, count read on the device), or every query 0 .. direct_n when
-// ovf is null. A query with 3/4 * HS or more distinct candidates or more
-// than FCAP results, or whose results do not fit the region, goes to the
-// general path (ovf2), which recomputes all its outputs.
+// the collisions (~1900). Phase 1 probes (thread per table), inserts into the
+// set and lists the set slot of every new id; phase 2 verifies the listed
+// candidates and appends (id << 32 | dist) to a shared found list; only that
+// list is sorted (ascending ids, index.cpp:171-186). The set is cleared once
+// per CTA and afterwards only at the listed slots. Queries: ovf[0 ..
+// *ovf_cnt) (the warp kernel's hand-over, count read on the device), or every
+// query 0 .. direct_n when ovf is null, handed out one at a time. A query with
+// 3/4 * HS or more distinct candidates or more than FCAP results, or whose
+// results do not fit the region, goes to the general path (ovf2), which
+// recomputes all its outputs.
 template <typename T, int LAYOUT, int HS, int FCAP>
 __global__ void __launch_bounds__(512) k_query_dense(
     const typename T::K* __restrict__ qkeys, uint32_t tables, const Tables<T> tb, const uint64_t* __restrict__ rows,
@@ -531,12 +532,13 @@ __global__ void __launch_bounds__(512) k_query_dense(
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
     uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
+    constexpr uint32_t kMaxDistinct = HS / 4 * 3;
+    uint16_t* clist = reinterpret_cast<uint16_t*>(set + HS); // set slot of each distinct candidate
+    static_assert(HS <= 65536, "slot numbers are 16-bit");
     __shared__ unsigned int coll_s, cand_s, found_s;
     __shared__ volatile int bad_s;
     __shared__ unsigned long long base_s;
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-    constexpr uint32_t kMaxDistinct = HS / 4 * 3;
-    constexpr int kV = 4; // candidates verified per thread at a time (one LDS.128)
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
     __shared__ unsigned int next_s;
@@ -545,15 +547,16 @@ __global__ void __launch_bounds__(512) k_query_dense(
         __syncthreads();
         return next_s; // rewritten only after the body's barriers
     };
+    // the set is cleared once here and afterwards only where a query wrote
+    for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
     for (uint32_t s_ = fetch(); s_ < ns; s_ = fetch()) {
         const uint64_t q = ovf ? ovf[s_] : s_;
-        for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
         if (tid == 0) {
             coll_s = cand_s = found_s = 0;
             bad_s = 0;
         }
         __syncthreads();
-        // phase 1: probe, dedup into the set
+        // phase 1: probe, dedup into the set, list each new id's slot
         const typename T::K* qk = qkeys + q * tables;
         uint32_t coll = 0;
         for (uint32_t t = tid; t < tables; t += nt) {
@@ -567,33 +570,39 @@ __global__ void __launch_bounds__(512) k_query_dense(
                     if (old == kEmpty) break;
                     h = (h + 1) & (HS - 1);
                 }
-                if (atomicAdd(&cand_s, 1u) >= kMaxDistinct) bad_s = 1;
+                const uint32_t pos = atomicAdd(&cand_s, 1u);
+                if (pos < kMaxDistinct)
+                    clist[pos] = uint16_t(h);
+                else
+                    bad_s = 1;
             });
         }
         atomicAdd(&coll_s, coll);
         __syncthreads();
-        // phase 2: verify the distinct candidates
+        const uint32_t ncand = cand_s;
+        // phase 2: verify the distinct candidates only
         if (!bad_s) {
             const uint64_t* qr = qrows + q * words;
-            for (uint32_t i0 = tid * kV; i0 < HS; i0 += nt * kV) {
-                const uint4 v = *reinterpret_cast<const uint4*>(set + i0);
-                uint32_t id[kV] = {v.x, v.y, v.z, v.w}, d[kV] = {0, 0, 0, 0};
-                for (uint32_t w = 0; w < words; ++w) {
-                    const uint64_t qw = __ldg(qr + w);
-#pragma unroll
-                    for (int u = 0; u < kV; ++u)
-                        if (id[u] != kEmpty) d[u] += __popcll(__ldg(rows + uint64_t(id[u]) * words + w) ^ qw);
+            for (uint32_t k = tid; k < ncand; k += nt) {
+                const uint32_t id = set[clist[k]];
+                const uint64_t* r = rows + uint64_t(id) * words;
+                uint32_t d = 0;
+                for (uint32_t w = 0; w < words; ++w) d += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+                if (d <= radius) {
+                    const uint32_t pos = atomicAdd(&found_s, 1u);
+                    if (pos < FCAP)
+                        fl[pos] = (static_cast<unsigned long long>(id) << 32) | d;
+                    else
+                        bad_s = 1;
                 }
-#pragma unroll
-                for (int u = 0; u < kV; ++u)
-                    if (id[u] != kEmpty && d[u] <= radius) {
-                        const uint32_t pos = atomicAdd(&found_s, 1u);
-                        if (pos < FCAP)
-                            fl[pos] = (static_cast<unsigned long long>(id[u]) << 32) | d[u];
-                        else
-                            bad_s = 1;
-                    }
             }
+        }
+        __syncthreads();
+        // clear what this query wrote (all of it when the list is incomplete)
+        if (ncand <= kMaxDistinct) {
+            for (uint32_t k = tid; k < ncand; k += nt) set[clist[k]] = kEmpty;
+        } else {
+            for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
         }
         __syncthreads();
         const uint32_t nf = found_s;
@@ -878,7 +887,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
                 cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
-    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4;
+    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
     // persistent grid: the overflow count is only known on the device
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
