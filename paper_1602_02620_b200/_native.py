@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfclsh_b200.so")
+# FCLSH_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FCLSH_LIB") or os.path.join(HERE, "lib", "libfclsh_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fclsh_gpu.h")
 
 u8p = C.POINTER(C.c_uint8)

@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace fclsh_b200 {
@@ -81,6 +82,10 @@ struct WideEntry { // 8-byte keys: {key, id}
 };
 
 constexpr int kSlots = 4; // per bucket
+#ifndef FCLSH_FUSED_CAP
+#define FCLSH_FUSED_CAP 256
+#endif
+constexpr int kFusedCap = FCLSH_FUSED_CAP; // warp-kernel id-set slots (3/4 of it: distinct ids; more: the CTA kernel)
 
 // One bucket (4 slots) with 256-bit loads: a random probe is one L1 request
 // for the narrow layout (two for wide) instead of four 64-bit ones; the
@@ -329,10 +334,18 @@ __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ d
 
 // ----------------------------------------------------------------- query
 
-// K3+K4+K5 fused, one warp per query (the common path). A query whose list
-// exceeds CAP or whose results exceed slot_cap is queued for the general
-// path (overflow list), which then writes all of that query's outputs.
-template <typename T, int LAYOUT, int CAP, int U>
+// K3+K4+K5 fused, one warp per query (the common path). Lanes probe tables
+// lane, lane+32, ... (U in flight); every colliding id goes into a per-warp
+// shared-memory open-addressing set of WS slots, so only distinct candidates
+// are kept (cfg2: ~1.1 distinct of ~103 collisions) and no collision list is
+// sorted. Lanes then verify the set's ids, the found (id, dist) pairs are
+// sorted in registers (at most 32, one per lane) and written to the query's
+// slots. The small footprint (WS ids per warp) leaves most of the unified
+// L1/shared array to L1, which holds the lines of the probes in flight. A
+// query with more than 3/4 * WS distinct candidates or more than slot_cap
+// results is handed to the CTA kernel (overflow list), which then writes all
+// of that query's outputs.
+template <typename T, int LAYOUT, int WS, int U>
 __global__ void __launch_bounds__(256) k_query_fused(
     const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -341,10 +354,15 @@ __global__ void __launch_bounds__(256) k_query_fused(
     uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
     unsigned int* __restrict__ qnext) {
     using E = typename T::E;
+    static_assert((WS & (WS - 1)) == 0 && WS >= 128 && WS % 32 == 0, "set size");
+    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+    constexpr uint32_t kMaxD = WS / 4 * 3; // distinct ids a query may have here (set load <= 3/4 + 32)
+    constexpr int kLogWS = __builtin_ctz(WS);
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* cnt_s = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* ids = reinterpret_cast<uint32_t*>(smem) + 8 + warp * CAP;
+    unsigned int* dcnt_s = reinterpret_cast<unsigned int*>(smem); // [8] distinct ids per warp
+    uint32_t* set = reinterpret_cast<uint32_t*>(smem) + 8 + warp * WS;
+    for (int k = lane; k < WS; k += 32) set[k] = kEmpty; // afterwards cleared as it is read
     // queries are handed out one at a time (a warp that finishes early takes
     // the next), so the last wave does not leave most warps idle
     auto fetch = [&]() -> uint64_t {
@@ -353,12 +371,21 @@ __global__ void __launch_bounds__(256) k_query_fused(
         return __shfl_sync(0xffffffffu, v, 0);
     };
     for (uint64_t q = fetch(); q < nq; q = fetch()) {
-        if (lane == 0) cnt_s[warp] = 0;
+        if (lane == 0) dcnt_s[warp] = 0;
         __syncwarp();
         const typename T::K* qk = qkeys + q * tables;
+        uint32_t coll = 0; // this lane's postings
         auto push = [&](uint32_t id) {
-            const uint32_t pos = atomicAdd(cnt_s + warp, 1u);
-            if (pos < CAP) ids[pos] = id;
+            ++coll;
+            if (dcnt_s[warp] >= kMaxD) return; // overflowing: only the count matters now
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - kLogWS);
+            for (;;) {
+                const uint32_t old = atomicCAS(set + h, kEmpty, id);
+                if (old == id) return; // seen
+                if (old == kEmpty) break;
+                h = (h + 1) & (WS - 1);
+            }
+            atomicAdd(dcnt_s + warp, 1u);
         };
         for (uint32_t t0 = 0; t0 < tables; t0 += 32 * U) {
             uint64_t key[U];
@@ -392,9 +419,8 @@ __global__ void __launch_bounds__(256) k_query_fused(
 #pragma unroll
                 for (int u = 0; u < U; ++u) { // U home buckets in flight
                     const uint32_t t = t0 + u * 32 + lane;
-                    if (t < tables) {
+                    if (t < tables)
                         load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
-                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -419,88 +445,68 @@ __global__ void __launch_bounds__(256) k_query_fused(
                 }
             }
             __syncwarp();
-            if (cnt_s[warp] > CAP) break; // overflowing: the dense kernel redoes it
+            // too many distinct ids: the CTA kernel redoes it (a vote keeps the exit warp-uniform)
+            if (__any_sync(0xffffffffu, dcnt_s[warp] >= kMaxD)) break;
         }
         __syncwarp();
-        const uint32_t m = cnt_s[warp];
-        if (m > CAP) {
-            if (lane == 0) {
-                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
-                found_q[q] = 0; // written by the general path later
-                src_pos[q] = 0;
-            }
-            continue;
-        }
-        // dedup: ascending-only bitonic sort of the list (padding = +inf)
-        uint32_t P = 1, lp = 0;
-        while (P < m) {
-            P <<= 1;
-            ++lp;
-        }
-        for (uint32_t i = m + lane; i < P; i += 32) ids[i] = 0xFFFFFFFFu;
-        __syncwarp();
-        for (uint32_t lk = 1; lk <= lp; ++lk) {
-            const uint32_t k = 1u << lk;
-            for (uint32_t i = lane; i < P / 2; i += 32) {
-                const uint32_t blk = i >> (lk - 1), off = i & ((k >> 1) - 1);
-                const uint32_t lo = blk * k + off, hi = blk * k + k - 1 - off;
-                const uint32_t x = ids[lo], y = ids[hi];
-                if (y < x) {
-                    ids[lo] = y;
-                    ids[hi] = x;
-                }
-            }
-            __syncwarp();
-            for (int lj = int(lk) - 2; lj >= 0; --lj) {
-                const uint32_t j = 1u << lj;
-                for (uint32_t i = lane; i < P / 2; i += 32) {
-                    const uint32_t lo = ((i >> lj) << (lj + 1)) + (i & (j - 1)), hi = lo + j;
-                    const uint32_t x = ids[lo], y = ids[hi];
-                    if (y < x) {
-                        ids[lo] = y;
-                        ids[hi] = x;
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        // verify distinct candidates, results in ascending id order
+        const uint32_t nd = __shfl_sync(0xffffffffu, dcnt_s[warp], 0);
+        const uint64_t m = __reduce_add_sync(0xffffffffu, coll);
+        // verify the distinct ids (clearing the set behind), collect passes in slot order
         const uint64_t* qr = qrows + q * words;
-        uint32_t ncand = 0, nfound = 0;
-        for (uint32_t base = 0; base < m; base += 32) {
-            const uint32_t k = base + lane;
-            const bool valid = k < m;
-            const uint32_t id = valid ? ids[k] : 0u;
-            const bool uniq = valid && (k == 0 || ids[k - 1] != id);
+        uint32_t nfound = 0;
+        unsigned long long mine = ~0ull; // this lane's found (id << 32 | dist), kept for the sort
+#pragma unroll 1
+        for (int k0 = 0; k0 < WS; k0 += 32) {
+            const uint32_t id = set[k0 + lane];
+            const bool valid = id != kEmpty;
+            if (valid) set[k0 + lane] = kEmpty;
             uint32_t dist = 0;
-            if (uniq) {
+            if (valid && nd < kMaxD) {
                 const uint64_t* r = rows + uint64_t(id) * words;
                 for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __ldg(qr + w));
             }
-            const bool pass = uniq && dist <= radius;
-            const uint32_t bu = __ballot_sync(0xffffffffu, uniq);
+            const bool pass = valid && nd < kMaxD && dist <= radius;
             const uint32_t bp = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
+            if (bp) {
+                // the pass of rank i among this query's passes goes to lane i
                 const uint32_t pos = nfound + __popc(bp & ((1u << lane) - 1u));
-                if (pos < slot_cap) {
-                    tmp_id[q * slot_cap + pos] = id;
-                    tmp_dist[q * slot_cap + pos] = dist;
+                const unsigned long long e = (static_cast<unsigned long long>(id) << 32) | dist;
+                for (uint32_t b = bp; b; b &= b - 1) {
+                    const int src = __ffs(b) - 1;
+                    const unsigned long long v = __shfl_sync(0xffffffffu, e, src);
+                    const uint32_t p = __shfl_sync(0xffffffffu, pos, src);
+                    if (p == uint32_t(lane)) mine = v;
                 }
+                nfound += __popc(bp);
             }
-            ncand += __popc(bu);
-            nfound += __popc(bp);
         }
-        if (nfound > slot_cap) {
+        if (nd >= kMaxD || nfound > slot_cap || nfound > 32) {
             if (lane == 0) {
                 overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
-                found_q[q] = 0; // written by the general path later
+                found_q[q] = 0; // written by the CTA kernel later
                 src_pos[q] = 0;
             }
             continue;
         }
+        // ascending ids: bitonic sort across the warp (one entry per lane, padding = +inf)
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, mine, j);
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
+                mine = (lower == up) ? lo : hi;
+            }
+        }
+        if (uint32_t(lane) < nfound) {
+            tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
+            tmp_dist[q * slot_cap + lane] = uint32_t(mine);
+        }
         if (lane == 0) {
             coll_q[q] = m;
-            cand_q[q] = ncand;
+            cand_q[q] = nd;
             found_q[q] = nfound;
             src_pos[q] = q * slot_cap;
         }
@@ -865,7 +871,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, cudaStream_t s) {
     auto kern = k_query_fused<T, LAYOUT, CAP, 4>;
-    const size_t smem = (8 + size_t(8) * CAP) * 4;
+    const size_t smem = (8 + size_t(8) * CAP) * 4; // CAP = set slots per warp
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
@@ -978,9 +984,16 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // per query, the CTA-per-query kernel for what it hands over (count read
     // on the device) or for every query, found scan, compaction + publish.
     bool capturing = false;
+    // FCLSH_DEBUG_SYNC=1: synchronize and report after every stage (eager
+    // batches only) to find a stage that faults or does not finish
+    static const bool debug_sync = getenv("FCLSH_DEBUG_SYNC") != nullptr;
     auto rec = [&](int k) { // stage events; inside a capture they must be external record nodes
         FCLSH_CUDA(capturing ? cudaEventRecordWithFlags(ix.ev[k], s, cudaEventRecordExternal)
                              : cudaEventRecord(ix.ev[k], s));
+        if (debug_sync && !capturing) {
+            FCLSH_CUDA(cudaStreamSynchronize(s));
+            fprintf(stderr, "[fclsh] query nq=%llu stage %d reached\n", (unsigned long long)nq, k);
+        }
     };
     auto enqueue_common = [&] {
         rec(0);
@@ -988,7 +1001,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(1);
         FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32, s));
         if (!dense_all)
-            launch_fused<T, LAYOUT, 1024>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+            launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
                                           tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, s);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,

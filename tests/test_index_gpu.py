@@ -91,16 +91,16 @@ def test_clustered_data_long_cells(oracle):
 
 def test_three_query_paths(oracle):
     """One batch that needs all three query kernels: warp per query (sparse),
-    CTA per query (more than 1024 collisions; more such queries than the
+    CTA per query (more than 32 results; more such queries than the
     persistent grid has CTAs) and the general sort path (more than 2048
     results)."""
     rng = np.random.default_rng(33)
     d, radius = 128, 6
     base = random_rows(rng, 700, d)
-    rows = random_rows(rng, 12000, d)
-    rows[:7000] = np.repeat(base, 10, axis=0)  # 700 values x 10 copies
-    rows[7000:9100] = base[0]  # base[0]: 2110 copies, more results than the CTA kernel holds
-    q = np.concatenate([base, random_rows(rng, 200, d), planted_queries(rng, rows[9100:], d, 100, radius)])
+    rows = random_rows(rng, 34000, d)
+    rows[:28000] = np.repeat(base, 40, axis=0)  # 700 values x 40 copies
+    rows[28000:30110] = base[0]  # base[0]: 2150 copies, more results than the CTA kernel holds
+    q = np.concatenate([base, random_rows(rng, 200, d), planted_queries(rng, rows[30110:], d, 100, radius)])
     for layout in LAYOUTS:
         force = F.PlanOverride(F.PlanKind.identity, 1)
         plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, force)
@@ -109,7 +109,7 @@ def test_three_query_paths(oracle):
         paths = ix.path_counts()
         assert paths["dense"] >= 600 and paths["general"] >= 1, paths
     res = check_against_oracle(oracle, rows, q, d, radius, (0, 1), M31)
-    assert res.found[0] >= 2110
+    assert res.found[0] >= 2150
 
 
 def test_many_tables_cta_per_query(oracle):
