@@ -85,6 +85,10 @@ constexpr int kSlots = 4; // per bucket
 #ifndef FCLSH_FUSED_CAP
 #define FCLSH_FUSED_CAP 256
 #endif
+#ifndef FCLSH_FUSED_U
+#define FCLSH_FUSED_U 2
+#endif
+constexpr int kFusedU = FCLSH_FUSED_U; // tables per lane in flight in the warp kernel
 constexpr int kFusedCap = FCLSH_FUSED_CAP; // warp-kernel id-set slots (3/4 of it: distinct ids; more: the CTA kernel)
 
 // One bucket (4 slots) with 256-bit loads: a random probe is one L1 request
@@ -870,7 +874,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, cudaStream_t s) {
-    auto kern = k_query_fused<T, LAYOUT, CAP, 4>;
+    auto kern = k_query_fused<T, LAYOUT, CAP, kFusedU>;
     const size_t smem = (8 + size_t(8) * CAP) * 4; // CAP = set slots per warp
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
     const uint64_t grid =
