@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(512) k_query_dense(
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
+    if (blockIdx.x >= ns) return; // at most ns CTAs can get a query (usually ns == 0: nothing handed over)
     __shared__ unsigned int next_s;
     auto fetch = [&]() -> uint32_t { // dynamic hand-out: query costs vary widely on clustered data
         if (tid == 0) next_s = atomicAdd(qnext, 1u);
