@@ -205,7 +205,10 @@ typedef struct {
 } fclsh_result;
 
 /* Host rows in, host result out (the library allocates; free with
- * fclsh_result_free). Synchronous. */
+ * fclsh_result_free). Synchronous. q_rows may be pinned (page-locked) host
+ * memory for a full-speed upload. The result is one pinned block (its
+ * arrays are slices of it) taken from a pool that fclsh_result_free refills,
+ * so the download runs at full speed without a staging copy. */
 int fclsh_query(fclsh_index* ix, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
                 fclsh_result** out);
 void fclsh_result_free(fclsh_result* r);

@@ -115,6 +115,60 @@ void need(const void* p, const char* what) {
     if (!p) throw UsageError(std::string(what) + " must not be NULL");
 }
 
+// fclsh_query results live in pinned blocks (device-to-host copies run at
+// full speed, no staging) recycled through this pool, so a steady stream of
+// batches does not pay cudaHostAlloc per call. A block starts with a header
+// {magic, capacity}; fclsh_result_free hands it back.
+constexpr size_t kResultHeader = 64;
+constexpr uint64_t kResultMagic = 0x66636c7368726573ull; // "fclshres"
+class PinnedPool {
+  public:
+    void* take(size_t bytes) {
+        size_t cap = 4096;
+        while (cap < bytes) cap <<= 1;
+        void* p = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = free_.find(cap);
+            if (it != free_.end()) {
+                p = it->second;
+                free_.erase(it);
+                cached_ -= cap;
+            }
+        }
+        if (!p && cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            throw ResourceError("query: pinned host memory for the result exhausted");
+        }
+        static_cast<uint64_t*>(p)[0] = kResultMagic;
+        static_cast<uint64_t*>(p)[1] = cap;
+        return p;
+    }
+    void give(void* blk) {
+        auto* h = static_cast<uint64_t*>(blk);
+        if (h[0] != kResultMagic) return; // not ours: leave it alone
+        const size_t cap = h[1];
+        h[0] = 0;
+        std::lock_guard<std::mutex> lk(mu_);
+        if (cached_ + cap <= (size_t(256) << 20)) {
+            free_.emplace(cap, blk);
+            cached_ += cap;
+        } else {
+            cudaFreeHost(blk);
+        }
+    }
+
+  private:
+    std::mutex mu_;
+    std::multimap<size_t, void*> free_;
+    size_t cached_ = 0;
+};
+
+PinnedPool& pinned_pool() {
+    static PinnedPool* pool = new PinnedPool; // never destroyed: CUDA may be torn down first at exit
+    return *pool;
+}
+
 } // namespace
 
 extern "C" {
@@ -339,35 +393,32 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
         if (nq) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
         QueryOutput o = query_device(ix, dq, nq, radius, ix.stream);
-        auto* r = static_cast<fclsh_result*>(std::calloc(1, sizeof(fclsh_result)));
-        if (!r) throw std::bad_alloc();
+        // one pinned block per result: [header | fclsh_result | counters | id | distance | query]
+        const uint64_t qb = (nq + 1) * 8, tb = std::max<uint64_t>(1, o.total) * 4;
+        const size_t bytes = kResultHeader + sizeof(fclsh_result) + 4 * qb + 3 * (tb + 16);
+        auto* blk = static_cast<unsigned char*>(pinned_pool().take(bytes));
+        auto* r = reinterpret_cast<fclsh_result*>(blk + kResultHeader);
+        std::memset(r, 0, sizeof(fclsh_result));
+        unsigned char* p = blk + kResultHeader + ((sizeof(fclsh_result) + 15) & ~size_t(15));
         r->nq = nq;
         r->total = o.total;
-        const uint64_t tb = std::max<uint64_t>(1, o.total) * 4, qb = (nq + 1) * 8;
-        r->query = static_cast<uint32_t*>(std::malloc(tb));
-        r->id = static_cast<uint32_t*>(std::malloc(tb));
-        r->distance = static_cast<uint32_t*>(std::malloc(tb));
-        r->offsets = static_cast<uint64_t*>(std::malloc(qb));
-        r->collisions = static_cast<uint64_t*>(std::malloc(qb));
-        r->candidates = static_cast<uint64_t*>(std::malloc(qb));
-        r->found = static_cast<uint64_t*>(std::malloc(qb));
-        if (!r->query || !r->id || !r->distance || !r->offsets || !r->collisions || !r->candidates || !r->found) {
-            fclsh_result_free(r);
-            throw std::bad_alloc();
-        }
+        r->offsets = reinterpret_cast<uint64_t*>(p); // device layout: offsets | collisions | candidates | found
+        r->collisions = r->offsets + (nq + 1);
+        r->candidates = r->offsets + 2 * (nq + 1);
+        r->found = r->offsets + 3 * (nq + 1);
+        p += 4 * qb;
+        r->id = reinterpret_cast<uint32_t*>(p);
+        r->distance = reinterpret_cast<uint32_t*>(p + ((tb + 15) & ~uint64_t(15)));
+        r->query = reinterpret_cast<uint32_t*>(p + 2 * ((tb + 15) & ~uint64_t(15)));
         cudaStream_t s = ix.stream;
+        FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
         if (o.total) {
-            FCLSH_CUDA(cudaMemcpyAsync(r->query, o.d_query, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
         }
-        FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, (nq + 1) * 8, cudaMemcpyDeviceToHost, s));
-        if (nq) {
-            FCLSH_CUDA(cudaMemcpyAsync(r->collisions, o.d_coll, nq * 8, cudaMemcpyDeviceToHost, s));
-            FCLSH_CUDA(cudaMemcpyAsync(r->candidates, o.d_cand, nq * 8, cudaMemcpyDeviceToHost, s));
-            FCLSH_CUDA(cudaMemcpyAsync(r->found, o.d_found, nq * 8, cudaMemcpyDeviceToHost, s));
-        }
         FCLSH_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t q = 0; q < nq; ++q) // the query column follows from the offsets
+            for (uint64_t k = r->offsets[q]; k < r->offsets[q + 1]; ++k) r->query[k] = uint32_t(q);
         ix.collect_stages();
         r->time_hash_ms = ix.t_hash_ms;
         r->time_probe_ms = ix.t_probe_ms;
@@ -378,14 +429,7 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
 
 void fclsh_result_free(fclsh_result* r) {
     if (!r) return;
-    std::free(r->query);
-    std::free(r->id);
-    std::free(r->distance);
-    std::free(r->offsets);
-    std::free(r->collisions);
-    std::free(r->candidates);
-    std::free(r->found);
-    std::free(r);
+    pinned_pool().give(reinterpret_cast<unsigned char*>(r) - kResultHeader);
 }
 
 int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius, void* stream,

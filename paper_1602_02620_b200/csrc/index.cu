@@ -933,10 +933,13 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     const bool big = T_ > 600;
     const uint32_t slot_cap = 32; // results per query in the warp kernel's slots
     K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
-    auto* coll_q = static_cast<unsigned long long*>(ix.coll.ensure((nq + 1) * 8));
-    auto* cand_q = static_cast<unsigned long long*>(ix.cand_cnt.ensure((nq + 1) * 8));
-    auto* found_q = static_cast<unsigned long long*>(ix.found.ensure((nq + 1) * 8));
-    auto* res_off = static_cast<unsigned long long*>(ix.res_off.ensure((nq + 1) * 8));
+    // per-query outputs in one block [offsets | collisions | candidates | found],
+    // nq + 1 words each, so a host caller reads them back with one copy
+    auto* counters = static_cast<unsigned long long*>(ix.counters.ensure(4 * (nq + 1) * 8));
+    auto* res_off = counters;
+    auto* coll_q = counters + (nq + 1);
+    auto* cand_q = counters + 2 * (nq + 1);
+    auto* found_q = counters + 3 * (nq + 1);
     auto* src_pos = static_cast<unsigned long long*>(ix.src_pos.ensure((nq + 1) * 8));
     uint32_t* tmp_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
     uint32_t* tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));

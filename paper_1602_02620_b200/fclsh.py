@@ -72,6 +72,19 @@ def _release(obj, destroy: str) -> None:
     obj._h = None
 
 
+class _ResultBlock:
+    """Owns one fclsh_result (a pinned block); frees it when collected."""
+
+    def __init__(self, rp):
+        self._rp = rp
+
+    def __del__(self, _lib=N.lib):
+        try:
+            _lib().fclsh_result_free(self._rp)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
 def _u64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.uint64)
 
@@ -375,22 +388,23 @@ class IndexSet:
             raise UsageError("query width does not match the index")
         rp = C.POINTER(N.Result)()
         _check(N.lib().fclsh_query(self._h, _ptr(q, N.u64p), nq, radius, C.byref(rp)))
-        try:
-            r = rp.contents
-            tot = int(r.total)
+        owner = _ResultBlock(rp)  # the arrays below are views of its pinned block
+        r = rp.contents
+        tot = int(r.total)
 
-            def arr(p, cnt, dt):
-                if cnt == 0:
-                    return np.zeros(0, dt)
-                return np.ctypeslib.as_array(p, shape=(cnt,)).copy().astype(dt, copy=False)
+        def arr(p, cnt, ct, dt):
+            if cnt == 0:
+                return np.zeros(0, dt)
+            buf = (ct * cnt).from_address(C.cast(p, C.c_void_p).value)
+            buf._owner = owner  # freed (fclsh_result_free) when the last view is gone
+            return np.frombuffer(buf, dtype=dt)
 
-            res = QueryResults(arr(r.query, tot, np.uint32), arr(r.id, tot, np.uint32), arr(r.distance, tot, np.uint32),
-                               arr(r.offsets, nq + 1, np.uint64), arr(r.collisions, nq, np.uint64),
-                               arr(r.candidates, nq, np.uint64), arr(r.found, nq, np.uint64),
-                               float(r.time_hash_ms), float(r.time_probe_ms), float(r.time_verify_ms))
-        finally:
-            N.lib().fclsh_result_free(rp)
-        return res
+        return QueryResults(arr(r.query, tot, C.c_uint32, np.uint32), arr(r.id, tot, C.c_uint32, np.uint32),
+                            arr(r.distance, tot, C.c_uint32, np.uint32),
+                            arr(r.offsets, nq + 1, C.c_uint64, np.uint64),
+                            arr(r.collisions, nq, C.c_uint64, np.uint64),
+                            arr(r.candidates, nq, C.c_uint64, np.uint64), arr(r.found, nq, C.c_uint64, np.uint64),
+                            float(r.time_hash_ms), float(r.time_probe_ms), float(r.time_verify_ms))
 
     STAGES = ("hash", "fused", "dense", "found_scan", "compact", "overflow")
 
