@@ -416,7 +416,7 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
             FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
         }
-        FCLSH_CUDA(cudaStreamSynchronize(s));
+        stream_spin_wait(s);
         for (uint64_t q = 0; q < nq; ++q) // the query column follows from the offsets
             for (uint64_t k = r->offsets[q]; k < r->offsets[q + 1]; ++k) r->query[k] = uint32_t(q);
         ix.collect_stages();

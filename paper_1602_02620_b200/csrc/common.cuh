@@ -41,6 +41,17 @@ inline int sm_count(int device) {
     return v;
 }
 
+// Waits for the stream by polling (a blocking cudaStreamSynchronize may
+// yield the thread and add tens of microseconds of wake-up to a ~0.3 ms
+// query batch).
+inline void stream_spin_wait(cudaStream_t s) {
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) FCLSH_CUDA(e);
+    }
+}
+
 // Resident CTAs per SM of kern at (threads, dynamic smem) on device, raising
 // the kernel's dynamic-smem limit first. Cached: the attribute call and the
 // occupancy query cost host microseconds on every query batch otherwise.
