@@ -89,6 +89,8 @@ SIGNATURES = {
     "fclsh_query_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, C.POINTER(DeviceResult)]),
     "fclsh_query_stage_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
     "fclsh_query_path_counts": (C.c_int, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "fclsh_query_stage_timing": (C.c_int, [vp, C.c_int]),
+    "fclsh_query_batch_ms": (C.c_int, [vp, C.POINTER(C.c_double)]),
     "fclsh_result_copy_device": (C.c_int, [C.POINTER(DeviceResult), vp, C.c_uint64, vp, vp, C.c_int, vp]),
     "fclsh_merge_shards": (C.c_int, [C.c_uint32, C.c_uint64, vp, vp, C.c_uint64, vp, C.c_uint64, vp, C.c_int, vp]),
     "fclsh_launch_count": (C.c_uint64, []),

@@ -497,6 +497,26 @@ int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n) {
     return k;
 }
 
+int fclsh_query_stage_timing(fclsh_index* ix, int enable) {
+    if (!ix) {
+        g_err = "fclsh_query_stage_timing: NULL index";
+        return FCLSH_ERR_USAGE;
+    }
+    ix->ix->stage_timing = enable != 0;
+    return FCLSH_OK;
+}
+
+int fclsh_query_batch_ms(const fclsh_index* ix, double* ms) {
+    if (!ix || !ms) {
+        g_err = "fclsh_query_batch_ms: NULL argument";
+        return FCLSH_ERR_USAGE;
+    }
+    return guarded([&] {
+        ix->ix->collect_stages();
+        *ms = ix->ix->batch_ms;
+    });
+}
+
 int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* general) {
     if (!ix) {
         g_err = "fclsh_query_path_counts: NULL index";

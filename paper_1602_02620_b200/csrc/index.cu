@@ -995,7 +995,10 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // FCLSH_DEBUG_SYNC=1: synchronize and report after every stage (eager
     // batches only) to find a stage that faults or does not finish
     static const bool debug_sync = getenv("FCLSH_DEBUG_SYNC") != nullptr;
+    const bool timing = ix.stage_timing;
     auto rec = [&](int k) { // stage events; inside a capture they must be external record nodes
+        // (each costs ~4 us in a replayed graph: only the batch bounds unless stage timing is on)
+        if (!timing && k != 0 && k != 5) return;
         FCLSH_CUDA(capturing ? cudaEventRecordWithFlags(ix.ev[k], s, cudaEventRecordExternal)
                              : cudaEventRecord(ix.ev[k], s));
         if (debug_sync && !capturing) {
@@ -1032,7 +1035,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         const std::vector<const void*> key = {d_q, reinterpret_cast<const void*>(nq),
                                               reinterpret_cast<const void*>(uintptr_t(radius)), s, qkeys, coll_q,
                                               cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
-                                              ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq};
+                                              ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq,
+                                              reinterpret_cast<const void*>(uintptr_t(timing))};
         if (ix.gexec && key == ix.gkey) {
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
@@ -1275,20 +1279,30 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));
     }
     ix.stages_pending = true;
+    ix.stages_timed = ix.stage_timing;
     return o;
 }
 
 void DeviceIndex::collect_stages() {
     if (!stages_pending) return;
     FCLSH_CUDA(cudaEventSynchronize(ev[kStages]));
+    float total = 0;
+    FCLSH_CUDA(cudaEventElapsedTime(&total, ev[0], ev[5]));
+    batch_ms = total;
     for (int i = 0; i < kStages; ++i) {
+        stage_ms[i] = -1; // not measured (stage timing off)
+        if (!stages_timed && i < 5) continue;
         float ms = 0;
         FCLSH_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
         stage_ms[i] = ms;
     }
-    t_hash_ms = stage_ms[0];
-    t_probe_ms = stage_ms[1] + stage_ms[2] + stage_ms[5]; // probe + dedup + verify are fused
-    t_verify_ms = stage_ms[3] + stage_ms[4];              // result assembly
+    if (stages_timed) {
+        t_hash_ms = stage_ms[0];
+        t_probe_ms = stage_ms[1] + stage_ms[2] + stage_ms[5]; // probe + dedup + verify are fused
+        t_verify_ms = stage_ms[3] + stage_ms[4];              // result assembly
+    } else {
+        t_hash_ms = t_probe_ms = t_verify_ms = -1;
+    }
     stages_pending = false;
 }
 

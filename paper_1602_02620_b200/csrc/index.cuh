@@ -73,7 +73,11 @@ struct DeviceIndex {
     double stage_ms[kStages] = {};
     cudaEvent_t ev[kStages + 1] = {};
     bool stages_pending = false;
-    void collect_stages(); // waits for the last batch, fills stage_ms / t_*_ms
+    // per-stage events cost ~4 us each in a replayed graph: off by default,
+    // the batch total (batch_ms) is always measured
+    bool stage_timing = false, stages_timed = false;
+    double batch_ms = 0;
+    void collect_stages(); // waits for the last batch, fills stage_ms / t_*_ms (-1 = not measured)
 
     ~DeviceIndex();
     uint64_t cells() const { return uint64_t(1) << dir_bits; }

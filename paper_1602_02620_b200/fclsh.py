@@ -416,6 +416,16 @@ class IndexSet:
             _check(-k)
         return {name: float(buf[i]) for i, name in enumerate(self.STAGES[:k])}
 
+    def stage_timing(self, enable: bool = True) -> None:
+        """Per-stage CUDA events on the next batches (off by default: ~4 us each)."""
+        _check(N.lib().fclsh_query_stage_timing(self._h, int(bool(enable))))
+
+    def batch_ms(self) -> float:
+        """Device time of the last batch (hash .. compaction)."""
+        ms = C.c_double(0)
+        _check(N.lib().fclsh_query_batch_ms(self._h, C.byref(ms)))
+        return float(ms.value)
+
     def path_counts(self) -> dict:
         """Queries of the last batch served by the dense (CTA) kernel and by the general path."""
         dense, general = C.c_uint64(0), C.c_uint64(0)
