@@ -344,6 +344,7 @@ def main():
     e2e = {"value": nq * e2e_steps / sum(e2e_t), "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
            "d2h_bytes_per_step": int(rr.id.size * 8 + 4 * (nq + 1) * 8),
            "steps": e2e_steps, "ms_per_step_median": 1e3 * statistics.median(e2e_t),
+           "ms_per_step_min_max": [1e3 * min(e2e_t), 1e3 * max(e2e_t)],
            "api": "fclsh_query (include/fclsh_gpu.h): pinned rows in, pinned result block out"}
 
     # ---------------- CPU baseline + parity against the reference on the same batch

@@ -122,15 +122,25 @@ int main() {
     cudaMemset(buf, 1, bytes);
     unsigned long long* sink;
     cudaMalloc(&sink, 8);
-    run<32, 8, 1>(buf, bytes, sink, sms, 0);
-    run<32, 8, 4>(buf, bytes, sink, sms, 0);
-    run<32, 8, 5>(buf, bytes, sink, sms, 0);
-    run<32, 8, 1>(buf, bytes, sink, sms, 32);
-    run<32, 8, 4>(buf, bytes, sink, sms, 32);
-    run<32, 8, 5>(buf, bytes, sink, sms, 32);
-    run<32, 8, 1>(buf, bytes, sink, sms, 48);
-    run<32, 8, 4>(buf, bytes, sink, sms, 48);
-    run<32, 8, 5>(buf, bytes, sink, sms, 48);
+    // access size and loads in flight per thread (16-byte .nc loads)
+    run<8, 4>(buf, bytes, sink, sms);
+    run<32, 4>(buf, bytes, sink, sms);
+    run<32, 8>(buf, bytes, sink, sms);
+    run<64, 4>(buf, bytes, sink, sms);
+    run<128, 4>(buf, bytes, sink, sms);
+    // load flavour for 32-byte accesses
+    run<32, 4, 1>(buf, bytes, sink, sms);
+    run<32, 8, 1>(buf, bytes, sink, sms);
+    run<32, 16, 1>(buf, bytes, sink, sms);
+    run<32, 8, 2>(buf, bytes, sink, sms);
+    run<32, 8, 3>(buf, bytes, sink, sms);
+    run<32, 8, 4>(buf, bytes, sink, sms);
+    run<32, 8, 5>(buf, bytes, sink, sms);
+    // shared-memory pressure (4 CTAs of 256 threads per SM)
+    for (int kb : {0, 32, 48}) {
+        run<32, 8, 1>(buf, bytes, sink, sms, kb);
+        run<32, 8, 4>(buf, bytes, sink, sms, kb);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     printf("%s\n", cudaGetErrorString(e));
     return e != cudaSuccess;
