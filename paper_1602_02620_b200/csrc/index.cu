@@ -159,14 +159,17 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
 
 // keys are point-major for one part: key of (row i, table t) at keys[i*L + t]
 template <typename T>
-__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t shift,
-                                uint64_t nbuckets, typename T::E* __restrict__ buckets) {
-    const uint64_t total = n * L;
+__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0,
+                                uint32_t tg, uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets) {
+    // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
+    // their postings are inserted (all 511 at once thrash it: 43 GB of DRAM
+    // reads for 8.6 GB of tables); keys are read tg at a time per row
+    const uint64_t total = n * tg;
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = x / L;
-        const uint32_t t = uint32_t(x % L);
+        const uint64_t i = x / tg;
+        const uint32_t t = t0 + uint32_t(x % tg);
         typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
-        const uint64_t key = keys[x];
+        const uint64_t key = keys[i * L + t];
         const typename T::E e = T::make(key, uint32_t(i));
         uint64_t b = key >> shift;
         for (;;) {
@@ -857,9 +860,15 @@ void build_all(DeviceIndex& ix) {
         hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, L, kLayoutPointMajor, s, p, 1);
         if (ix.layout == kLayoutBuckets) {
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
-            k_bucket_insert<T><<<grid_for(n * L, ix.device, 256, 8), 256, 0, s>>>(
-                static_cast<const K*>(keys.p), n, uint32_t(L), ix.key_shift, ix.nbuckets, bk);
-            FCLSH_LAUNCHED();
+            // table groups of ~64 MB of buckets (half the L2)
+            const uint64_t tbytes = ix.nbuckets * kSlots * sizeof(typename T::E);
+            const uint32_t tg = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (uint64_t(64) << 20) / tbytes)));
+            for (uint32_t t0 = 0; t0 < L; t0 += tg) {
+                const uint32_t c = uint32_t(std::min<uint64_t>(tg, L - t0));
+                k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(
+                    static_cast<const K*>(keys.p), n, uint32_t(L), t0, c, ix.key_shift, ix.nbuckets, bk);
+                FCLSH_LAUNCHED();
+            }
         } else {
             for (uint32_t t = 0; t < L; t += chunk) {
                 const uint32_t c = uint32_t(std::min<uint64_t>(chunk, L - t));
