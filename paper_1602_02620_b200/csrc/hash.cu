@@ -31,6 +31,7 @@
 #include "hash.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace fclsh_b200 {
@@ -596,6 +597,169 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_m31_pm(const 
     }
 }
 
+// FP64 variant of the point-major kernel for direct families. The sketch t
+// and every partial transform are exact doubles (|F| <= d * 2^31 < 2^53 for
+// d < 2^22), so one butterfly is a single DADD instead of one 32-bit add on
+// each of two planes, and the FP64 pipe runs beside the integer pipes that do
+// the sketch and the reduction. The last stage computes (T + 2^52) - F: for
+// 0 <= D = T - F < 2^52 that double is exact and its low 52 mantissa bits are
+// D, so the final reduction needs no float-to-int conversion.
+template <int LOGN>
+__global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const FastParams p) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = lanes_for(LOGN);
+    constexpr int E = N / G;
+    constexpr int EP = E + 2; // padded transpose row (doubles)
+    constexpr int EG = E / G;
+    constexpr int SPW = 32 / G; // rows per warp
+    constexpr int WARPS = pm_warps<LOGN>();
+    constexpr int NT = 32 * WARPS;
+    constexpr int NP = N / 2; // column pairs per part
+    static_assert(G > 1 && (EG == 1 || EG == 2), "phase-2 layout");
+    constexpr double kTwo52 = 4503599627370496.0;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* xbuf = reinterpret_cast<double*>(smem);                            // WARPS x 32*EP
+    uint64_t* rows_s = reinterpret_cast<uint64_t*>(xbuf + WARPS * 32 * EP);    // WARPS x SPW x row_words
+    double2* seed_s = reinterpret_cast<double2*>(rows_s + WARPS * SPW * p.row_words); // [parts][NP]
+    uint2* pos_s = reinterpret_cast<uint2*>(seed_s + p.parts * NP);            // [parts][NP]
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int slot = lane / G; // row within the warp
+    const int g = lane % G;
+
+    // the direct table holds {pos, seed} for column pairs, lane-fastest: pair
+    // i = (j/2)*G + g of a part is entries 2i, 2i+1 -> positions and seeds apart
+    for (uint32_t i = tid; i < p.parts * NP; i += NT) {
+        const uint2 e0 = p.fam[2 * i], e1 = p.fam[2 * i + 1];
+        pos_s[i] = make_uint2(e0.x, e1.x);
+        seed_s[i] = make_double2(double(e0.y), double(e1.y));
+    }
+    __syncthreads();
+
+    double* xw = xbuf + warp * 32 * EP;                     // this warp's transpose region
+    uint64_t* rw = rows_s + warp * SPW * p.row_words;       // this warp's rows
+    const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rw + slot * p.row_words);
+    double* xs = xw + slot * G * EP;                        // this row's transpose region
+    double* xs_w = xs + g * EP;                             // phase-1 row of this lane
+    const double* xs_r = xs + g * EG;                       // phase-2 column of this lane
+
+    const uint64_t groups = (p.n + SPW - 1) / SPW;
+    const uint64_t nwarps = uint64_t(gridDim.x) * WARPS;
+    for (uint64_t grp = uint64_t(blockIdx.x) * WARPS + warp; grp < groups; grp += nwarps) {
+        const uint64_t p0 = grp * SPW;
+        {
+            const uint64_t base = p0 * p.row_words;
+            const uint64_t lim = p.n * p.row_words;
+            for (uint32_t i = lane; i < SPW * p.row_words; i += 32)
+                rw[i] = (base + i < lim) ? __ldg(p.rows + base + i) : 0ull;
+        }
+        __syncwarp();
+        const uint64_t my_point = p0 + slot;
+
+        for (uint32_t part = 0; part < p.parts; ++part) {
+            const uint2* ps = pos_s + part * NP + g;
+            const double2* sd = seed_s + part * NP + g;
+            double x[E];
+            // sketch: seed where the row bit is set, +0.0 elsewhere (a 64-bit mask)
+#pragma unroll
+            for (int j = 0; j < E; j += 2) {
+                const uint2 pp = ps[(j / 2) * G];
+                const double2 s2 = sd[(j / 2) * G];
+                // the row bit as an all-ones / zero 32-bit mask applied to both words
+                const int m0 = int(myrow[pp.x >> 5] << (31 - (pp.x & 31))) >> 31;
+                const int m1 = int(myrow[pp.y >> 5] << (31 - (pp.y & 31))) >> 31;
+                x[j] = __hiloint2double(__double2hiint(s2.x) & m0, __double2loint(s2.x) & m0);
+                x[j + 1] = __hiloint2double(__double2hiint(s2.y) & m1, __double2loint(s2.y) & m1);
+            }
+            // phase 1
+#pragma unroll
+            for (int h = 1; h < E; h <<= 1) {
+#pragma unroll
+                for (int i = 0; i < E; ++i) {
+                    if ((i & h) == 0) {
+                        const double a = x[i], b = x[i + h];
+                        x[i] = a + b;
+                        x[i + h] = a - b;
+                    }
+                }
+            }
+            // total T: sum of the G block totals (element 0 of each lane)
+            double T = x[0];
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+            const double Tp = T + kTwo52;
+            // transpose (warp-local): element c = hb*E + j lives at xs[hb*EP + j]
+#pragma unroll
+            for (int j = 0; j < E; j += 2) *reinterpret_cast<double2*>(xs_w + j) = make_double2(x[j], x[j + 1]);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                if constexpr (EG == 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(xs_r + h * EP);
+                    x[h] = v.x;
+                    x[G + h] = v.y;
+                } else {
+                    x[h] = xs_r[h * EP];
+                }
+            }
+            __syncwarp();
+            // phase 2: all but the last stage, then the last stage emits 2^52 + D
+#pragma unroll
+            for (int k = 0; k < EG; ++k) {
+                double* xl = x + k * G;
+#pragma unroll
+                for (int hs = 1; hs < G / 2; hs <<= 1) {
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        if ((i & hs) == 0) {
+                            const double a = xl[i], b = xl[i + hs];
+                            xl[i] = a + b;
+                            xl[i + hs] = a - b;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < G / 2; ++i) {
+                    const double a = xl[i], b = xl[i + G / 2];
+                    xl[i] = (Tp - a) - b;
+                    xl[i + G / 2] = (Tp - a) + b;
+                }
+            }
+            // keys straight to HBM: element (k, h) is code v = h*E + g*EG + k
+            auto finish = [](double v) -> uint32_t {
+                // D = bits & (2^52 - 1) = dh * 2^32 + lo (even), O = D / 2 = dh * 2^31 + lo / 2
+                // == dh + lo / 2 (mod P); s = that + 1 < 2^32, then the canonical fold
+                const uint32_t lo = uint32_t(__double2loint(v)), dh = uint32_t(__double2hiint(v)) & 0xFFFFFu;
+                const uint32_t s = (lo >> 1) + dh + 1u;
+                return (s & kP31) + (s >> 31) - 1u;
+            };
+            if (my_point < p.n) {
+                if (p.key_bytes == 4) {
+                    uint32_t* out = static_cast<uint32_t*>(p.keys) + my_point * p.key_stride + part * p.L +
+                                    (g * EG - 1);
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + g * EG + k != 0) out[h * E + k] = finish(x[k * G + h]);
+                } else {
+                    uint64_t* out = static_cast<uint64_t*>(p.keys) + my_point * p.key_stride + part * p.L +
+                                    (g * EG - 1);
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + g * EG + k != 0) out[h * E + k] = finish(x[k * G + h]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <int LOGN, bool DIRECT>
 size_t fast_smem_bytes(const DeviceFamilySet& fs) {
     constexpr int G = lanes_for(LOGN);
@@ -614,6 +778,20 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
         constexpr int E = (1 << LOGN) / G;
         const size_t smem_pm = size_t(WARPS) * 32 * (E + 2) * 8 + size_t(WARPS) * (32 / G) * fs.row_words * 8 +
                                size_t(fs.parts) * fs.part_words * 8;
+        // FP64 butterflies for direct families (FCLSH_HASH_INT=1 keeps the two int32 planes)
+        static const bool use_int = getenv("FCLSH_HASH_INT") != nullptr;
+        const size_t smem_f64 = size_t(WARPS) * 32 * (E + 2) * 8 + size_t(WARPS) * (32 / G) * fs.row_words * 8 +
+                                size_t(fs.parts) * (1 << LOGN) / 2 * 24;
+        if (DIRECT && !use_int && prm.layout == kLayoutPointMajor && smem_f64 <= 227 * 1024) {
+            auto kern = k_hash_f64_pm<LOGN>;
+            const int per_sm = resident_ctas(kern, 32 * WARPS, smem_f64, fs.device);
+            if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
+            const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
+            const uint64_t grid = std::min<uint64_t>((groups + WARPS - 1) / WARPS, uint64_t(per_sm) * sm_count(fs.device));
+            kern<<<unsigned(std::max<uint64_t>(grid, 1)), 32 * WARPS, smem_f64, stream>>>(prm);
+            FCLSH_LAUNCHED();
+            return;
+        }
         // (a family table too large for the 12-warp layout falls back to the staged kernel)
         if (prm.layout == kLayoutPointMajor && smem_pm <= 227 * 1024) {
             auto kern = k_hash_m31_pm<LOGN, DIRECT>;
