@@ -668,11 +668,11 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
             for (int j = 0; j < E; j += 2) {
                 const uint2 pp = ps[(j / 2) * G];
                 const double2 s2 = sd[(j / 2) * G];
-                // the row bit as an all-ones / zero 32-bit mask applied to both words
-                const int m0 = int(myrow[pp.x >> 5] << (31 - (pp.x & 31))) >> 31;
-                const int m1 = int(myrow[pp.y >> 5] << (31 - (pp.y & 31))) >> 31;
-                x[j] = __hiloint2double(__double2hiint(s2.x) & m0, __double2loint(s2.x) & m0);
-                x[j + 1] = __hiloint2double(__double2hiint(s2.y) & m1, __double2loint(s2.y) & m1);
+                // row bit -> predicate (funnel shift = 1 << (pos mod 32)), then select the seed words
+                const bool b0 = (myrow[pp.x >> 5] & __funnelshift_l(0u, 1u, pp.x)) != 0u;
+                const bool b1 = (myrow[pp.y >> 5] & __funnelshift_l(0u, 1u, pp.y)) != 0u;
+                x[j] = b0 ? s2.x : 0.0;
+                x[j + 1] = b1 ? s2.y : 0.0;
             }
             // phase 1
 #pragma unroll
