@@ -731,10 +731,11 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
             // keys straight to HBM: element (k, h) is code v = h*E + g*EG + k
             auto finish = [](double v) -> uint32_t {
                 // D = bits & (2^52 - 1) = dh * 2^32 + lo (even), O = D / 2 = dh * 2^31 + lo / 2
-                // == dh + lo / 2 (mod P); s = that + 1 < 2^32, then the canonical fold
+                // == dh + lo / 2 (mod P)
+                // O' = dh + lo/2 < 2P: one conditional subtraction, as an unsigned min
                 const uint32_t lo = uint32_t(__double2loint(v)), dh = uint32_t(__double2hiint(v)) & 0xFFFFFu;
-                const uint32_t s = (lo >> 1) + dh + 1u;
-                return (s & kP31) + (s >> 31) - 1u;
+                const uint32_t o = (lo >> 1) + dh;
+                return min(o, o - kP31);
             };
             if (my_point < p.n) {
                 if (p.key_bytes == 4) {
