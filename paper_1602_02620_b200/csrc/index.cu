@@ -120,6 +120,22 @@ struct Tables {
     uint32_t shift;            // CSR: cell = key >> shift; buckets: home = key >> shift
 };
 
+// First position in [a, e) of a CSR cell (sorted by (key, id)) whose key is
+// >= key. Clustered data makes some cells long (a run of one popular key),
+// and every other key of that cell would otherwise scan past the run.
+template <typename T>
+__device__ __forceinline__ uint32_t cell_lower_bound(const typename T::E* et, uint32_t a, uint32_t e, uint64_t key) {
+    while (e - a > 8) {
+        const uint32_t mid = a + (e - a) / 2;
+        if (T::key(et[mid]) < key)
+            a = mid + 1;
+        else
+            e = mid;
+    }
+    while (a < e && T::key(et[a]) < key) ++a;
+    return a;
+}
+
 // Calls on_id(id) for every posting of table t with this key; returns the count.
 template <typename T, int LAYOUT, typename F>
 __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, uint64_t key, F&& on_id) {
@@ -130,7 +146,7 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
         uint32_t a = __ldg(d);
         const uint32_t e = __ldg(d + 1);
         const E* et = tb.data + uint64_t(t) * tb.n;
-        while (a < e && T::key(et[a]) < key) ++a;
+        a = cell_lower_bound<T>(et, a, e, key);
         while (a < e && T::key(et[a]) == key) {
             on_id(T::id(et[a]));
             ++a;
@@ -418,7 +434,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
                 for (int u = 0; u < U; ++u) {
                     const E* et = tb.data + uint64_t(t0 + u * 32 + lane) * tb.n;
                     uint32_t a = s[u];
-                    while (a < e[u] && T::key(et[a]) < key[u]) ++a;
+                    a = cell_lower_bound<T>(et, a, e[u], key[u]);
                     while (a < e[u] && T::key(et[a]) == key[u]) push(T::id(et[a++]));
                 }
             } else {
