@@ -274,6 +274,50 @@ int fclsh_query_batch_ms(const fclsh_index* ix, double* ms);
  * NULL. Returns 0 or a negative error code. */
 int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* general);
 
+/* --------------------------------------------------------------- dataset ---
+ * The reference's containers (dataset.hpp:20-31; load_dataset /
+ * save_dataset / save_dataset_text, dataset.cpp:82-111), read into the row
+ * layout above. FCL1 rows are byte-identical to it for d % 64 == 0, so the
+ * file body is read with one fread into pinned host memory; upload copies it
+ * to the device at full speed. Errors and messages follow the reference
+ * (truncation, dirty padding bits, trailing bytes, text width / characters:
+ * DataError; unopenable path: UsageError). */
+#define FCLSH_DATASET_FCL1 1
+#define FCLSH_DATASET_TEXT 2
+typedef struct fclsh_dataset fclsh_dataset;
+/* load_dataset: sniffs the "FCL1" magic, else parses text. */
+int fclsh_dataset_load(const char* path, fclsh_dataset** out);
+/* n, dims, format and the host rows [n][ceil(dims/64)] (valid until destroy);
+ * any output may be NULL. */
+int fclsh_dataset_info_get(const fclsh_dataset* ds, uint64_t* n, uint64_t* dims, int32_t* format,
+                           const uint64_t** rows);
+/* Copies the rows to d_rows (n * ceil(dims/64) words on `device`), async on stream. */
+int fclsh_dataset_upload(const fclsh_dataset* ds, uint64_t* d_rows, int device, void* stream);
+void fclsh_dataset_destroy(fclsh_dataset* ds);
+/* save_dataset (FCLSH_DATASET_FCL1) / save_dataset_text (FCLSH_DATASET_TEXT)
+ * of host rows [n][ceil(dims/64)] (padding bits are written as zero). */
+int fclsh_dataset_save(const char* path, const uint64_t* rows, uint64_t n, uint64_t dims, int32_t format);
+
+/* ----------------------------------------------------------- linear scan ---
+ * scan_truth (workload.cpp:56-71) and distance_histogram
+ * (workload.cpp:133-151) on device rows: an exhaustive second oracle at full
+ * config scale and the reference's `linear` method. A scan handle owns its
+ * device workspace; results live until its next call. */
+typedef struct fclsh_scan fclsh_scan;
+int fclsh_scan_create(int device, fclsh_scan** out);
+void fclsh_scan_destroy(fclsh_scan* sc);
+/* Every (query, point, distance) with distance <= radius, ordered by
+ * (query, point); out's counter pointers are NULL. Synchronous (the total
+ * sizes the output). */
+int fclsh_scan_truth(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const uint64_t* d_q_rows, uint64_t nq,
+                     uint64_t dims, uint32_t radius, void* stream, fclsh_device_result* out);
+/* counts[dims + 1] (host): every pair if sample_per_query is 0 or >= n, else
+ * sample_per_query points per query drawn as the reference draws them
+ * (Rng(seed).stream("histogram").below(n), query-major). Synchronous. */
+int fclsh_distance_histogram(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const uint64_t* d_q_rows,
+                             uint64_t nq, uint64_t dims, uint64_t sample_per_query, uint64_t seed, void* stream,
+                             uint64_t* counts);
+
 /* Number of kernels the library launched on this thread since the last
  * reset (launch accounting for the bench). */
 uint64_t fclsh_launch_count(void);

@@ -104,6 +104,12 @@ class Oracle:
                                           C.c_int, C.c_int, C.c_uint32, C.c_double, C.c_uint64,
                                           C.c_uint64, C.c_int, C.c_uint64, C.c_int,
                                           C.POINTER(C.c_double), C.POINTER(C.c_int)]
+            self._ds_save = f("dataset_save")
+            self._ds_save.argtypes = [C.c_char_p, u64p, C.c_uint64, C.c_uint64, C.c_int]
+            self._ds_load = f("dataset_load")
+            self._ds_load.argtypes = [C.c_char_p, u64p, u64p, C.POINTER(u64p)]
+            self._hist = f("distance_histogram")
+            self._hist.argtypes = [u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p]
         else:
             self._hash = f("hash_batch")
             self._hash.argtypes = [u32p, u64p, C.c_uint64, C.c_uint32, C.c_uint64, u64p,
@@ -227,6 +233,31 @@ class Oracle:
         out = np.ctypeslib.as_array(ptr, shape=(max(n, 1) * 3,))[: 3 * n].copy().reshape(n, 3)
         self._free(ptr)
         return out
+
+
+    # dataset containers and the distance histogram: the compiled reference only
+    def dataset_save(self, path, rows, dims, text=False):
+        """save_dataset / save_dataset_text (dataset.cpp:82-98)."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        self._check(self._ds_save(str(path).encode(), _p(rows, u64p), rows.shape[0], dims, int(text)))
+
+    def dataset_load(self, path):
+        """load_dataset (dataset.cpp:101-111) -> (rows [n, W] uint64, dims)."""
+        n, d, ptr = C.c_uint64(0), C.c_uint64(0), u64p()
+        self._check(self._ds_load(str(path).encode(), C.byref(n), C.byref(d), C.byref(ptr)))
+        W = (d.value + 63) // 64
+        out = np.ctypeslib.as_array(ptr, shape=(max(1, n.value * W),))[: n.value * W].copy().reshape(n.value, W)
+        self._free(ptr)
+        return out, d.value
+
+    def distance_histogram(self, rows, qrows, dims, sample_per_query=0, seed=0):
+        """distance_histogram (workload.cpp:133-151): counts[dims + 1]."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        qrows = np.ascontiguousarray(qrows, dtype=np.uint64)
+        counts = np.zeros(dims + 1, np.uint64)
+        self._check(self._hist(_p(rows, u64p), rows.shape[0], _p(qrows, u64p), qrows.shape[0], dims,
+                               sample_per_query, seed, _p(counts, u64p)))
+        return counts
 
 
 class OracleIndex:

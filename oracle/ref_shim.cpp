@@ -13,6 +13,9 @@
 //   ref_index_build    -> fclsh::build_index              (index.cpp:49-119)
 //   ref_index_query    -> fclsh::query_r_nn               (index.cpp:157-188)
 //   ref_scan_truth     -> fclsh::scan_truth               (workload.cpp:56-71)
+//   ref_distance_histogram -> fclsh::distance_histogram   (workload.cpp:133-151)
+//   ref_dataset_save / ref_dataset_load -> fclsh::save_dataset[_text] /
+//                         fclsh::load_dataset             (dataset.cpp:82-111)
 //   ref_fht_mod / ref_batch_hash_kernel -> hadamard.cpp:51-72
 //
 // Rows cross the boundary as row-major uint64 words, bit i of a row in word
@@ -404,6 +407,42 @@ int ref_scan_truth(const uint64_t* rows, uint64_t n, const uint64_t* qrows, uint
             }
         *triples_out = out;
         *count = total;
+    });
+}
+
+// distance_histogram(data, queries, sample_per_query, seed): counts[dims + 1].
+int ref_distance_histogram(const uint64_t* rows, uint64_t n, const uint64_t* qrows, uint64_t nq, uint64_t dims,
+                           uint64_t sample_per_query, uint64_t seed, uint64_t* counts) {
+    return guarded([&] {
+        Dataset data = rows_to_dataset(rows, n, dims, 8);
+        Dataset qs = rows_to_dataset(qrows, nq, dims, 8);
+        std::vector<uint64_t> c = distance_histogram(data, qs, sample_per_query, seed);
+        std::copy(c.begin(), c.end(), counts);
+    });
+}
+
+// save_dataset (text == 0, FCL1) or save_dataset_text (text != 0).
+int ref_dataset_save(const char* path, const uint64_t* rows, uint64_t n, uint64_t dims, int text) {
+    return guarded([&] {
+        Dataset ds = rows_to_dataset(rows, n, dims, 1);
+        if (text)
+            save_dataset_text(ds, path);
+        else
+            save_dataset(ds, path);
+    });
+}
+
+// load_dataset; *rows_out: malloc'd [n][ceil(dims/64)] words.
+int ref_dataset_load(const char* path, uint64_t* n, uint64_t* dims, uint64_t** rows_out) {
+    return guarded([&] {
+        Dataset ds = load_dataset(path);
+        const size_t W = (ds.dims + 63) / 64;
+        uint64_t* out = static_cast<uint64_t*>(std::calloc(std::max<size_t>(1, ds.size() * W), 8));
+        for (size_t i = 0; i < ds.size(); ++i)
+            std::copy(ds[i].words().begin(), ds[i].words().end(), out + i * W);
+        *n = ds.size();
+        *dims = ds.dims;
+        *rows_out = out;
     });
 }
 

@@ -93,6 +93,17 @@ SIGNATURES = {
     "fclsh_query_batch_ms": (C.c_int, [vp, C.POINTER(C.c_double)]),
     "fclsh_result_copy_device": (C.c_int, [C.POINTER(DeviceResult), vp, C.c_uint64, vp, vp, C.c_int, vp]),
     "fclsh_merge_shards": (C.c_int, [C.c_uint32, C.c_uint64, vp, vp, C.c_uint64, vp, C.c_uint64, vp, C.c_int, vp]),
+    "fclsh_dataset_load": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "fclsh_dataset_info_get": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int32), C.POINTER(u64p)]),
+    "fclsh_dataset_upload": (C.c_int, [vp, vp, C.c_int, vp]),
+    "fclsh_dataset_destroy": (None, [vp]),
+    "fclsh_dataset_save": (C.c_int, [C.c_char_p, u64p, C.c_uint64, C.c_uint64, C.c_int32]),
+    "fclsh_scan_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "fclsh_scan_destroy": (None, [vp]),
+    "fclsh_scan_truth": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, C.c_uint32, vp,
+                                   C.POINTER(DeviceResult)]),
+    "fclsh_distance_histogram": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                           vp, u64p]),
     "fclsh_launch_count": (C.c_uint64, []),
     "fclsh_launch_count_reset": (None, []),
     "fclsh_gen_bernoulli": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]),

@@ -16,7 +16,9 @@
 #include "common.cuh"
 #include "hash.cuh"
 #include "host.hpp"
+#include "dataset.hpp"
 #include "index.cuh"
+#include "scan.hpp"
 
 namespace fclsh_b200 {
 void gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
@@ -83,6 +85,14 @@ struct fclsh_family {
 
 struct fclsh_plan {
     Plan p;
+};
+
+struct fclsh_dataset {
+    HostDataset ds;
+};
+
+struct fclsh_scan {
+    ScanState st;
 };
 
 struct fclsh_index {
@@ -525,6 +535,107 @@ int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* ge
     if (dense) *dense = ix->ix->last_dense;
     if (general) *general = ix->ix->last_overflow;
     return 0;
+}
+
+int fclsh_dataset_load(const char* path, fclsh_dataset** out) {
+    return guarded([&] {
+        need(path, "path");
+        need(out, "out");
+        auto h = std::make_unique<fclsh_dataset>();
+        h->ds = load_dataset(path);
+        *out = h.release();
+    });
+}
+
+int fclsh_dataset_info_get(const fclsh_dataset* ds, uint64_t* n, uint64_t* dims, int32_t* format,
+                           const uint64_t** rows) {
+    return guarded([&] {
+        need(ds, "dataset");
+        if (n) *n = ds->ds.n;
+        if (dims) *dims = ds->ds.dims;
+        if (format) *format = ds->ds.format;
+        if (rows) *rows = ds->ds.rows;
+    });
+}
+
+int fclsh_dataset_upload(const fclsh_dataset* ds, uint64_t* d_rows, int device, void* stream) {
+    return guarded([&] {
+        need(ds, "dataset");
+        const uint64_t bytes = ds->ds.n * ds->ds.words() * 8;
+        if (!bytes) return;
+        need(d_rows, "d_rows");
+        FCLSH_CUDA(cudaSetDevice(device));
+        FCLSH_CUDA(cudaMemcpyAsync(d_rows, ds->ds.rows, bytes, cudaMemcpyHostToDevice,
+                                   static_cast<cudaStream_t>(stream)));
+    });
+}
+
+void fclsh_dataset_destroy(fclsh_dataset* ds) { delete ds; }
+
+int fclsh_dataset_save(const char* path, const uint64_t* rows, uint64_t n, uint64_t dims, int32_t format) {
+    return guarded([&] {
+        need(path, "path");
+        if (n) need(rows, "rows");
+        save_dataset(path, rows, n, dims, format);
+    });
+}
+
+int fclsh_scan_create(int device, fclsh_scan** out) {
+    return guarded([&] {
+        need(out, "out");
+        auto h = std::make_unique<fclsh_scan>();
+        h->st.device = device;
+        *out = h.release();
+    });
+}
+
+void fclsh_scan_destroy(fclsh_scan* sc) { delete sc; }
+
+int fclsh_scan_truth(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const uint64_t* d_q_rows, uint64_t nq,
+                     uint64_t dims, uint32_t radius, void* stream, fclsh_device_result* out) {
+    return guarded([&] {
+        need(sc, "scan");
+        need(out, "out");
+        if (dims == 0) throw UsageError("scan: zero width");
+        if (n) need(d_rows, "d_rows");
+        if (nq) need(d_q_rows, "d_q_rows");
+        ScanArgs a;
+        a.rows = d_rows;
+        a.n = n;
+        a.qrows = d_q_rows;
+        a.nq = nq;
+        a.dims = dims;
+        a.words = uint32_t((dims + 63) / 64);
+        a.radius = radius;
+        const ScanOutput o = scan_truth_device(sc->st, a, static_cast<cudaStream_t>(stream));
+        std::memset(out, 0, sizeof(*out));
+        out->nq = o.nq;
+        out->total = o.total;
+        out->d_query = o.d_query;
+        out->d_id = o.d_id;
+        out->d_distance = o.d_dist;
+        out->d_offsets = o.d_offsets;
+    });
+}
+
+int fclsh_distance_histogram(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const uint64_t* d_q_rows,
+                             uint64_t nq, uint64_t dims, uint64_t sample_per_query, uint64_t seed, void* stream,
+                             uint64_t* counts) {
+    return guarded([&] {
+        need(sc, "scan");
+        need(counts, "counts");
+        if (dims == 0) throw UsageError("histogram: zero width");
+        if (n) need(d_rows, "d_rows");
+        if (nq) need(d_q_rows, "d_q_rows");
+        ScanArgs a;
+        a.rows = d_rows;
+        a.n = n;
+        a.qrows = d_q_rows;
+        a.nq = nq;
+        a.dims = dims;
+        a.words = uint32_t((dims + 63) / 64);
+        distance_histogram_device(sc->st, a, sample_per_query, seed, counts, static_cast<cudaStream_t>(stream));
+    });
 }
 
 uint64_t fclsh_launch_count(void) { return launch_counter(); }

@@ -506,3 +506,97 @@ def gen_planted(seed: int, data: np.ndarray, dims: int, nq: int, kmax: int):
     _check(N.lib().fclsh_gen_planted(seed, _ptr(d, N.u64p), d.shape[0], dims, nq, kmax, _ptr(out, N.u64p),
                                      _ptr(src, N.u32p)))
     return out, src
+
+
+# ----------------------------------------------------------------- datasets
+
+DATASET_FCL1 = 1
+DATASET_TEXT = 2
+
+
+class Dataset:
+    """load_dataset (dataset.cpp:101-111): rows [n, ceil(dims/64)] uint64 in
+    the engine's row layout, held in pinned host memory when a GPU is usable."""
+
+    def __init__(self, handle):
+        self._h = handle
+        n, d, fmt, rows = C.c_uint64(0), C.c_uint64(0), C.c_int32(0), N.u64p()
+        _check(N.lib().fclsh_dataset_info_get(self._h, C.byref(n), C.byref(d), C.byref(fmt), C.byref(rows)))
+        self.n, self.dims, self.format = int(n.value), int(d.value), int(fmt.value)
+        W = words_for(self.dims)
+        if self.n:
+            buf = (C.c_uint64 * (self.n * W)).from_address(C.cast(rows, C.c_void_p).value)
+            buf._owner = self  # the handle outlives every view of its rows
+            self.rows = np.frombuffer(buf, dtype=np.uint64).reshape(self.n, W)
+        else:
+            self.rows = np.zeros((0, W), np.uint64)
+
+    def __del__(self, _free=_release):
+        _free(self, "fclsh_dataset_destroy")
+
+    def __len__(self) -> int:
+        return self.n
+
+    def upload(self, device: int = 0, stream=None):
+        """The rows as a CUDA int64 tensor [n, W] (pinned host -> device copy)."""
+        import torch
+        out = torch.empty((self.n, words_for(self.dims)), dtype=torch.int64, device=f"cuda:{device}")
+        _check(N.lib().fclsh_dataset_upload(self._h, C.c_void_p(out.data_ptr()), device, _stream_ptr(stream)))
+        return out
+
+
+def load_dataset(path: str) -> Dataset:
+    """load_dataset (dataset.hpp:30): FCL1 (magic sniffed) or text."""
+    h = C.c_void_p()
+    _check(N.lib().fclsh_dataset_load(str(path).encode(), C.byref(h)))
+    return Dataset(h)
+
+
+def save_dataset(path: str, rows, dims: int, text: bool = False) -> None:
+    """save_dataset / save_dataset_text (dataset.hpp:22-27) of rows [n, ceil(dims/64)]."""
+    r = _u64(rows)
+    if r.ndim == 1:
+        r = r.reshape(-1, words_for(dims))
+    _check(N.lib().fclsh_dataset_save(str(path).encode(), _ptr(r, N.u64p), r.shape[0], dims,
+                                      DATASET_TEXT if text else DATASET_FCL1))
+
+
+# -------------------------------------------------------------- linear scan
+
+class LinearScan:
+    """scan_truth (workload.cpp:56-71) and distance_histogram
+    (workload.cpp:133-151) on device rows (CUDA int64/uint64 tensors [n, W])."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(N.lib().fclsh_scan_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def __del__(self, _free=_release):
+        _free(self, "fclsh_scan_destroy")
+
+    def scan_truth(self, rows, q_rows, dims: int, radius: int, stream=None) -> DeviceQueryResults:
+        out = N.DeviceResult()
+        _check(N.lib().fclsh_scan_truth(self._h, C.c_void_p(rows.data_ptr()), rows.shape[0],
+                                        C.c_void_p(q_rows.data_ptr()), q_rows.shape[0], dims, radius,
+                                        _stream_ptr(stream), C.byref(out)))
+        return DeviceQueryResults(int(out.nq), int(out.total), out.d_query or 0, out.d_id or 0,
+                                  out.d_distance or 0, out.d_offsets or 0, 0, 0, 0, raw=out)
+
+    def triples(self, rows, q_rows, dims: int, radius: int) -> np.ndarray:
+        """(query, point, distance) uint32 triples ordered by (query, point), on the host."""
+        import torch
+        r = self.scan_truth(rows, q_rows, dims, radius)
+        tri = torch.zeros((3, max(r.total, 1)), dtype=torch.int32, device=f"cuda:{self.device}")
+        r.copy_to(tri, None, None, device=self.device)
+        torch.cuda.synchronize(self.device)
+        return tri[:, :r.total].cpu().numpy().view(np.uint32).T.copy()
+
+    def distance_histogram(self, rows, q_rows, dims: int, sample_per_query: int = 0, seed: int = 0,
+                           stream=None) -> np.ndarray:
+        counts = np.zeros(dims + 1, np.uint64)
+        _check(N.lib().fclsh_distance_histogram(self._h, C.c_void_p(rows.data_ptr()), rows.shape[0],
+                                                C.c_void_p(q_rows.data_ptr()), q_rows.shape[0], dims,
+                                                sample_per_query, seed, _stream_ptr(stream), _ptr(counts, N.u64p)))
+        return counts
