@@ -108,6 +108,11 @@ class Oracle:
             self._ds_save.argtypes = [C.c_char_p, u64p, C.c_uint64, C.c_uint64, C.c_int]
             self._ds_load = f("dataset_load")
             self._ds_load.argtypes = [C.c_char_p, u64p, u64p, C.POINTER(u64p)]
+            self._run_exp = f("run_experiment")
+            self._run_exp.argtypes = [u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, u32p, C.c_uint64, C.c_uint32,
+                                      C.c_char_p, C.c_uint32, C.c_double, C.c_int, C.c_uint32, C.c_uint64,
+                                      C.c_uint32, C.c_int, C.c_uint64, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_char_p)]
             self._hist = f("distance_histogram")
             self._hist.argtypes = [u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p]
         else:
@@ -249,6 +254,22 @@ class Oracle:
         out = np.ctypeslib.as_array(ptr, shape=(max(1, n.value * W),))[: n.value * W].copy().reshape(n.value, W)
         self._free(ptr)
         return out, d.value
+
+    def run_experiment(self, rows, qrows, dims, truth, truth_radius, method, radius, c=1.0, override=None,
+                       seed=0, repeats=1, fresh_seeds=True, prime=(1 << 61) - 1):
+        """run_experiment (bench.cpp:64-158) -> rows [nq, 12] doubles: query_id, radius, collisions,
+        candidates, found, true_near, precision, recall, time_s1_us, time_s2_us, time_s3_us, 0."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        qrows = np.ascontiguousarray(qrows, dtype=np.uint64)
+        truth = np.ascontiguousarray(truth, dtype=np.uint32).reshape(-1, 3)
+        out = np.zeros((qrows.shape[0], 12), np.float64)
+        csv = C.c_char_p()
+        kind, t = (-1, 0) if override is None else override
+        self._check(self._run_exp(_p(rows, u64p), rows.shape[0], _p(qrows, u64p), qrows.shape[0], dims,
+                                  _p(truth, u32p), truth.shape[0], truth_radius, method.encode(), radius, c,
+                                  kind, t, seed, repeats, int(fresh_seeds), prime,
+                                  out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(csv)))
+        return out
 
     def distance_histogram(self, rows, qrows, dims, sample_per_query=0, seed=0):
         """distance_histogram (workload.cpp:133-151): counts[dims + 1]."""

@@ -14,6 +14,7 @@
 //   ref_index_query    -> fclsh::query_r_nn               (index.cpp:157-188)
 //   ref_scan_truth     -> fclsh::scan_truth               (workload.cpp:56-71)
 //   ref_distance_histogram -> fclsh::distance_histogram   (workload.cpp:133-151)
+//   ref_run_experiment -> fclsh::run_experiment + write_metrics (bench.cpp:64-170)
 //   ref_dataset_save / ref_dataset_load -> fclsh::save_dataset[_text] /
 //                         fclsh::load_dataset             (dataset.cpp:82-111)
 //   ref_fht_mod / ref_batch_hash_kernel -> hadamard.cpp:51-72
@@ -28,6 +29,7 @@
 // PostingTable::finalize as build_index, only with the table sorts spread
 // over threads (threads == 1 calls build_index itself).
 
+#include "fclsh/bench.hpp"
 #include "fclsh/bitvec.hpp"
 #include "fclsh/covering.hpp"
 #include "fclsh/dataset.hpp"
@@ -47,6 +49,7 @@
 #include <memory>
 #include <optional>
 #include <span>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -443,6 +446,53 @@ int ref_dataset_load(const char* path, uint64_t* n, uint64_t* dims, uint64_t** r
         *n = ds.size();
         *dims = ds.dims;
         *rows_out = out;
+    });
+}
+
+// run_experiment(data, queries, truth, cfg): one row of 12 doubles per query
+// {query_id, radius, collisions, candidates, found, true_near, precision,
+// recall, s1_us, s2_us, s3_us, 0}; csv_out is unused.
+int ref_run_experiment(const uint64_t* rows, uint64_t n, const uint64_t* qrows, uint64_t nq, uint64_t dims,
+                       const uint32_t* truth, uint64_t ntruth, uint32_t truth_radius, const char* method,
+                       uint32_t radius, double c, int override_kind, uint32_t override_t, uint64_t seed,
+                       uint32_t repeats, int fresh_seeds, uint64_t prime, double* out, char** csv_out) {
+    return guarded([&] {
+        Dataset data = rows_to_dataset(rows, n, dims, 8);
+        Dataset qs = rows_to_dataset(qrows, nq, dims, 8);
+        GroundTruth g;
+        g.radius = truth_radius;
+        for (uint64_t k = 0; k < ntruth; ++k)
+            g.entries.push_back(TruthEntry{truth[3 * k], truth[3 * k + 1], truth[3 * k + 2]});
+        ExperimentConfig cfg;
+        cfg.method = method;
+        cfg.radius = radius;
+        cfg.c = c;
+        if (override_kind >= 0) cfg.plan_override = PlanOverride{static_cast<PlanKind>(override_kind), override_t};
+        cfg.seed = seed;
+        cfg.repeats = repeats;
+        cfg.fresh_seeds = fresh_seeds != 0;
+        cfg.prime = prime;
+        std::vector<MetricsRow> res = run_experiment(data, qs, g, cfg);
+        for (size_t i = 0; i < res.size(); ++i) {
+            const MetricsRow& r = res[i];
+            double* o = out + 12 * i;
+            o[0] = r.query_id;
+            o[1] = r.radius;
+            o[2] = r.collisions;
+            o[3] = r.candidates;
+            o[4] = r.found;
+            o[5] = r.true_near;
+            o[6] = r.precision;
+            o[7] = r.recall;
+            o[8] = r.time_s1_us;
+            o[9] = r.time_s2_us;
+            o[10] = r.time_s3_us;
+            o[11] = 0;
+        }
+        // (write_metrics needs iostreams, which crash when this statically
+        // linked libstdc++ shares a process with another one: the CSV comes
+        // from oracle/_ref/ref_write_metrics instead)
+        (void)csv_out;
     });
 }
 
