@@ -235,6 +235,15 @@ typedef struct {
 int fclsh_query_device(fclsh_index* ix, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
                        void* stream, fclsh_device_result* out);
 
+/* query_c_r_nn (index.hpp:90-93, index.cpp:190-235) for nq host rows:
+ * walk the buckets in table order and stop after posting_budget postings
+ * (< 0: the reference's default 3L), return the closest point retrieved
+ * (ties: the lowest id). counters[nq][3] = {collisions, candidates, found},
+ * best[nq][2] = {id, distance}, both UINT32_MAX when nothing was retrieved.
+ * Budgets above 12288 are rejected (the CTA's shared set). Synchronous. */
+int fclsh_query_c_r_nn(fclsh_index* ix, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
+                       int64_t posting_budget, uint64_t* counters, uint32_t* best);
+
 /* Copies a device result into caller device buffers (all on `device`):
  * d_triples [3][cap] (rows: query, id, distance; cap >= r->total),
  * d_offsets [nq+1], d_counters [3][nq] (rows: collisions, candidates, found).

@@ -108,6 +108,9 @@ class Oracle:
             self._ds_save.argtypes = [C.c_char_p, u64p, C.c_uint64, C.c_uint64, C.c_int]
             self._ds_load = f("dataset_load")
             self._ds_load.argtypes = [C.c_char_p, u64p, u64p, C.POINTER(u64p)]
+            self._index_query_c = f("index_query_c")
+            self._index_query_c.argtypes = [C.c_void_p, u64p, C.c_uint64, C.c_uint32, C.c_int64, C.c_int, u64p,
+                                            u32p]
             self._run_exp = f("run_experiment")
             self._run_exp.argtypes = [u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, u32p, C.c_uint64, C.c_uint32,
                                       C.c_char_p, C.c_uint32, C.c_double, C.c_int, C.c_uint32, C.c_uint64,
@@ -327,6 +330,17 @@ class OracleIndex:
         ids = np.ctypeslib.as_array(ptr, shape=(max(total, 1),))[:total].copy()
         self.o._free(ptr)
         return counters, offsets, ids
+
+    def query_c(self, qrows, radius, budget=None, threads=1):
+        """query_c_r_nn per row (compiled reference only) -> (counters [nq, 3], best [nq, 2] id/distance,
+        UINT32_MAX when nothing was retrieved)."""
+        qrows = np.ascontiguousarray(qrows, dtype=np.uint64)
+        nq = qrows.shape[0]
+        counters = np.zeros((nq, 3), np.uint64)
+        best = np.zeros((nq, 2), np.uint32)
+        self.o._check(self.o._index_query_c(self.h, _p(qrows, u64p), nq, radius, -1 if budget is None else budget,
+                                            threads, _p(counters, u64p), _p(best, u32p)))
+        return counters, best
 
 
 _cache: dict = {}

@@ -12,6 +12,7 @@
 //   ref_make_plan      -> fclsh::make_plan                (transform.cpp:32-113)
 //   ref_index_build    -> fclsh::build_index              (index.cpp:49-119)
 //   ref_index_query    -> fclsh::query_r_nn               (index.cpp:157-188)
+//   ref_index_query_c  -> fclsh::query_c_r_nn             (index.cpp:190-235)
 //   ref_scan_truth     -> fclsh::scan_truth               (workload.cpp:56-71)
 //   ref_distance_histogram -> fclsh::distance_histogram   (workload.cpp:133-151)
 //   ref_run_experiment -> fclsh::run_experiment + write_metrics (bench.cpp:64-170)
@@ -373,6 +374,29 @@ int ref_index_query(void* h, const uint64_t* qrows, uint64_t nq, uint32_t radius
         for (uint64_t q = 0; q < nq; ++q)
             std::copy(res[q].begin(), res[q].end(), ids + offsets[q]);
         *ids_out = ids;
+    });
+}
+
+// query_c_r_nn (index.cpp:190-235) for nq rows: counters[3*q] =
+// {collisions, candidates, found}, best[2*q] = {id, distance} or
+// {UINT32_MAX, UINT32_MAX} when nothing was retrieved. budget < 0: default 3L.
+int ref_index_query_c(void* h, const uint64_t* qrows, uint64_t nq, uint32_t radius, int64_t budget, int threads,
+                      uint64_t* counters, uint32_t* best) {
+    return guarded([&] {
+        auto* idx = static_cast<RefIndex*>(h);
+        Dataset qs = rows_to_dataset(qrows, nq, idx->data.dims, threads);
+        int T = std::max(1, threads);
+        std::vector<QueryScratch> scratch(T);
+        std::optional<uint64_t> b;
+        if (budget >= 0) b = uint64_t(budget);
+        parallel_for(nq, T, [&](uint64_t q, int t) {
+            CrnnResult r = query_c_r_nn(idx->index, qs[q], radius, scratch[t], b);
+            counters[3 * q + 0] = r.report.collisions;
+            counters[3 * q + 1] = r.report.candidates;
+            counters[3 * q + 2] = r.report.found;
+            best[2 * q] = r.id ? *r.id : UINT32_MAX;
+            best[2 * q + 1] = r.id ? r.distance : UINT32_MAX;
+        });
     });
 }
 

@@ -86,6 +86,7 @@ SIGNATURES = {
     "fclsh_index_destroy": (None, [vp]),
     "fclsh_query": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.POINTER(C.POINTER(Result))]),
     "fclsh_result_free": (None, [C.POINTER(Result)]),
+    "fclsh_query_c_r_nn": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.c_int64, u64p, u32p]),
     "fclsh_query_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, C.POINTER(DeviceResult)]),
     "fclsh_query_stage_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int]),
     "fclsh_query_path_counts": (C.c_int, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -442,6 +442,32 @@ void fclsh_result_free(fclsh_result* r) {
     pinned_pool().give(reinterpret_cast<unsigned char*>(r) - kResultHeader);
 }
 
+int fclsh_query_c_r_nn(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
+                       int64_t posting_budget, uint64_t* counters, uint32_t* best) {
+    return guarded([&] {
+        need(ixh, "index");
+        if (nq) {
+            need(q_rows, "q_rows");
+            need(counters, "counters");
+            need(best, "best");
+        }
+        DeviceIndex& ix = *ixh->ix;
+        FCLSH_CUDA(cudaSetDevice(ix.device));
+        const uint64_t W = ix.row_words;
+        uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
+        DevBuf out;
+        auto* dc = static_cast<uint64_t*>(out.ensure(std::max<uint64_t>(1, nq) * 32));
+        auto* db = reinterpret_cast<uint32_t*>(dc + 3 * nq);
+        if (nq) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
+        query_c_device(ix, dq, nq, radius, posting_budget, dc, db, ix.stream);
+        if (nq) {
+            FCLSH_CUDA(cudaMemcpyAsync(counters, dc, nq * 24, cudaMemcpyDeviceToHost, ix.stream));
+            FCLSH_CUDA(cudaMemcpyAsync(best, db, nq * 8, cudaMemcpyDeviceToHost, ix.stream));
+            FCLSH_CUDA(cudaStreamSynchronize(ix.stream));
+        }
+    });
+}
+
 int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius, void* stream,
                        fclsh_device_result* out) {
     return guarded([&] {

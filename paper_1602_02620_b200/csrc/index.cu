@@ -674,6 +674,146 @@ __global__ void __launch_bounds__(512) k_query_dense(
 }
 
 
+struct NarrowIdOrder {
+    __device__ __forceinline__ static bool less(uint32_t a, uint32_t b) { return a < b; }
+};
+
+// ------------------------------------------------------- Strategy 1 query
+
+// query_c_r_nn (index.cpp:190-235), one CTA per query: walk the buckets in
+// table order (part, then table; ids ascending inside a bucket) and stop
+// after `budget` postings, duplicates included; count collisions, distinct
+// candidates, found (<= radius), and keep the closest point retrieved, ties
+// to the lowest id. The walk is order-dependent, so the CTA first counts
+// every table's postings, scans the counts to find the table where the
+// budget runs out, then inserts the ids of the tables before it plus the
+// smallest ids of that table into a shared set, and verifies the set.
+template <typename T, int LAYOUT, int HS, int KCAP>
+__global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict__ qkeys, uint64_t nq,
+                                                 uint32_t tables, const Tables<T> tb,
+                                                 const uint64_t* __restrict__ rows,
+                                                 const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
+                                                 uint64_t budget, unsigned long long* __restrict__ counters,
+                                                 uint32_t* __restrict__ best, unsigned int* __restrict__ qnext,
+                                                 unsigned int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* set = reinterpret_cast<uint32_t*>(smem);        // HS ids
+    uint32_t* kbuf = set + HS;                                // KCAP ids of the table the budget cuts
+    uint32_t* cnt = kbuf + KCAP;                              // tables: postings per table, then their prefix
+    __shared__ unsigned long long wsum[16], best_s;
+    __shared__ unsigned int cand_s, found_s, cut_s, cutr_s, kn_s, next_s, bad_s;
+    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
+    auto fetch = [&]() -> uint32_t {
+        if (tid == 0) next_s = atomicAdd(qnext, 1u);
+        __syncthreads();
+        return next_s;
+    };
+    for (uint64_t q = fetch(); q < nq; q = fetch()) {
+        const typename T::K* qk = qkeys + q * tables;
+        // A: postings per table
+        for (uint32_t t = tid; t < tables; t += nt) cnt[t] = probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), [](uint32_t) {});
+        if (tid == 0) {
+            cand_s = found_s = kn_s = bad_s = 0;
+            best_s = ~0ull;
+            cut_s = tables; // no cut
+            cutr_s = 0;
+        }
+        __syncthreads();
+        // B: exclusive prefix over tables in walk order (contiguous chunk per thread)
+        const uint32_t per = (tables + nt - 1) / nt, b0 = min(tables, tid * per), b1 = min(tables, b0 + per);
+        unsigned long long mine = 0;
+        for (uint32_t t = b0; t < b1; ++t) mine += cnt[t];
+        unsigned long long x = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= uint32_t(o)) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        unsigned long long run = x - mine;
+        for (uint32_t w = 0; w < wid; ++w) run += wsum[w];
+        unsigned long long total = 0;
+        for (uint32_t w = 0; w < (nt >> 5); ++w) total += wsum[w];
+        // the table where the budget runs out: cum < budget < cum + cnt
+        for (uint32_t t = b0; t < b1; ++t) {
+            const uint32_t c = cnt[t];
+            if (run < budget && run + c > budget) {
+                cut_s = t;
+                cutr_s = uint32_t(budget - run);
+            }
+            cnt[t] = uint32_t(run < 0xFFFFFFFFull ? run : 0xFFFFFFFFull); // now the exclusive prefix
+            run += c;
+        }
+        __syncthreads();
+        const uint32_t cut = cut_s, cutr = cutr_s;
+        const unsigned long long coll = total < budget ? total : budget;
+        // C: ids of the tables walked in full, and of the cut table's smallest ids
+        auto insert = [&](uint32_t id) {
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
+            for (;;) {
+                const uint32_t old = atomicCAS(set + h, kEmpty, id);
+                if (old == id) return;
+                if (old == kEmpty) break;
+                h = (h + 1) & (HS - 1);
+            }
+            atomicAdd(&cand_s, 1u);
+        };
+        for (uint32_t t = tid; t < tables; t += nt) {
+            const bool full = t < cut && cnt[t] < budget;
+            if (full) {
+                probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), insert);
+            } else if (t == cut) {
+                probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), [&](uint32_t id) {
+                    const uint32_t p = atomicAdd(&kn_s, 1u);
+                    if (p < KCAP) kbuf[p] = id;
+                    else bad_s = 1;
+                });
+            }
+        }
+        __syncthreads();
+        if (cut < tables) { // the cut table: ascending ids, the first cutr of them
+            const uint32_t m = min(kn_s, uint32_t(KCAP));
+            uint32_t P = 1;
+            while (P < m) P <<= 1;
+            for (uint32_t i = m + tid; i < P; i += nt) kbuf[i] = kEmpty;
+            __syncthreads();
+            bitonic_sort<NarrowIdOrder>(kbuf, P, P);
+            for (uint32_t i = tid; i < cutr && i < m; i += nt) insert(kbuf[i]);
+            __syncthreads();
+        }
+        // D: verify the distinct candidates, closest first (ties: lowest id)
+        const uint64_t* qr = qrows + q * words;
+        uint32_t fnd = 0;
+        unsigned long long bst = ~0ull;
+        for (uint32_t i = tid; i < HS; i += nt) {
+            const uint32_t id = set[i];
+            if (id == kEmpty) continue;
+            set[i] = kEmpty;
+            const uint64_t* r = rows + uint64_t(id) * words;
+            uint32_t d = 0;
+            for (uint32_t w = 0; w < words; ++w) d += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+            if (d <= radius) ++fnd;
+            const unsigned long long key = (static_cast<unsigned long long>(d) << 32) | id;
+            bst = key < bst ? key : bst;
+        }
+        if (fnd) atomicAdd(&found_s, fnd);
+        if (bst != ~0ull) atomicMin(&best_s, bst);
+        __syncthreads();
+        if (tid == 0) {
+            counters[3 * q] = coll;
+            counters[3 * q + 1] = cand_s;
+            counters[3 * q + 2] = found_s;
+            best[2 * q] = best_s == ~0ull ? kEmpty : uint32_t(best_s);
+            best[2 * q + 1] = best_s == ~0ull ? kEmpty : uint32_t(best_s >> 32);
+            if (bad_s) atomicAdd(err, 1u);
+        }
+        __syncthreads();
+    }
+}
+
 // General path for the selected queries qsel[0..ns): per (query, table)
 // counts -> per-query collision totals; scan; gather the ids; CUB segmented
 // sort; verify.
@@ -1276,6 +1416,60 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return ix;
+}
+
+namespace {
+constexpr int kCHS = 16384, kCKCAP = 4096; // set slots and cut-table ids of the budgeted query
+
+template <typename T, int LAYOUT>
+void query_c_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, uint64_t budget,
+                  unsigned long long* counters, uint32_t* best, cudaStream_t s) {
+    using K = typename T::K;
+    const uint64_t T_ = ix.tables;
+    K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
+    auto* ctr = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32)); // [6] hand-out, [7] errors
+    FCLSH_CUDA(cudaMemsetAsync(ctr + 6, 0, 8, s));
+    hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
+    auto kern = k_query_c<T, LAYOUT, kCHS, kCKCAP>;
+    const size_t smem = size_t(kCHS + kCKCAP + T_) * 4;
+    const int per_sm = resident_ctas(kern, 512, smem, ix.device);
+    if (per_sm < 1) throw ResourceError("query_c_r_nn: too many tables for the device kernel");
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(nq, uint64_t(per_sm) * sm_count(ix.device)));
+    kern<<<unsigned(grid), 512, smem, s>>>(qkeys, nq, uint32_t(T_), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
+                                          ix.row_words, radius, budget, counters, best, ctr + 6, ctr + 7);
+    FCLSH_LAUNCHED();
+    unsigned int errs = 0;
+    FCLSH_CUDA(cudaMemcpyAsync(&errs, ctr + 7, 4, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    if (errs) throw ResourceError("query_c_r_nn: a bucket cut by the posting budget holds more than 4096 postings");
+}
+} // namespace
+
+void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, int64_t posting_budget,
+                    uint64_t* d_counters, uint32_t* d_best, cudaStream_t stream) {
+    if (radius > ix.radius) // index.cpp:147-153 (check_query)
+        throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
+                         std::to_string(ix.radius));
+    const uint64_t budget = posting_budget < 0 ? 3 * ix.tables : uint64_t(posting_budget); // index.cpp:201
+    if (budget > uint64_t(kCHS) / 4 * 3)
+        throw UsageError("query_c_r_nn: posting budgets above " + std::to_string(kCHS / 4 * 3) +
+                         " are not supported on the device");
+    if (ix.tables > 16384) throw UsageError("query_c_r_nn: more than 16384 tables");
+    if (nq == 0) return;
+    FCLSH_CUDA(cudaSetDevice(ix.device));
+    cudaStream_t s = stream ? stream : ix.stream;
+    auto* c = reinterpret_cast<unsigned long long*>(d_counters);
+    if (ix.wide) {
+        if (ix.layout == kLayoutBuckets)
+            query_c_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, budget, c, d_best, s);
+        else
+            query_c_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, budget, c, d_best, s);
+    } else {
+        if (ix.layout == kLayoutBuckets)
+            query_c_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, budget, c, d_best, s);
+        else
+            query_c_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, budget, c, d_best, s);
+    }
 }
 
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream) {

@@ -110,4 +110,10 @@ struct QueryOutput {
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                          cudaStream_t stream);
 
+// query_c_r_nn (index.cpp:190-235) for nq device rows: d_counters [nq][3]
+// {collisions, candidates, found}, d_best [nq][2] {id, distance} (all-ones
+// when nothing was retrieved). posting_budget < 0: the default 3L. Synchronous.
+void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, int64_t posting_budget,
+                    uint64_t* d_counters, uint32_t* d_best, cudaStream_t stream);
+
 } // namespace fclsh_b200

@@ -416,6 +416,25 @@ class IndexSet:
             _check(-k)
         return {name: float(buf[i]) for i, name in enumerate(self.STAGES[:k])}
 
+    def query_c_r_nn(self, q_rows, radius: int, posting_budget: int | None = None):
+        """query_c_r_nn (index.cpp:190-235) per row -> (counters [nq, 3] collisions/candidates/found,
+        best_id [nq], best_distance [nq]); -1 where nothing was retrieved."""
+        q = _u64(q_rows)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        nq = q.shape[0]
+        if nq and q.shape[1] != words_for(self.dims):
+            raise UsageError("query width does not match the index")
+        counters = np.zeros((nq, 3), np.uint64)
+        best = np.zeros((nq, 2), np.uint32)
+        _check(N.lib().fclsh_query_c_r_nn(self._h, _ptr(q, N.u64p), nq, radius,
+                                          -1 if posting_budget is None else posting_budget,
+                                          _ptr(counters, N.u64p), _ptr(best, N.u32p)))
+        none = best[:, 0] == 0xFFFFFFFF
+        bid = np.where(none, -1, best[:, 0].astype(np.int64))
+        bd = np.where(none, -1, best[:, 1].astype(np.int64))
+        return counters, bid, bd
+
     def stage_timing(self, enable: bool = True) -> None:
         """Per-stage CUDA events on the next batches (off by default: ~4 us each)."""
         _check(N.lib().fclsh_query_stage_timing(self._h, int(bool(enable))))

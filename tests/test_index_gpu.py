@@ -210,3 +210,30 @@ def test_id_offset_shards_reassemble(oracle):
     for qi in range(80):
         merged.extend(a.ids(qi).tolist() + b.ids(qi).tolist())
     assert merged == full.id.tolist()
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("override,radius,budget", [((0, 1), 4, None), ((2, 2), 8, None), ((0, 1), 5, 7),
+                                                     ((0, 1), 5, 0), ((1, 2), 3, 40)])
+def test_query_c_r_nn_matches_the_reference(layout, override, radius, budget):
+    """Strategy 1 (index.cpp:190-235): budgeted walk in table order, closest
+    point retrieved (ties: lowest id); duplicates make the budget bite."""
+    from oracle import oracle as O
+    if not O.reference_available():
+        pytest.skip("compiled reference unavailable")
+    ref = O.reference()
+    rng = np.random.default_rng(radius * 7 + (budget or 0))
+    d = 128
+    rows = random_rows(rng, 3000, d)
+    rows[10:60] = rows[5]  # a 51-copy cluster: long buckets cut by small budgets
+    q = np.concatenate([rows[5:6], planted_queries(rng, rows, d, 100, radius + 2), random_rows(rng, 5, d)])
+    force = F.PlanOverride(F.PlanKind(override[0]), override[1])
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, force)
+    ix = F.build_index(rows, radius, plan, 22, prime=M31, layout=layout)
+    counters, bid, bd = ix.query_c_r_nn(q, radius, budget)
+    oi = ref.index_build(rows, d, radius, 11, 22, override=override, prime=M31, threads=4)
+    want_c, want_b = oi.query_c(q, radius, budget, threads=4)
+    assert (counters == want_c).all(), np.argwhere((counters != want_c).any(1))[:5].ravel()
+    none = want_b[:, 0] == 0xFFFFFFFF
+    assert (bid[none] == -1).all() and (bd[none] == -1).all()
+    assert (bid[~none] == want_b[~none, 0]).all() and (bd[~none] == want_b[~none, 1]).all()
