@@ -201,7 +201,8 @@ typedef struct {
     uint64_t* collisions;/* [nq] */
     uint64_t* candidates;/* [nq] */
     uint64_t* found;     /* [nq] */
-    double time_hash_ms, time_probe_ms, time_verify_ms; /* S1 / S2 / S3, CUDA events */
+    double time_hash_ms, time_probe_ms, time_verify_ms; /* S1 / S2 / S3, CUDA events; -1 unless
+                                                            fclsh_query_stage_timing is on */
 } fclsh_result;
 
 /* Host rows in, host result out (the library allocates; free with

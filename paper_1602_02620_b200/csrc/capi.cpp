@@ -402,26 +402,53 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         const uint64_t W = ix.row_words;
         uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
         if (nq) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
-        QueryOutput o = query_device(ix, dq, nq, radius, ix.stream);
-        // one pinned block per result: [header | fclsh_result | counters | id | distance | query]
-        const uint64_t qb = (nq + 1) * 8, tb = std::max<uint64_t>(1, o.total) * 4;
-        const size_t bytes = kResultHeader + sizeof(fclsh_result) + 4 * qb + 3 * (tb + 16);
-        auto* blk = static_cast<unsigned char*>(pinned_pool().take(bytes));
-        auto* r = reinterpret_cast<fclsh_result*>(blk + kResultHeader);
-        std::memset(r, 0, sizeof(fclsh_result));
-        unsigned char* p = blk + kResultHeader + ((sizeof(fclsh_result) + 15) & ~size_t(15));
-        r->nq = nq;
-        r->total = o.total;
-        r->offsets = reinterpret_cast<uint64_t*>(p); // device layout: offsets | collisions | candidates | found
-        r->collisions = r->offsets + (nq + 1);
-        r->candidates = r->offsets + 2 * (nq + 1);
-        r->found = r->offsets + 3 * (nq + 1);
-        p += 4 * qb;
-        r->id = reinterpret_cast<uint32_t*>(p);
-        r->distance = reinterpret_cast<uint32_t*>(p + ((tb + 15) & ~uint64_t(15)));
-        r->query = reinterpret_cast<uint32_t*>(p + 2 * ((tb + 15) & ~uint64_t(15)));
+        // one pinned block per result: [header | fclsh_result | counters | id | distance | query].
+        // Sized for a guess of the result count, so the counters can be read
+        // back while the batch runs; a larger total takes a larger block.
+        const uint64_t qb = (nq + 1) * 8;
         cudaStream_t s = ix.stream;
-        FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
+        unsigned char* blk = nullptr;
+        fclsh_result* r = nullptr;
+        uint64_t cap = 0;
+        auto layout = [&](uint64_t ids) {
+            const uint64_t tb = std::max<uint64_t>(1, ids) * 4;
+            const size_t bytes = kResultHeader + sizeof(fclsh_result) + 4 * qb + 3 * (tb + 16);
+            blk = static_cast<unsigned char*>(pinned_pool().take(bytes));
+            r = reinterpret_cast<fclsh_result*>(blk + kResultHeader);
+            std::memset(r, 0, sizeof(fclsh_result));
+            unsigned char* p = blk + kResultHeader + ((sizeof(fclsh_result) + 15) & ~size_t(15));
+            r->nq = nq;
+            r->offsets = reinterpret_cast<uint64_t*>(p); // device layout: offsets | collisions | candidates | found
+            r->collisions = r->offsets + (nq + 1);
+            r->candidates = r->offsets + 2 * (nq + 1);
+            r->found = r->offsets + 3 * (nq + 1);
+            p += 4 * qb;
+            r->id = reinterpret_cast<uint32_t*>(p);
+            r->distance = reinterpret_cast<uint32_t*>(p + ((tb + 15) & ~uint64_t(15)));
+            r->query = reinterpret_cast<uint32_t*>(p + 2 * ((tb + 15) & ~uint64_t(15)));
+            cap = ids;
+        };
+        layout(std::max<uint64_t>(1024, ix.last_total + ix.last_total / 4));
+        QueryOutput o;
+        try {
+            o = query_device(ix, dq, nq, radius, s, [&](const QueryOutput& early) {
+                FCLSH_CUDA(cudaMemcpyAsync(r->offsets, early.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
+            });
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            pinned_pool().give(blk);
+            throw;
+        }
+        if (ix.last_overflow && o.total <= cap) // the general path rewrote the counters after the early copy
+            FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
+        if (o.total > cap) { // more results than the guess: a larger block, the counters again
+            unsigned char* old = blk;
+            layout(o.total);
+            FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
+            stream_spin_wait(s); // the first copy may still target the old block
+            pinned_pool().give(old);
+        }
+        r->total = o.total;
         if (o.total) {
             FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
@@ -429,10 +456,13 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         stream_spin_wait(s);
         for (uint64_t q = 0; q < nq; ++q) // the query column follows from the offsets
             for (uint64_t k = r->offsets[q]; k < r->offsets[q + 1]; ++k) r->query[k] = uint32_t(q);
-        ix.collect_stages();
-        r->time_hash_ms = ix.t_hash_ms;
-        r->time_probe_ms = ix.t_probe_ms;
-        r->time_verify_ms = ix.t_verify_ms;
+        r->time_hash_ms = r->time_probe_ms = r->time_verify_ms = -1; // stage timing off: not measured
+        if (ix.stage_timing) {
+            ix.collect_stages();
+            r->time_hash_ms = ix.t_hash_ms;
+            r->time_probe_ms = ix.t_probe_ms;
+            r->time_verify_ms = ix.t_verify_ms;
+        }
         *out = r;
     });
 }

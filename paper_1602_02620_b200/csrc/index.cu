@@ -1090,7 +1090,8 @@ void wait_published(const unsigned long long* h_pub, unsigned long long seq, cud
 }
 
 template <typename T, int LAYOUT>
-QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s) {
+QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s,
+                       const std::function<void(const QueryOutput&)>& before_wait) {
     using K = typename T::K;
     QueryOutput out;
     out.nq = nq;
@@ -1234,6 +1235,15 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         } else {
             enqueue_common();
             ix.gpending = key;
+        }
+        if (before_wait) {
+            QueryOutput early;
+            early.nq = nq;
+            early.d_offsets = reinterpret_cast<uint64_t*>(res_off);
+            early.d_coll = reinterpret_cast<uint64_t*>(coll_q);
+            early.d_cand = reinterpret_cast<uint64_t*>(cand_q);
+            early.d_found = reinterpret_cast<uint64_t*>(found_q);
+            before_wait(early);
         }
         wait_published(ix.h_pub, ++ix.pub_seq, s);
         hs.total = ix.h_pub[0];
@@ -1472,7 +1482,8 @@ void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t 
     }
 }
 
-QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream) {
+QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
+                         const std::function<void(const QueryOutput&)>& before_wait) {
     if (radius > ix.radius) // index.cpp:147-153
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
@@ -1488,11 +1499,11 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
     }
     QueryOutput o;
     if (ix.wide)
-        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
-                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s);
+        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait)
+                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait);
     else
-        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s)
-                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s);
+        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait)
+                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait);
     if (join) {
         FCLSH_CUDA(cudaEventRecord(ix.ev_out, s));
         FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));

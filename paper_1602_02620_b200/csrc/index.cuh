@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -107,8 +108,11 @@ struct QueryOutput {
 };
 
 // query_r_nn for nq device rows; results in index-owned device buffers.
+// before_wait (optional) runs once the batch is enqueued and before the host
+// waits for its total: the offsets / counters pointers are valid (their
+// values complete in stream order), d_query / d_id / d_dist and total are not.
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
-                         cudaStream_t stream);
+                         cudaStream_t stream, const std::function<void(const QueryOutput&)>& before_wait = {});
 
 // query_c_r_nn (index.cpp:190-235) for nq device rows: d_counters [nq][3]
 // {collisions, candidates, found}, d_best [nq][2] {id, distance} (all-ones
