@@ -1061,13 +1061,14 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
                 uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
-                cudaStream_t s) {
+                uint64_t max_grid, cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
     // persistent grid: the overflow count is only known on the device
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
     if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
+    else grid = std::max<uint64_t>(1, std::min(grid, max_grid)); // sized by the last batch's hand-over
     kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
                                                      d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
                                          src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext);
@@ -1122,6 +1123,10 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* cta_dist = static_cast<uint32_t*>(ix.res_cta_dist.ensure(cta_cap * 4));
     for (auto& e : ix.ev)
         if (!e) FCLSH_CUDA(cudaEventCreate(&e));
+    // CTAs for the hand-over: most batches hand nothing over, and an idle
+    // full grid still costs ~4 us; a batch handing over more than the last
+    // one did still completes (queries are handed out dynamically)
+    const uint64_t dense_grid = std::max<uint64_t>(32, 2 * ix.last_dense);
     // Many tables (cfg4: 1022): CTA per query for every query (measured
     // faster than the warp kernel there, clustered or sharded).
     const bool dense_all = big;
@@ -1183,7 +1188,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
                                 found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, ovf_cnt + 5, s);
+                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, s);
         rec(3);
         scan_found(scan_tmp, scan_bytes);
         rec(4);
@@ -1202,7 +1207,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                               reinterpret_cast<const void*>(uintptr_t(radius)), s, qkeys, coll_q,
                                               cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
                                               ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq,
-                                              reinterpret_cast<const void*>(uintptr_t(timing))};
+                                              reinterpret_cast<const void*>(uintptr_t(timing)),
+                                              reinterpret_cast<const void*>(uintptr_t(dense_grid))};
         if (ix.gexec && key == ix.gkey) {
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
