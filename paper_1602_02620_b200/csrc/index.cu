@@ -82,6 +82,8 @@ struct WideEntry { // 8-byte keys: {key, id}
 };
 
 constexpr int kSlots = 4; // per bucket
+constexpr int kScanTileLog = 10; // queries per tile of the found scan (k_scan_compact): 1024
+constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 #ifndef FCLSH_FUSED_CAP
 #define FCLSH_FUSED_CAP 256
 #endif
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
     unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
     uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
-    unsigned int* __restrict__ qnext) {
+    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum) {
     using E = typename T::E;
     static_assert((WS & (WS - 1)) == 0 && WS >= 128 && WS % 32 == 0, "set size");
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
@@ -532,6 +534,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
             cand_q[q] = nd;
             found_q[q] = nfound;
             src_pos[q] = q * slot_cap;
+            if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
         }
     }
 }
@@ -557,7 +560,8 @@ __global__ void __launch_bounds__(512) k_query_dense(
     unsigned long long* __restrict__ cand_q, unsigned long long* __restrict__ found_q,
     unsigned long long* __restrict__ src_pos, uint64_t src_base, uint32_t* __restrict__ res_id,
     uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
-    uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext) {
+    uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext,
+    unsigned long long* __restrict__ tile_sum) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
     uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
@@ -653,6 +657,7 @@ __global__ void __launch_bounds__(512) k_query_dense(
                 cand_q[q] = cand_s;
                 found_q[q] = nf;
                 src_pos[q] = src_base + base_s;
+                if (nf) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nf);
             }
         }
         __syncthreads();
@@ -940,6 +945,110 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
     }
 }
 
+// The found scan, the offsets, the compaction and the publish in one kernel
+// (replaces a memset + CUB's two scan kernels + k_compact): CTA t owns the
+// 1024 queries of tile t; the query kernels have added each tile's results
+// to tile_sum[t], so the tile's prefix is the sum of the earlier tiles'
+// sums, a block scan gives every query's offset, and one thread per result
+// (its query found by a binary search over the tile's offsets) copies it.
+// The CTA of the last tile knows the total and publishes the batch; kScanSplit
+// CTAs share each tile (each recomputes its scan, one writes the offsets).
+__global__ void __launch_bounds__(1024) k_scan_compact(
+    uint64_t nq, const unsigned long long* __restrict__ found_q, const unsigned long long* __restrict__ tile_sum,
+    unsigned long long* __restrict__ res_off, const unsigned long long* __restrict__ src_pos,
+    const uint32_t* __restrict__ tmp_id, const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len,
+    const uint32_t* __restrict__ cta_id, const uint32_t* __restrict__ cta_dist, uint64_t id_offset,
+    uint32_t* __restrict__ out_q, uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist,
+    unsigned long long* __restrict__ pub, unsigned long long* __restrict__ dseq, const unsigned int* __restrict__ cnts) {
+    constexpr uint32_t TQ = 1u << kScanTileLog;
+    __shared__ unsigned long long off_s[TQ + 1], src_s[TQ], wsum[32];
+    __shared__ unsigned long long prefix_s;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t t = blockIdx.x / kScanSplit, part = blockIdx.x % kScanSplit; // kScanSplit CTAs per tile
+    const uint64_t q0 = uint64_t(t) * TQ;
+    const uint32_t m = uint32_t(nq - q0 < TQ ? nq - q0 : TQ);
+    // prefix of the earlier tiles
+    unsigned long long pre = 0;
+    for (uint32_t i = tid; i < t; i += blockDim.x) pre += tile_sum[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (lane == 0) wsum[wid] = pre;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long p = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) p += wsum[w];
+        prefix_s = p;
+    }
+    __syncthreads();
+    const unsigned long long prefix = prefix_s;
+    // block exclusive scan of this tile's found counts
+    const unsigned long long f = tid < m ? found_q[q0 + tid] : 0ull;
+    if (tid < m) src_s[tid] = src_pos[q0 + tid];
+    unsigned long long x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= uint32_t(o)) x += y;
+    }
+    __syncthreads(); // wsum reuse
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= uint32_t(o)) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const unsigned long long excl = x - f + (wid ? wsum[wid - 1] : 0ull);
+    const unsigned long long tile_total = wsum[(blockDim.x >> 5) - 1];
+    off_s[tid] = excl;
+    if (tid == 0) off_s[TQ] = tile_total;
+    if (part == 0 && tid < m) res_off[q0 + tid] = prefix + excl;
+    const bool last = q0 + TQ >= nq;
+    if (part == 0 && last && tid == 0) {
+        res_off[nq] = prefix + tile_total;
+        if (pub) {
+            const unsigned long long seq = *dseq + 1;
+            *dseq = seq;
+            pub[0] = prefix + tile_total;
+            pub[1] = cnts[0];
+            pub[2] = cnts[1];
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
+        }
+    }
+    __syncthreads();
+    // one thread per result of this CTA's share of the tile
+    for (unsigned long long idx = uint64_t(part) * blockDim.x + tid; idx < tile_total;
+         idx += uint64_t(blockDim.x) * kScanSplit) {
+        uint32_t lo = 0, hi = m; // the query j with off_s[j] <= idx < off_s[j+1] (first such: skips empty ones)
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (off_s[mid] <= idx)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const unsigned long long k = idx - off_s[lo];
+        unsigned long long src = src_s[lo];
+        const uint32_t* ti = tmp_id;
+        const uint32_t* td = tmp_dist;
+        if (src >= tmp_len) {
+            src -= tmp_len;
+            ti = cta_id;
+            td = cta_dist;
+        }
+        const unsigned long long dst = prefix + idx;
+        out_q[dst] = uint32_t(q0 + lo);
+        out_id[dst] = uint32_t(ti[src + k] + id_offset);
+        out_dist[dst] = td[src + k];
+    }
+}
+
 uint32_t bit_length(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
 
 unsigned grid_for(uint64_t work, int device, unsigned threads = 256, unsigned per_sm = 8) {
@@ -1039,7 +1148,8 @@ template <typename T, int LAYOUT, int CAP>
 void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
-                  uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, cudaStream_t s) {
+                  uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, unsigned long long* tile_sum,
+                  cudaStream_t s) {
     auto kern = k_query_fused<T, LAYOUT, CAP, kFusedU>;
     const size_t smem = (8 + size_t(8) * CAP) * 4; // CAP = set slots per warp
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
@@ -1047,7 +1157,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
     kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
                                            ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                           tmp_dist, ovf, ovf_cnt, qnext);
+                                           tmp_dist, ovf, ovf_cnt, qnext, tile_sum);
     FCLSH_LAUNCHED();
 }
 
@@ -1061,7 +1171,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
                 uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
-                uint64_t max_grid, cudaStream_t s) {
+                uint64_t max_grid, unsigned long long* tile_sum, cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
@@ -1071,7 +1181,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     else grid = std::max<uint64_t>(1, std::min(grid, max_grid)); // sized by the last batch's hand-over
     kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
                                                      d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
-                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext);
+                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum);
     FCLSH_LAUNCHED();
 }
 
@@ -1117,6 +1227,9 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // query to hand out in the warp / CTA kernel
     auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32));
     auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
+    // results per tile of 1024 queries, added by the query kernels (k_scan_compact)
+    const uint64_t ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
+    auto* tile_sum = static_cast<unsigned long long*>(ix.tile_sum.ensure(std::max<uint64_t>(1, ntiles) * 8));
     // CTA-kernel result region; queries that do not fit go on to the general path
     const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
     uint32_t* cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(cta_cap * 4));
@@ -1182,17 +1295,20 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
         rec(1);
         FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32, s));
+        FCLSH_CUDA(cudaMemsetAsync(tile_sum, 0, std::max<uint64_t>(1, ntiles) * 8, s));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, s);
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, s);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
                                 found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, s);
+                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, s);
         rec(3);
-        scan_found(scan_tmp, scan_bytes);
-        rec(4);
-        compact(ix.d_pub);
+        rec(4); // (one kernel: scan, offsets, compaction, publish)
+        k_scan_compact<<<unsigned(ntiles * kScanSplit), 1024, 0, s>>>(nq, found_q, tile_sum, res_off, src_pos, tmp_id, tmp_dist,
+                                                         nq * slot_cap, cta_id, cta_dist, ix.id_offset, oq, oi, od,
+                                                         ix.d_pub, d_seq, ovf_cnt);
+        FCLSH_LAUNCHED();
         rec(5);
     };
     struct {
@@ -1208,7 +1324,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                               cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
                                               ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq,
                                               reinterpret_cast<const void*>(uintptr_t(timing)),
-                                              reinterpret_cast<const void*>(uintptr_t(dense_grid))};
+                                              reinterpret_cast<const void*>(uintptr_t(dense_grid)), tile_sum};
         if (ix.gexec && key == ix.gkey) {
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
