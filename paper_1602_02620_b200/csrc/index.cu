@@ -1224,12 +1224,13 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
     // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
-    // query to hand out in the warp / CTA kernel
-    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32));
-    auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
-    // results per tile of 1024 queries, added by the query kernels (k_scan_compact)
+    // query to hand out in the warp / CTA kernel; from byte 32 the results
+    // per tile of 1024 queries, added by the query kernels for
+    // k_scan_compact. One memset clears all of it.
     const uint64_t ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
-    auto* tile_sum = static_cast<unsigned long long*>(ix.tile_sum.ensure(std::max<uint64_t>(1, ntiles) * 8));
+    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32 + std::max<uint64_t>(1, ntiles) * 8));
+    auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
+    auto* tile_sum = reinterpret_cast<unsigned long long*>(ovf_cnt + 8);
     // CTA-kernel result region; queries that do not fit go on to the general path
     const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
     uint32_t* cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(cta_cap * 4));
@@ -1294,8 +1295,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(0);
         hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
         rec(1);
-        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32, s));
-        FCLSH_CUDA(cudaMemsetAsync(tile_sum, 0, std::max<uint64_t>(1, ntiles) * 8, s));
+        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32 + ntiles * 8, s));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
                                           tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, s);
