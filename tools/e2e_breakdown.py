@@ -43,3 +43,15 @@ for _ in range(50):
 med = lambda v: 1e3 * statistics.median(v)  # noqa: E731
 print(f"device batch {statistics.median(dev_t):.3f} ms | C fclsh_query {med(c_t):.3f} ms | "
       f"Python query_r_nn {med(py_t):.3f} ms (medians of 50)")
+
+# the bench's order: a stage-timed pass first, then end-to-end calls
+ix.stage_timing(True)
+for _ in range(3):
+    ix.query_r_nn(pq, cfg.radius)
+ix.stage_timing(False)
+ts = []
+for _ in range(40):
+    t0 = time.perf_counter()
+    r = ix.query_r_nn(pq, cfg.radius)
+    ts.append(1e3 * (time.perf_counter() - t0))
+print("per call ms:", " ".join(f"{t:.2f}" for t in ts))
