@@ -761,6 +761,211 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
     }
 }
 
+// FP64 point-major kernel with a column-pair table. The sketch and the first
+// butterfly stage of a column pair (j, j+1) depend only on the two row bits,
+// so the shared table holds the four outcomes {(0,0), (s0,s0), (s1,-s1),
+// (s0+s1, s0-s1)} per pair, and one 16-byte load replaces two selects per
+// column and the first stage. Layout [part][outcome][pair] (16 B entries):
+// lanes read consecutive pairs, so a quarter-warp's loads hit distinct banks
+// whatever outcome each lane selects. The outcome is bits S, S+1 of the byte
+// offset (S = log2(16 * N/2)); the pair's positions are stored with their low
+// five bits pre-rotated so that rotating the row word moves the bit straight
+// to bit S (S+1).
+// The transpose runs in E/G rounds of G columns through a (G+2)-double padded
+// buffer, half the size of a one-round transpose: after round k lane g holds
+// column k*G + g of every lane's block, so the keys of one store are G
+// consecutive codes.
+// d = LUT(a, b, c) bitwise; 0xE2 = b ? a : c, 0xEA = (a & b) | c
+template <uint32_t LUT, uint32_t B>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "n"(B), "r"(c), "n"(LUT));
+    return d;
+}
+
+// 8-byte global -> shared async copy; src_bytes 0 zero-fills the destination
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, uint32_t src_bytes) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int LOGN>
+__host__ __device__ constexpr int pt_warps() {
+    return LOGN == 11 ? 12 : 8;
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const FastParams p) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = lanes_for(LOGN);
+    constexpr int E = N / G;
+    constexpr int GP = G + 2; // padded transpose row (doubles)
+    constexpr int EG = E / G;
+    constexpr int SPW = 32 / G; // rows per warp
+    constexpr int WARPS = pt_warps<LOGN>();
+    constexpr int NT = 32 * WARPS;
+    constexpr int NP = N / 2; // column pairs per part
+    static_assert(G > 1 && EG >= 1 && E % 2 == 0, "layout");
+    constexpr double kTwo52 = 4503599627370496.0;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int S = LOGN + 3; // outcome bit of the table byte offset
+    double2* tab_s = reinterpret_cast<double2*>(smem);                         // [parts][4][NP]
+    double* xbuf = reinterpret_cast<double*>(tab_s + size_t(p.parts) * NP * 4); // WARPS x 32*GP
+    uint2* pk_s = reinterpret_cast<uint2*>(xbuf + WARPS * 32 * GP);             // [parts][NP]
+    uint64_t* rows_s = reinterpret_cast<uint64_t*>(pk_s + p.parts * NP);        // WARPS x 2 x SPW x row_words
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int slot = lane / G; // row within the warp
+    const int g = lane % G;
+
+    // pair i = (j/2)*G + g of a part is entries 2i, 2i+1 of the direct table
+    for (uint32_t i = tid; i < p.parts * NP; i += NT) {
+        const uint2 e0 = p.fam[2 * i], e1 = p.fam[2 * i + 1];
+        const double s0 = double(e0.y), s1 = double(e1.y);
+        double2* t = tab_s + size_t(i / NP) * 4 * NP + (i % NP);
+        t[0] = make_double2(0.0, 0.0);
+        t[NP] = make_double2(s0, s0);
+        t[2 * NP] = make_double2(s1, -s1);
+        t[3 * NP] = make_double2(s0 + s1, s0 - s1);
+        // (byte offset of the row word) << 5 | rotation: bit (pos mod 32) -> bit S (S+1)
+        pk_s[i] = make_uint2(((e0.x & ~31u) << 2) | ((e0.x - S) & 31u),
+                             ((e1.x & ~31u) << 2) | ((e1.x - S - 1) & 31u));
+    }
+    __syncthreads();
+
+    double* xw = xbuf + warp * 32 * GP; // this warp's transpose region
+    const uint32_t wrow = SPW * p.row_words;
+    uint64_t* rw = rows_s + warp * 2 * wrow; // this warp's rows, double-buffered
+    double* xs = xw + slot * G * GP;         // this row's transpose region
+    double* xs_w = xs + g * GP;              // round write: row g
+    const double* xs_r = xs + g;             // round read: column g
+
+    const uint64_t groups = (p.n + SPW - 1) / SPW;
+    const uint64_t nwarps = uint64_t(gridDim.x) * WARPS;
+    // the next group's rows stream into the other buffer (cp.async) while
+    // this group computes: the row loads' latency is off the critical path
+    auto fetch = [&](uint64_t gr, uint64_t* dst) {
+        const uint64_t base = gr * wrow, lim = p.n * p.row_words;
+        for (uint32_t i = lane; i < wrow; i += 32) {
+            const bool ok = gr < groups && base + i < lim;
+            cp_async8(dst + i, ok ? p.rows + base + i : p.rows, ok ? 8u : 0u);
+        }
+        cp_async_commit();
+    };
+    uint64_t grp = uint64_t(blockIdx.x) * WARPS + warp;
+    fetch(grp, rw);
+    for (uint32_t it = 0; grp < groups; grp += nwarps, ++it) {
+        fetch(grp + nwarps, rw + ((it + 1) & 1) * wrow);
+        cp_async_wait_one();
+        __syncwarp();
+        const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rw + (it & 1) * wrow + slot * p.row_words);
+        const uint64_t p0 = grp * SPW;
+        const uint64_t my_point = p0 + slot;
+
+        for (uint32_t part = 0; part < p.parts; ++part) {
+            const uint2* pk = pk_s + part * NP + g;
+            const uint32_t tb_off = part * NP * 64u + g * 16u; // this lane's first pair, outcome 0
+            const char* rowb = reinterpret_cast<const char*>(myrow);
+            const char* tabb = reinterpret_cast<const char*>(tab_s);
+            double x[E];
+            // sketch + first stage: one table entry per column pair
+#pragma unroll
+            for (int j = 0; j < E; j += 2) {
+                const uint2 pp = pk[(j / 2) * G];
+                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(rowb + (pp.x >> 5));
+                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(rowb + (pp.y >> 5));
+                const uint32_t r0 = __funnelshift_r(w0, w0, pp.x), r1 = __funnelshift_r(w1, w1, pp.y);
+                const uint32_t t = lop3<0xE2, 1u << S>(r0, r1);      // bit S from r0, S+1 from r1
+                const uint32_t off = lop3<0xEA, 3u << S>(t, tb_off); // + outcome (b0 + 2 b1) * NP * 16
+                const double2 v = *reinterpret_cast<const double2*>(tabb + off + (j / 2) * G * 16);
+                x[j] = v.x;
+                x[j + 1] = v.y;
+            }
+            // phase 1, remaining stages
+#pragma unroll
+            for (int h = 2; h < E; h <<= 1) {
+#pragma unroll
+                for (int i = 0; i < E; ++i) {
+                    if ((i & h) == 0) {
+                        const double a = x[i], b = x[i + h];
+                        x[i] = a + b;
+                        x[i + h] = a - b;
+                    }
+                }
+            }
+            // total T: sum of the G block totals (element 0 of each lane)
+            double T = x[0];
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+            const double Tp = T + kTwo52;
+            // transpose, G columns per round: x[k*G + h] <- element h*E + k*G + g
+#pragma unroll
+            for (int k = 0; k < EG; ++k) {
+#pragma unroll
+                for (int j = 0; j < G; j += 2)
+                    *reinterpret_cast<double2*>(xs_w + j) = make_double2(x[k * G + j], x[k * G + j + 1]);
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < G; ++h) x[k * G + h] = xs_r[h * GP];
+                __syncwarp();
+            }
+            // phase 2: all but the last stage, then the last stage emits 2^52 + D
+#pragma unroll
+            for (int k = 0; k < EG; ++k) {
+                double* xl = x + k * G;
+#pragma unroll
+                for (int hs = 1; hs < G / 2; hs <<= 1) {
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        if ((i & hs) == 0) {
+                            const double a = xl[i], b = xl[i + hs];
+                            xl[i] = a + b;
+                            xl[i + hs] = a - b;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < G / 2; ++i) {
+                    const double a = xl[i], b = xl[i + G / 2];
+                    xl[i] = (Tp - a) - b;
+                    xl[i + G / 2] = (Tp - a) + b;
+                }
+            }
+            auto finish = [](double v) -> uint32_t {
+                const uint32_t lo = uint32_t(__double2loint(v)), dh = uint32_t(__double2hiint(v)) & 0xFFFFFu;
+                const uint32_t o = (lo >> 1) + dh;
+                return min(o, o - kP31);
+            };
+            // element (k, h) is code v = h*E + k*G + g: G consecutive keys per store
+            if (my_point < p.n) {
+                if (p.key_bytes == 4) {
+                    uint32_t* out = static_cast<uint32_t*>(p.keys) + my_point * p.key_stride + part * p.L + g - 1;
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + k * G + g != 0) out[h * E + k * G] = finish(x[k * G + h]);
+                } else {
+                    uint64_t* out = static_cast<uint64_t*>(p.keys) + my_point * p.key_stride + part * p.L + g - 1;
+#pragma unroll
+                    for (int h = 0; h < G; ++h)
+#pragma unroll
+                        for (int k = 0; k < EG; ++k)
+                            if (h * E + k * G + g != 0) out[h * E + k * G] = finish(x[k * G + h]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    cp_async_wait_all();
+}
+
 template <int LOGN, bool DIRECT>
 size_t fast_smem_bytes(const DeviceFamilySet& fs) {
     constexpr int G = lanes_for(LOGN);
@@ -781,6 +986,20 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
                                size_t(fs.parts) * fs.part_words * 8;
         // FP64 butterflies for direct families (FCLSH_HASH_INT=1 keeps the two int32 planes)
         static const bool use_int = getenv("FCLSH_HASH_INT") != nullptr;
+        static const bool use_pm = getenv("FCLSH_HASH_F64_PM") != nullptr;
+        constexpr int PW = pt_warps<LOGN>();
+        const size_t smem_pt = size_t(fs.parts) * (1 << LOGN) / 2 * 72 + size_t(PW) * 32 * (G + 2) * 8 +
+                               size_t(PW) * 2 * (32 / G) * fs.row_words * 8;
+        if (DIRECT && !use_int && !use_pm && prm.layout == kLayoutPointMajor && smem_pt <= 227 * 1024) {
+            auto kern = k_hash_f64_pt<LOGN>;
+            const int per_sm = resident_ctas(kern, 32 * PW, smem_pt, fs.device);
+            if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
+            const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
+            const uint64_t grid = std::min<uint64_t>((groups + PW - 1) / PW, uint64_t(per_sm) * sm_count(fs.device));
+            kern<<<unsigned(std::max<uint64_t>(grid, 1)), 32 * PW, smem_pt, stream>>>(prm);
+            FCLSH_LAUNCHED();
+            return;
+        }
         const size_t smem_f64 = size_t(WARPS) * 32 * (E + 2) * 8 + size_t(WARPS) * (32 / G) * fs.row_words * 8 +
                                 size_t(fs.parts) * (1 << LOGN) / 2 * 24;
         if (DIRECT && !use_int && prm.layout == kLayoutPointMajor && smem_f64 <= 227 * 1024) {
