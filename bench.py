@@ -555,10 +555,10 @@ def bench_hash(F, cfg5, dev, args, hbm, peak_src, flush, stream, threads, clocks
         check = str(e)
     return {"metric": "fcLSH hash keys/sec (cfg5: 8M x 1024-bit rows, r=10, L=2047, 32-bit keys)",
             "value": n * L / (avg / 1e3), "unit": "keys/s", "ms_per_step": avg, "points": n, "chunk": chunk,
-            "roofline": {"bound": "hbm", "kernel": "k_hash_f64_pm<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": measured_traffic("k_hash_f64_pm<11")[0],
+            "roofline": {"bound": "hbm", "kernel": "k_hash_f64_pt<11>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "traffic": measured_traffic("k_hash_f64_pt<11")[0],
                          "traffic_unit": "bytes per launch (one 1M-row chunk)",
-                         "traffic_source": measured_traffic("k_hash_f64_pm<11")[1], "peak_source": peak_src,
+                         "traffic_source": measured_traffic("k_hash_f64_pt<11")[1], "peak_source": peak_src,
                          "algorithmic_bytes_per_step": algo_bytes,
                          "algorithmic_bytes_per_launch": chunk * (cfg5.dims / 8 + L * 4)},
             "keys_match_oracle_sample": check}
