@@ -146,13 +146,29 @@ class PinnedPool {
                 cached_ -= cap;
             }
         }
-        if (!p && cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
-            cudaGetLastError();
-            throw ResourceError("query: pinned host memory for the result exhausted");
+        if (!p) {
+            // mapped: the batch kernel writes results straight into the block
+            if (cudaHostAlloc(&p, cap, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                throw ResourceError("query: pinned host memory for the result exhausted");
+            }
+            void* d = nullptr;
+            if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) {
+                cudaGetLastError();
+                d = nullptr;
+            }
+            static_cast<uint64_t*>(p)[2] = reinterpret_cast<uintptr_t>(d);
         }
         static_cast<uint64_t*>(p)[0] = kResultMagic;
         static_cast<uint64_t*>(p)[1] = cap;
         return p;
+    }
+    // device-usable address of a pointer into a block (null: not mapped)
+    template <typename T>
+    static T* device_view(void* blk, T* host) {
+        const uint64_t d = static_cast<uint64_t*>(blk)[2];
+        if (!d) return nullptr;
+        return reinterpret_cast<T*>(d + (reinterpret_cast<unsigned char*>(host) - static_cast<unsigned char*>(blk)));
     }
     void give(void* blk) {
         auto* h = static_cast<uint64_t*>(blk);
@@ -429,33 +445,37 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
             cap = ids;
         };
         layout(std::max<uint64_t>(1024, ix.last_total + ix.last_total / 4));
+        // the batch kernel writes counters and results straight into the block
+        HostDest dest{PinnedPool::device_view(blk, reinterpret_cast<unsigned long long*>(r->offsets)),
+                      PinnedPool::device_view(blk, r->query), PinnedPool::device_view(blk, r->id),
+                      PinnedPool::device_view(blk, r->distance), cap};
         QueryOutput o;
         try {
-            o = query_device(ix, dq, nq, radius, s, [&](const QueryOutput& early) {
-                FCLSH_CUDA(cudaMemcpyAsync(r->offsets, early.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
-            });
+            static const bool no_dest = getenv("FCLSH_NO_HOST_DEST") != nullptr; // A/B: D2H copies instead
+            o = query_device(ix, dq, nq, radius, s, {}, dest.counters && !no_dest ? &dest : nullptr);
         } catch (...) {
             cudaStreamSynchronize(s);
             pinned_pool().give(blk);
             throw;
         }
-        if (ix.last_overflow && o.total <= cap) // the general path rewrote the counters after the early copy
-            FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
-        if (o.total > cap) { // more results than the guess: a larger block, the counters again
-            unsigned char* old = blk;
+        bool copies = false;
+        const bool grew = o.total > cap;
+        if (grew) { // more results than the guess: a larger block
+            pinned_pool().give(blk); // (no copy or kernel targets it any more: the batch was published)
             layout(o.total);
+        }
+        if (!o.host_counters || grew) {
             FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
-            stream_spin_wait(s); // the first copy may still target the old block
-            pinned_pool().give(old);
+            copies = true;
         }
         r->total = o.total;
-        if (o.total) {
+        if (o.total && (!o.host_results || grew)) {
+            FCLSH_CUDA(cudaMemcpyAsync(r->query, o.d_query, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
             FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
+            copies = true;
         }
-        stream_spin_wait(s);
-        for (uint64_t q = 0; q < nq; ++q) // the query column follows from the offsets
-            for (uint64_t k = r->offsets[q]; k < r->offsets[q + 1]; ++k) r->query[k] = uint32_t(q);
+        if (copies) stream_spin_wait(s);
         r->time_hash_ms = r->time_probe_ms = r->time_verify_ms = -1; // stage timing off: not measured
         if (ix.stage_timing) {
             ix.collect_stages();

@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -377,8 +378,11 @@ __global__ void __launch_bounds__(256) k_query_fused(
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
     unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
     uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
-    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum) {
+    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum,
+    const unsigned long long* __restrict__ desc) {
     using E = typename T::E;
+    // host destination of the counters (HostDest, null: device only), written as each query completes
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     static_assert((WS & (WS - 1)) == 0 && WS >= 128 && WS % 32 == 0, "set size");
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     constexpr uint32_t kMaxD = WS / 4 * 3; // distinct ids a query may have here (set load <= 3/4 + 32)
@@ -533,6 +537,11 @@ __global__ void __launch_bounds__(256) k_query_fused(
             coll_q[q] = m;
             cand_q[q] = nd;
             found_q[q] = nfound;
+            if (hc) {
+                hc[(nq + 1) + q] = m;
+                hc[2 * (nq + 1) + q] = nd;
+                hc[3 * (nq + 1) + q] = nfound;
+            }
             src_pos[q] = q * slot_cap;
             if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
         }
@@ -561,9 +570,10 @@ __global__ void __launch_bounds__(512) k_query_dense(
     unsigned long long* __restrict__ src_pos, uint64_t src_base, uint32_t* __restrict__ res_id,
     uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
     uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext,
-    unsigned long long* __restrict__ tile_sum) {
+    unsigned long long* __restrict__ tile_sum, const unsigned long long* __restrict__ desc, uint64_t nq_all) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
     constexpr uint32_t kMaxDistinct = HS / 4 * 3;
     uint16_t* clist = reinterpret_cast<uint16_t*>(set + HS); // set slot of each distinct candidate
@@ -656,6 +666,11 @@ __global__ void __launch_bounds__(512) k_query_dense(
                 coll_q[q] = coll_s;
                 cand_q[q] = cand_s;
                 found_q[q] = nf;
+                if (hc) {
+                    hc[(nq_all + 1) + q] = coll_s;
+                    hc[2 * (nq_all + 1) + q] = cand_s;
+                    hc[3 * (nq_all + 1) + q] = nf;
+                }
                 src_pos[q] = src_base + base_s;
                 if (nf) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nf);
             }
@@ -951,36 +966,75 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
 // to tile_sum[t], so the tile's prefix is the sum of the earlier tiles'
 // sums, a block scan gives every query's offset, and one thread per result
 // (its query found by a binary search over the tile's offsets) copies it.
-// The CTA of the last tile knows the total and publishes the batch; kScanSplit
-// CTAs share each tile (each recomputes its scan, one writes the offsets).
+// kScanSplit CTAs share each tile (each recomputes its scan, one writes the
+// offsets). With a host destination (desc: copied from pinned memory in the
+// batch, beside the hash; reading mapped host memory from every CTA costs
+// ~0.35 ms) the counters and, when they fit, the results go straight into
+// mapped pinned host memory, coalesced, instead of a D2H copy after the
+// kernel; the last CTA to finish publishes the batch (total, overflow counts,
+// sequence number) once every CTA's writes are fenced.
 __global__ void __launch_bounds__(1024) k_scan_compact(
     uint64_t nq, const unsigned long long* __restrict__ found_q, const unsigned long long* __restrict__ tile_sum,
     unsigned long long* __restrict__ res_off, const unsigned long long* __restrict__ src_pos,
     const uint32_t* __restrict__ tmp_id, const uint32_t* __restrict__ tmp_dist, uint64_t tmp_len,
     const uint32_t* __restrict__ cta_id, const uint32_t* __restrict__ cta_dist, uint64_t id_offset,
     uint32_t* __restrict__ out_q, uint32_t* __restrict__ out_id, uint32_t* __restrict__ out_dist,
-    unsigned long long* __restrict__ pub, unsigned long long* __restrict__ dseq, const unsigned int* __restrict__ cnts) {
+    unsigned long long* __restrict__ pub, unsigned long long* __restrict__ dseq, unsigned int* __restrict__ cnts,
+    const unsigned long long* __restrict__ coll_q, const unsigned long long* __restrict__ cand_q,
+    const unsigned long long* __restrict__ desc) {
     constexpr uint32_t TQ = 1u << kScanTileLog;
     __shared__ unsigned long long off_s[TQ + 1], src_s[TQ], wsum[32];
-    __shared__ unsigned long long prefix_s;
+    __shared__ unsigned long long prefix_s, grand_s;
+    __shared__ HostDest hd_s;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t t = blockIdx.x / kScanSplit, part = blockIdx.x % kScanSplit; // kScanSplit CTAs per tile
     const uint64_t q0 = uint64_t(t) * TQ;
     const uint32_t m = uint32_t(nq - q0 < TQ ? nq - q0 : TQ);
-    // prefix of the earlier tiles
-    unsigned long long pre = 0;
-    for (uint32_t i = tid; i < t; i += blockDim.x) pre += tile_sum[i];
+    const uint32_t ntiles = gridDim.x / kScanSplit;
+    if (tid == 0) { // the host destination (null counters: device buffers only)
+        const unsigned long long* h = desc;
+        hd_s.counters = h ? reinterpret_cast<unsigned long long*>(h[0]) : nullptr;
+        hd_s.q = h ? reinterpret_cast<uint32_t*>(h[1]) : nullptr;
+        hd_s.id = h ? reinterpret_cast<uint32_t*>(h[2]) : nullptr;
+        hd_s.dist = h ? reinterpret_cast<uint32_t*>(h[3]) : nullptr;
+        hd_s.cap = h ? h[4] : 0;
+    }
+    // prefix of the earlier tiles, and the batch total
+    unsigned long long pre = 0, all = 0;
+    for (uint32_t i = tid; i < ntiles; i += blockDim.x) {
+        const unsigned long long v = tile_sum[i];
+        all += v;
+        if (i < t) pre += v;
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    if (lane == 0) wsum[wid] = pre;
+    for (int o = 16; o > 0; o >>= 1) {
+        pre += __shfl_xor_sync(0xffffffffu, pre, o);
+        all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) {
+        wsum[wid] = pre;
+        off_s[wid] = all; // (scratch: off_s is filled below)
+    }
     __syncthreads();
     if (tid == 0) {
-        unsigned long long p = 0;
-        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) p += wsum[w];
+        unsigned long long p = 0, a = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+            p += wsum[w];
+            a += off_s[w];
+        }
         prefix_s = p;
+        grand_s = a;
     }
     __syncthreads();
     const unsigned long long prefix = prefix_s;
+    const HostDest hd = hd_s;
+    const bool host_cnt = hd.counters != nullptr;
+    const bool host_res = host_cnt && grand_s <= hd.cap;
+    if (host_res) { // results into the host block
+        out_q = hd.q;
+        out_id = hd.id;
+        out_dist = hd.dist;
+    }
     // block exclusive scan of this tile's found counts
     const unsigned long long f = tid < m ? found_q[q0 + tid] : 0ull;
     if (tid < m) src_s[tid] = src_pos[q0 + tid];
@@ -1008,10 +1062,14 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     off_s[tid] = excl;
     if (tid == 0) off_s[TQ] = tile_total;
     if (part == 0 && tid < m) res_off[q0 + tid] = prefix + excl;
+    // (the query kernels wrote the other counters to the host as each query completed)
+    if (host_cnt && tid < m && tid / (TQ / kScanSplit) == part) hd.counters[q0 + tid] = prefix + excl;
     const bool last = q0 + TQ >= nq;
     if (part == 0 && last && tid == 0) {
         res_off[nq] = prefix + tile_total;
-        if (pub) {
+        if (host_cnt) {
+            hd.counters[nq] = prefix + tile_total;
+        } else if (pub) { // device outputs: the caller's copies follow the kernel in stream order, publish now
             const unsigned long long seq = *dseq + 1;
             *dseq = seq;
             pub[0] = prefix + tile_total;
@@ -1046,6 +1104,26 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         out_q[dst] = uint32_t(q0 + lo);
         out_id[dst] = uint32_t(ti[src + k] + id_offset);
         out_dist[dst] = td[src + k];
+    }
+    if (!pub || !host_cnt) return;
+    // host outputs: publish once every CTA's writes are visible: the
+    // barrier orders the CTA's writes before thread 0's system fence
+    // (cumulative), which orders them before its count (one fence per CTA:
+    // a fence per thread serialises in the memory system, ~0.3 ms per batch)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence_system();
+        const unsigned int done = atomicAdd(cnts + 8, 1u);
+        if (done + 1 == gridDim.x) {
+            __threadfence_system();
+            const unsigned long long seq = *dseq + 1;
+            *dseq = seq;
+            pub[0] = grand_s;
+            pub[1] = reinterpret_cast<volatile unsigned int*>(cnts)[0];
+            pub[2] = reinterpret_cast<volatile unsigned int*>(cnts)[1];
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
+        }
     }
 }
 
@@ -1149,7 +1227,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, unsigned long long* tile_sum,
-                  cudaStream_t s) {
+                  const unsigned long long* desc, cudaStream_t s) {
     auto kern = k_query_fused<T, LAYOUT, CAP, kFusedU>;
     const size_t smem = (8 + size_t(8) * CAP) * 4; // CAP = set slots per warp
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
@@ -1157,7 +1235,7 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
     kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
                                            ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                           tmp_dist, ovf, ovf_cnt, qnext, tile_sum);
+                                           tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc);
     FCLSH_LAUNCHED();
 }
 
@@ -1171,7 +1249,8 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
                 uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
-                uint64_t max_grid, unsigned long long* tile_sum, cudaStream_t s) {
+                uint64_t max_grid, unsigned long long* tile_sum, const unsigned long long* desc, uint64_t nq_all,
+                cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
@@ -1181,7 +1260,8 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     else grid = std::max<uint64_t>(1, std::min(grid, max_grid)); // sized by the last batch's hand-over
     kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
                                                      d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
-                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum);
+                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum,
+                                         desc, nq_all);
     FCLSH_LAUNCHED();
 }
 
@@ -1202,7 +1282,7 @@ void wait_published(const unsigned long long* h_pub, unsigned long long seq, cud
 
 template <typename T, int LAYOUT>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s,
-                       const std::function<void(const QueryOutput&)>& before_wait) {
+                       const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest) {
     using K = typename T::K;
     QueryOutput out;
     out.nq = nq;
@@ -1224,13 +1304,13 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     uint32_t* ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
     // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
-    // query to hand out in the warp / CTA kernel; from byte 32 the results
-    // per tile of 1024 queries, added by the query kernels for
-    // k_scan_compact. One memset clears all of it.
+    // query to hand out in the warp / CTA kernel, [8]: k_scan_compact CTAs
+    // done; from byte 64 the results per tile of 1024 queries, added by the
+    // query kernels for k_scan_compact. One memset clears all of it.
     const uint64_t ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
-    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32 + std::max<uint64_t>(1, ntiles) * 8));
+    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(64 + std::max<uint64_t>(1, ntiles) * 8));
     auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
-    auto* tile_sum = reinterpret_cast<unsigned long long*>(ovf_cnt + 8);
+    auto* tile_sum = reinterpret_cast<unsigned long long*>(ovf_cnt + 16);
     // CTA-kernel result region; queries that do not fit go on to the general path
     const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
     uint32_t* cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(cta_cap * 4));
@@ -1254,10 +1334,14 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, found_q, res_off, nq + 1, s));
     void* scan_tmp = ix.cub_tmp.ensure(scan_bytes);
     if (!ix.h_pub) {
-        FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 64, cudaHostAllocMapped));
+        // [0] total, [1] [2] overflow counts, [3] sequence, [4..8] HostDest
+        FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 128, cudaHostAllocMapped));
         FCLSH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ix.d_pub), ix.h_pub, 0));
-        ix.h_pub[3] = 0;
-        FCLSH_CUDA(cudaMemset(ix.pub_seq_dev.ensure(8), 0, 8));
+        std::memset(ix.h_pub, 0, 128);
+        FCLSH_CUDA(cudaMemset(ix.pub_seq_dev.ensure(64), 0, 64)); // [0] sequence, [1..5] HostDest
+        FCLSH_CUDA(cudaStreamCreateWithFlags(&ix.side, cudaStreamNonBlocking));
+        FCLSH_CUDA(cudaEventCreateWithFlags(&ix.ev_fork, cudaEventDisableTiming));
+        FCLSH_CUDA(cudaEventCreateWithFlags(&ix.ev_join, cudaEventDisableTiming));
         ix.pub_seq = 0;
     }
     auto* d_seq = ix.pub_seq_dev.as<unsigned long long>();
@@ -1291,23 +1375,31 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             fprintf(stderr, "[fclsh] query nq=%llu stage %d reached\n", (unsigned long long)nq, k);
         }
     };
+    const unsigned long long* d_desc = d_seq + 1;
     auto enqueue_common = [&] {
         rec(0);
+        // the destination descriptor, copied at run time from pinned memory on a side branch
+        FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
+        FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
+        FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
+                                   ix.side));
+        FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
         rec(1);
-        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 32 + ntiles * 8, s));
+        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 64 + ntiles * 8, s));
+        FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0)); // (the copy ran beside the hash)
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, s);
+                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, d_desc, s);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
                                 found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, s);
+                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, d_desc, nq, s);
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
         k_scan_compact<<<unsigned(ntiles * kScanSplit), 1024, 0, s>>>(nq, found_q, tile_sum, res_off, src_pos, tmp_id, tmp_dist,
                                                          nq * slot_cap, cta_id, cta_dist, ix.id_offset, oq, oi, od,
-                                                         ix.d_pub, d_seq, ovf_cnt);
+                                                         ix.d_pub, d_seq, ovf_cnt, coll_q, cand_q, d_desc);
         FCLSH_LAUNCHED();
         rec(5);
     };
@@ -1315,6 +1407,18 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         unsigned long long total;
         unsigned int cnt[2];
     } hs{0, {0, 0}};
+    // the host destination for this batch (read by k_scan_compact at run time,
+    // so a replayed graph serves any destination)
+    const bool host_cnt = nq && dest && dest->counters;
+    {
+        volatile unsigned long long* h = ix.h_pub + 4;
+        h[0] = host_cnt ? reinterpret_cast<uintptr_t>(dest->counters) : 0;
+        h[1] = host_cnt ? reinterpret_cast<uintptr_t>(dest->q) : 0;
+        h[2] = host_cnt ? reinterpret_cast<uintptr_t>(dest->id) : 0;
+        h[3] = host_cnt ? reinterpret_cast<uintptr_t>(dest->dist) : 0;
+        h[4] = host_cnt ? dest->cap : 0;
+        std::atomic_thread_fence(std::memory_order_release);
+    }
     if (nq) {
         // A shape seen twice in a row (same rows pointer, batch size, radius,
         // stream and workspace) is captured once into a CUDA graph and
@@ -1435,6 +1539,9 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     out.d_coll = reinterpret_cast<uint64_t*>(coll_q);
     out.d_cand = reinterpret_cast<uint64_t*>(cand_q);
     out.d_found = reinterpret_cast<uint64_t*>(found_q);
+    // the general path rewrote counters and results in device memory
+    out.host_counters = host_cnt && !ns;
+    out.host_results = out.host_counters && total <= dest->cap;
     ix.last_total = total;
     ix.last_dense = dense_all ? nq : hs.cnt[0];
     ix.last_overflow = ns;
@@ -1447,6 +1554,9 @@ DeviceIndex::~DeviceIndex() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (h_pub) cudaFreeHost(h_pub);
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
@@ -1605,7 +1715,7 @@ void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t 
 }
 
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
-                         const std::function<void(const QueryOutput&)>& before_wait) {
+                         const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest) {
     if (radius > ix.radius) // index.cpp:147-153
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
@@ -1621,11 +1731,11 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
     }
     QueryOutput o;
     if (ix.wide)
-        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait)
-                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait);
+        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest)
+                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest);
     else
-        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait)
-                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait);
+        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest)
+                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest);
     if (join) {
         FCLSH_CUDA(cudaEventRecord(ix.ev_out, s));
         FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));

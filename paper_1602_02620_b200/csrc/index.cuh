@@ -62,6 +62,9 @@ struct DeviceIndex {
     std::vector<const void*> gkey, gpending;
     uint64_t gkernels = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr; // caller-stream fork / join
+    // side branch of a batch: the HostDest descriptor's H2D copy (beside the hash)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     uint64_t last_total = 0;
     uint64_t last_dense = 0;    // queries the CTA-per-query kernel served
     uint64_t last_overflow = 0; // queries that took the general path
@@ -105,6 +108,22 @@ struct QueryOutput {
     uint64_t nq = 0, total = 0;
     uint32_t *d_query = nullptr, *d_id = nullptr, *d_dist = nullptr;
     uint64_t *d_offsets = nullptr, *d_coll = nullptr, *d_cand = nullptr, *d_found = nullptr;
+    // host_counters: the batch kernel wrote [offsets | collisions | candidates
+    // | found] into HostDest::counters; host_results: also query / id /
+    // distance into the HostDest arrays (total <= cap). Otherwise those are
+    // in the device buffers above.
+    bool host_counters = false, host_results = false;
+};
+
+// Mapped pinned host destination (device-usable pointers) that the batch's
+// compaction kernel writes directly, overlapping the transfer with its own
+// work: counters = 4 x (nq + 1) words, q / id / distance = cap entries each.
+struct HostDest {
+    unsigned long long* counters;
+    uint32_t* q;
+    uint32_t* id;
+    uint32_t* dist;
+    unsigned long long cap;
 };
 
 // query_r_nn for nq device rows; results in index-owned device buffers.
@@ -112,7 +131,8 @@ struct QueryOutput {
 // waits for its total: the offsets / counters pointers are valid (their
 // values complete in stream order), d_query / d_id / d_dist and total are not.
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
-                         cudaStream_t stream, const std::function<void(const QueryOutput&)>& before_wait = {});
+                         cudaStream_t stream, const std::function<void(const QueryOutput&)>& before_wait = {},
+                         const HostDest* dest = nullptr);
 
 // query_c_r_nn (index.cpp:190-235) for nq device rows: d_counters [nq][3]
 // {collisions, candidates, found}, d_best [nq][2] {id, distance} (all-ones
