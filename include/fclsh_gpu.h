@@ -207,9 +207,10 @@ typedef struct {
 
 /* Host rows in, host result out (the library allocates; free with
  * fclsh_result_free). Synchronous. q_rows may be pinned (page-locked) host
- * memory for a full-speed upload. The result is one pinned block (its
- * arrays are slices of it) taken from a pool that fclsh_result_free refills,
- * so the download runs at full speed without a staging copy. */
+ * memory for a full-speed upload. The result is one mapped pinned block (its
+ * arrays are slices of it) taken from a pool that fclsh_result_free refills;
+ * the batch's kernels write the counters and results into it directly, as
+ * they complete (D2H copies only when the total outgrows the block). */
 int fclsh_query(fclsh_index* ix, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
                 fclsh_result** out);
 void fclsh_result_free(fclsh_result* r);
