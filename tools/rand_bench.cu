@@ -141,6 +141,19 @@ int main() {
         run<32, 8, 1>(buf, bytes, sink, sms, kb);
         run<32, 8, 4>(buf, bytes, sink, sms, kb);
     }
+    // L2 fetch granularity (cudaLimitMaxL2FetchGranularity, bytes the L2 fetches per miss)
+    size_t gran = 0;
+    cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity);
+    printf("default L2 fetch granularity: %zu B\n", gran);
+    for (size_t g : {32, 64}) {
+        cudaError_t le = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g);
+        cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity);
+        printf("set %zu -> %s, now %zu B\n", g, cudaGetErrorString(le), gran);
+        run<32, 8, 1>(buf, bytes, sink, sms);
+        run<32, 8, 4>(buf, bytes, sink, sms);
+        run<32, 16, 1>(buf, bytes, sink, sms);
+        run<64, 4>(buf, bytes, sink, sms);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     printf("%s\n", cudaGetErrorString(e));
     return e != cudaSuccess;
