@@ -360,6 +360,23 @@ __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ d
 
 // ----------------------------------------------------------------- query
 
+// the run of bucketed table t from bucket b on (b, b+1, ... until a bucket
+// with a free last slot): push every id whose key matches
+template <typename T, typename F>
+__device__ __forceinline__ void probe_run(const Tables<T>& tb, uint32_t t, uint64_t b, typename T::K key, F&& push) {
+    using E = typename T::E;
+    const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
+    for (;;) {
+        E x[kSlots];
+        load_bucket(base + b * kSlots, x);
+#pragma unroll
+        for (int j = 0; j < kSlots; ++j)
+            if (!T::empty(x[j]) && T::key(x[j]) == key) push(T::id(x[j]));
+        if (T::empty(x[kSlots - 1])) break;
+        b = (b + 1) & (tb.nbuckets - 1);
+    }
+}
+
 // K3+K4+K5 fused, one warp per query (the common path). Lanes probe tables
 // lane, lane+32, ... (U in flight); every colliding id goes into a per-warp
 // shared-memory open-addressing set of WS slots, so only distinct candidates
@@ -458,19 +475,8 @@ __global__ void __launch_bounds__(256) k_query_fused(
 #pragma unroll
                     for (int j = 0; j < kSlots; ++j)
                         if (!T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u]) push(T::id(sl[u][j]));
-                    if (!T::empty(sl[u][kSlots - 1])) { // run continues (rare)
-                        uint64_t b = key[u] >> tb.shift;
-                        const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
-                        for (;;) {
-                            b = (b + 1) & (tb.nbuckets - 1);
-                            E x[kSlots];
-                            load_bucket(base + b * kSlots, x);
-#pragma unroll
-                            for (int j = 0; j < kSlots; ++j)
-                                if (!T::empty(x[j]) && T::key(x[j]) == key[u]) push(T::id(x[j]));
-                            if (T::empty(x[kSlots - 1])) break;
-                        }
-                    }
+                    if (!T::empty(sl[u][kSlots - 1])) // the run continues into the next bucket (~3 %)
+                        probe_run<T>(tb, t, ((key[u] >> tb.shift) + 1) & (tb.nbuckets - 1), key[u], push);
                 }
             }
             __syncwarp();
@@ -1600,23 +1606,31 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     const uint32_t kbits = bit_length(opt.prime - 1);
     const uint64_t W = ix->row_words;
     const uint64_t eb = ix->entry_bytes();
-    // bucket table: 2^bb >= n/2 buckets of 4 slots (load <= 50%), home = key >> (kbits - bb)
+    // bucket table: 2^bb buckets of 4 slots, home = key >> (kbits - bb).
+    // Preferred: 2^bb >= n (slot load <= 25%): a probe then needs the next
+    // bucket (its home bucket full) ~3 % of the time instead of ~18 % at
+    // 2^bb >= n/2 (load <= 50%), and each such continuation is a dependent
+    // random read (cfg2: fused probe kernel 190 -> 168 us, 8.6 -> 17.2 GB).
+    // The sparser table is taken when it fits in half the free memory.
     uint32_t bb = bit_length(std::max<uint64_t>(2, (n + 1) / 2) - 1);
     if (bb < 1) bb = 1;
-    const bool bkt_ok = bb <= kbits && (uint64_t(kSlots) << bb) > n;
-    const uint64_t bkt_bytes = ix->tables * (uint64_t(1) << bb) * kSlots * eb;
+    auto bkt_fits = [&](uint32_t bits) { return bits <= kbits && (uint64_t(kSlots) << bits) > n; };
+    auto bkt_size = [&](uint32_t bits) { return ix->tables * (uint64_t(1) << bits) * kSlots * eb; };
     // CSR directory: 2^b cells, about two postings per cell
     uint32_t b = opt.directory_bits > 0 ? uint32_t(opt.directory_bits)
                                         : std::max<uint32_t>(1, bit_length(n - 1) > 1 ? bit_length(n - 1) - 1 : 1);
     b = std::min<uint32_t>({b, kbits, 30u});
     const uint64_t csr_bytes = ix->tables * (n * eb + ((uint64_t(1) << b) + 1) * 4);
     int layout = opt.layout;
-    if (layout == kLayoutAuto) {
+    {
         size_t free_b = 0, total_b = 0;
         FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
         const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * (ix->wide ? 8 : 4) + (uint64_t(2) << 30);
-        layout = (bkt_ok && bkt_bytes + need_extra <= free_b) ? kLayoutBuckets : kLayoutCsr;
+        if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) ++bb;
+        if (layout == kLayoutAuto)
+            layout = (bkt_fits(bb) && bkt_size(bb) + need_extra <= free_b) ? kLayoutBuckets : kLayoutCsr;
     }
+    const bool bkt_ok = bkt_fits(bb);
     if (layout == kLayoutBuckets && !bkt_ok)
         throw UsageError("index: bucket layout needs a key field wider than the bucket count");
     ix->layout = layout;
@@ -1632,7 +1646,7 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     try {
         ix->rows.ensure(n * W * 8);
         if (layout == kLayoutBuckets) {
-            ix->entries.ensure(bkt_bytes);
+            ix->entries.ensure(bkt_size(bb));
         } else {
             ix->entries.ensure(ix->tables * n * eb);
             ix->dir.ensure(ix->tables * (ix->cells() + 1) * 4);
