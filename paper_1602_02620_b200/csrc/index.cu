@@ -176,19 +176,46 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
 
 // ----------------------------------------------------------------- build
 
-// keys are point-major for one part: key of (row i, table t) at keys[i*L + t]
+// point-major keys [n][L] -> table-major [L][n] through 32 x 32 shared tiles
+// (both sides 128-byte coalesced), so the inserts of a few tables read their
+// keys contiguously instead of a 4-byte word out of every row's sector
+template <typename K>
+__global__ void __launch_bounds__(256) k_keys_table_major(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+                                                          uint32_t L) {
+    __shared__ K tile[32][33];
+    const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const uint64_t tiles_t = (L + 31) / 32, tiles = tiles_t * ((n + 31) / 32);
+    for (uint64_t tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
+        const uint32_t t0 = uint32_t(tl % tiles_t) * 32;
+        const uint64_t i0 = (tl / tiles_t) * 32;
+        for (uint32_t r = ty; r < 32; r += 8) {
+            const uint64_t i = i0 + r;
+            const uint32_t t = t0 + tx;
+            if (i < n && t < L) tile[r][tx] = in[i * L + t];
+        }
+        __syncthreads();
+        for (uint32_t r = ty; r < 32; r += 8) {
+            const uint32_t t = t0 + r;
+            const uint64_t i = i0 + tx;
+            if (i < n && t < L) out[uint64_t(t) * n + i] = tile[tx][r];
+        }
+        __syncthreads();
+    }
+}
+
+// keys are table-major for one part: key of (row i, table t) at keys[t*n + i]
 template <typename T>
-__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0,
-                                uint32_t tg, uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets) {
+__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t t0, uint32_t tg,
+                                uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets) {
     // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
     // their postings are inserted (all 511 at once thrash it: 43 GB of DRAM
-    // reads for 8.6 GB of tables); keys are read tg at a time per row
+    // reads for 8.6 GB of tables)
     const uint64_t total = n * tg;
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t i = x / tg;
-        const uint32_t t = t0 + uint32_t(x % tg);
+        const uint32_t t = t0 + uint32_t(x / n);
+        const uint64_t i = x % n;
         typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
-        const uint64_t key = keys[i * L + t];
+        const uint64_t key = keys[uint64_t(t) * n + i];
         const typename T::E e = T::make(key, uint32_t(i));
         uint64_t b = key >> shift;
         for (;;) {
@@ -1197,7 +1224,7 @@ void build_all(DeviceIndex& ix) {
     const uint64_t n = ix.n, L = ix.fs->tables;
     const uint32_t kb = sizeof(K);
     cudaStream_t s = ix.stream;
-    DevBuf keys, cnt, cur, big, bigc;
+    DevBuf keys, keys_tm, cnt, cur, big, bigc;
     keys.ensure(L * n * kb);
     if (ix.layout == kLayoutBuckets)
         FCLSH_CUDA(cudaMemsetAsync(ix.entries.p, T::empty_byte(), ix.entries.bytes, s));
@@ -1209,13 +1236,18 @@ void build_all(DeviceIndex& ix) {
         hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, L, kLayoutPointMajor, s, p, 1);
         if (ix.layout == kLayoutBuckets) {
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
-            // table groups of ~64 MB of buckets (half the L2)
+            // keys table-major, then table groups of ~64 MB of buckets (half the L2)
+            K* ktm = static_cast<K*>(keys_tm.ensure(L * n * kb));
+            k_keys_table_major<K><<<unsigned(std::min<uint64_t>(((L + 31) / 32) * ((n + 31) / 32),
+                                                                 uint64_t(sm_count(ix.device)) * 8)),
+                                    256, 0, s>>>(static_cast<const K*>(keys.p), ktm, n, uint32_t(L));
+            FCLSH_LAUNCHED();
             const uint64_t tbytes = ix.nbuckets * kSlots * sizeof(typename T::E);
             const uint32_t tg = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (uint64_t(64) << 20) / tbytes)));
             for (uint32_t t0 = 0; t0 < L; t0 += tg) {
                 const uint32_t c = uint32_t(std::min<uint64_t>(tg, L - t0));
-                k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(
-                    static_cast<const K*>(keys.p), n, uint32_t(L), t0, c, ix.key_shift, ix.nbuckets, bk);
+                k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(ktm, n, t0, c, ix.key_shift,
+                                                                                      ix.nbuckets, bk);
                 FCLSH_LAUNCHED();
             }
         } else {
