@@ -271,12 +271,13 @@ int fclsh_merge_shards(uint32_t world, uint64_t nq, const uint64_t* d_offsets, c
  * written (negative on error). */
 int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n);
 
-/* Per-stage timing (the events of fclsh_query_stage_ms [0]..[4], and the
- * time_*_ms fields of fclsh_result) is off by default: each stage event
- * costs ~4 us of device time in a replayed batch. Off, those values are -1
- * and only [5] and the batch total are measured. */
+/* Per-stage timing (the events of fclsh_query_stage_ms, the batch total of
+ * fclsh_query_batch_ms and the time_*_ms fields of fclsh_result) is off by
+ * default: each event costs ~4 us of device time in a replayed batch. Off,
+ * those values are -1. */
 int fclsh_query_stage_timing(fclsh_index* ix, int enable);
-/* Device time (ms) of the last query batch on ix, hash to compaction. */
+/* Device time (ms) of the last query batch on ix, hash to compaction (-1
+ * unless stage timing was on for it). */
 int fclsh_query_batch_ms(const fclsh_index* ix, double* ms);
 
 /* How the last query on ix was served: *dense = queries handed from the

@@ -1404,8 +1404,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     static const bool debug_sync = getenv("FCLSH_DEBUG_SYNC") != nullptr;
     const bool timing = ix.stage_timing;
     auto rec = [&](int k) { // stage events; inside a capture they must be external record nodes
-        // (each costs ~4 us in a replayed graph: only the batch bounds unless stage timing is on)
-        if (!timing && k != 0 && k != 5) return;
+        // (each costs ~4 us in a replayed graph: none unless stage timing is on)
+        if (!timing) return;
         FCLSH_CUDA(capturing ? cudaEventRecordWithFlags(ix.ev[k], s, cudaEventRecordExternal)
                              : cudaEventRecord(ix.ev[k], s));
         if (debug_sync && !capturing) {
@@ -1416,16 +1416,17 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     const unsigned long long* d_desc = d_seq + 1;
     auto enqueue_common = [&] {
         rec(0);
-        // the destination descriptor, copied at run time from pinned memory on a side branch
+        // on a side branch beside the hash: clear the batch counters and copy
+        // the destination descriptor (read at run time from pinned memory)
         FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
         FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
+        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 64 + ntiles * 8, ix.side));
         FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
                                    ix.side));
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
         rec(1);
-        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 64 + ntiles * 8, s));
-        FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0)); // (the copy ran beside the hash)
+        FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
                                           tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, d_desc, s);
@@ -1794,17 +1795,17 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
 void DeviceIndex::collect_stages() {
     if (!stages_pending) return;
     FCLSH_CUDA(cudaEventSynchronize(ev[kStages]));
-    float total = 0;
-    FCLSH_CUDA(cudaEventElapsedTime(&total, ev[0], ev[5]));
-    batch_ms = total;
-    for (int i = 0; i < kStages; ++i) {
-        stage_ms[i] = -1; // not measured (stage timing off)
-        if (!stages_timed && i < 5) continue;
+    batch_ms = -1; // not measured (stage timing off: the events cost ~2 % of a cfg2 batch)
+    for (int i = 0; i < kStages; ++i) stage_ms[i] = -1;
+    for (int i = 0; i < kStages && stages_timed; ++i) {
         float ms = 0;
         FCLSH_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
         stage_ms[i] = ms;
     }
     if (stages_timed) {
+        float total = 0;
+        FCLSH_CUDA(cudaEventElapsedTime(&total, ev[0], ev[5]));
+        batch_ms = total;
         t_hash_ms = stage_ms[0];
         t_probe_ms = stage_ms[1] + stage_ms[2] + stage_ms[5]; // probe + dedup + verify are fused
         t_verify_ms = stage_ms[3] + stage_ms[4];              // result assembly
