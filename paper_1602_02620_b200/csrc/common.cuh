@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "host.hpp"
 
@@ -28,6 +30,32 @@ uint64_t& launch_counter();
             throw ::fclsh_b200::CudaError(std::string("kernel launch (") + __FILE__ + ":" +            \
                                           std::to_string(__LINE__) + "): " + cudaGetErrorString(_e));  \
     } while (0)
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// be scheduled while its stream predecessor still runs (the predecessor calls
+// pdl_trigger once all its CTAs are placed); it must call pdl_wait before it
+// reads anything the predecessor writes (griddepcontrol.wait returns once the
+// predecessor grid has completed and its memory is visible). Captured into a
+// graph this is a programmatic edge: the launch latency between the batch's
+// kernels overlaps the predecessor's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = std::getenv("FCLSH_NO_PDL") != nullptr; // A/B switch
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    FCLSH_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 constexpr int kNumSMs = 148; // B200
 

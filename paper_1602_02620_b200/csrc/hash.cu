@@ -823,6 +823,7 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
     const int warp = tid >> 5;
     const int slot = lane / G; // row within the warp
     const int g = lane % G;
+    pdl_trigger(); // the query kernel may be scheduled behind this grid (it waits for its completion)
 
     // pair i = (j/2)*G + g of a part is entries 2i, 2i+1 of the direct table
     for (uint32_t i = tid; i < p.parts * NP; i += NT) {

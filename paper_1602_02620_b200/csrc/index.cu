@@ -436,6 +436,8 @@ __global__ void __launch_bounds__(256) k_query_fused(
     unsigned int* dcnt_s = reinterpret_cast<unsigned int*>(smem); // [8] distinct ids per warp
     uint32_t* set = reinterpret_cast<uint32_t*>(smem) + 8 + warp * WS;
     for (int k = lane; k < WS; k += 32) set[k] = kEmpty; // afterwards cleared as it is read
+    pdl_trigger();
+    pdl_wait(); // the batch's keys (hash kernel) are complete from here on
     // queries are handed out one at a time (a warp that finishes early takes
     // the next), so the last wave does not leave most warps idle
     auto fetch = [&]() -> uint64_t {
@@ -616,6 +618,8 @@ __global__ void __launch_bounds__(512) k_query_dense(
     __shared__ unsigned long long base_s;
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    pdl_trigger();
+    pdl_wait(); // the warp kernel's hand-over list is complete from here on
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
     if (blockIdx.x >= ns) return; // at most ns CTAs can get a query (usually ns == 0: nothing handed over)
     __shared__ unsigned int next_s;
@@ -1024,6 +1028,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     const uint64_t q0 = uint64_t(t) * TQ;
     const uint32_t m = uint32_t(nq - q0 < TQ ? nq - q0 : TQ);
     const uint32_t ntiles = gridDim.x / kScanSplit;
+    pdl_wait(); // the query kernels' outputs are complete from here on
     if (tid == 0) { // the host destination (null counters: device buffers only)
         const unsigned long long* h = desc;
         hd_s.counters = h ? reinterpret_cast<unsigned long long*>(h[0]) : nullptr;
@@ -1271,9 +1276,9 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
-    kern<<<unsigned(grid), 256, smem, s>>>(qkeys, nq, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
-                                           ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
-                                           tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc);
+    launch_pdl(kern, unsigned(grid), 256, smem, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
+               ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos, tmp_id,
+               tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc);
     FCLSH_LAUNCHED();
 }
 
@@ -1296,10 +1301,10 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
     if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
     else grid = std::max<uint64_t>(1, std::min(grid, max_grid)); // sized by the last batch's hand-over
-    kern<<<unsigned(grid), kDenseThreads, smem, s>>>(qkeys, uint32_t(ix.tables), view<T>(ix), ix.rows.as<uint64_t>(),
-                                                     d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q, found_q, src_pos,
-                                         src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum,
-                                         desc, nq_all);
+    launch_pdl(kern, unsigned(grid), kDenseThreads, smem, s, qkeys, uint32_t(ix.tables), view<T>(ix),
+               ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q,
+               found_q, src_pos, src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum, desc,
+               nq_all);
     FCLSH_LAUNCHED();
 }
 
@@ -1436,9 +1441,13 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                 ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, d_desc, nq, s);
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
-        k_scan_compact<<<unsigned(ntiles * kScanSplit), 1024, 0, s>>>(nq, found_q, tile_sum, res_off, src_pos, tmp_id, tmp_dist,
-                                                         nq * slot_cap, cta_id, cta_dist, ix.id_offset, oq, oi, od,
-                                                         ix.d_pub, d_seq, ovf_cnt, coll_q, cand_q, d_desc);
+        launch_pdl(k_scan_compact, unsigned(ntiles * kScanSplit), 1024, 0, s, nq,
+                   static_cast<const unsigned long long*>(found_q), static_cast<const unsigned long long*>(tile_sum),
+                   res_off, static_cast<const unsigned long long*>(src_pos), static_cast<const uint32_t*>(tmp_id),
+                   static_cast<const uint32_t*>(tmp_dist), nq * slot_cap, static_cast<const uint32_t*>(cta_id),
+                   static_cast<const uint32_t*>(cta_dist), ix.id_offset, oq, oi, od, ix.d_pub, d_seq, ovf_cnt,
+                   static_cast<const unsigned long long*>(coll_q), static_cast<const unsigned long long*>(cand_q),
+                   d_desc);
         FCLSH_LAUNCHED();
         rec(5);
     };
