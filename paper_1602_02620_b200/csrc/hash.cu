@@ -797,7 +797,9 @@ __host__ __device__ constexpr int pt_warps() {
     return LOGN == 11 ? 12 : 8;
 }
 
-template <int LOGN>
+// P16: both positions of a pair in one 32-bit word (16 bits each: row-word
+// byte offset << 5 | rotation; rows up to 2 KB), halving the position loads
+template <int LOGN, bool P16>
 __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const FastParams p) {
     constexpr int N = 1 << LOGN;
     constexpr int G = lanes_for(LOGN);
@@ -835,8 +837,12 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
         t[2 * NP] = make_double2(s1, -s1);
         t[3 * NP] = make_double2(s0 + s1, s0 - s1);
         // (byte offset of the row word) << 5 | rotation: bit (pos mod 32) -> bit S (S+1)
-        pk_s[i] = make_uint2(((e0.x & ~31u) << 2) | ((e0.x - S) & 31u),
-                             ((e1.x & ~31u) << 2) | ((e1.x - S - 1) & 31u));
+        if constexpr (P16)
+            reinterpret_cast<uint32_t*>(pk_s)[i] = ((((e0.x >> 5) << 7) | ((e0.x - S) & 31u)) & 0xFFFFu) |
+                                                   ((((e1.x >> 5) << 7) | ((e1.x - S - 1) & 31u)) << 16);
+        else
+            pk_s[i] = make_uint2(((e0.x & ~31u) << 2) | ((e0.x - S) & 31u),
+                                 ((e1.x & ~31u) << 2) | ((e1.x - S - 1) & 31u));
     }
     __syncthreads();
 
@@ -878,10 +884,20 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
             // sketch + first stage: one table entry per column pair
 #pragma unroll
             for (int j = 0; j < E; j += 2) {
-                const uint2 pp = pk[(j / 2) * G];
-                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(rowb + (pp.x >> 5));
-                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(rowb + (pp.y >> 5));
-                const uint32_t r0 = __funnelshift_r(w0, w0, pp.x), r1 = __funnelshift_r(w1, w1, pp.y);
+                uint32_t r0, r1;
+                if constexpr (P16) {
+                    const uint32_t v = reinterpret_cast<const uint32_t*>(pk_s)[part * NP + g + (j / 2) * G];
+                    const uint32_t w0 = *reinterpret_cast<const uint32_t*>(rowb + ((v << 16) >> 21));
+                    const uint32_t w1 = *reinterpret_cast<const uint32_t*>(rowb + (v >> 21));
+                    r0 = __funnelshift_r(w0, w0, v);
+                    r1 = __funnelshift_r(w1, w1, v >> 16);
+                } else {
+                    const uint2 pp = pk[(j / 2) * G];
+                    const uint32_t w0 = *reinterpret_cast<const uint32_t*>(rowb + (pp.x >> 5));
+                    const uint32_t w1 = *reinterpret_cast<const uint32_t*>(rowb + (pp.y >> 5));
+                    r0 = __funnelshift_r(w0, w0, pp.x);
+                    r1 = __funnelshift_r(w1, w1, pp.y);
+                }
                 const uint32_t t = lop3<0xE2, 1u << S>(r0, r1);      // bit S from r0, S+1 from r1
                 const uint32_t off = lop3<0xEA, 3u << S>(t, tb_off); // + outcome (b0 + 2 b1) * NP * 16
                 const double2 v = *reinterpret_cast<const double2*>(tabb + off + (j / 2) * G * 16);
@@ -992,7 +1008,8 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
         const size_t smem_pt = size_t(fs.parts) * (1 << LOGN) / 2 * 72 + size_t(PW) * 32 * (G + 2) * 8 +
                                size_t(PW) * 2 * (32 / G) * fs.row_words * 8;
         if (DIRECT && !use_int && !use_pm && prm.layout == kLayoutPointMajor && smem_pt <= 227 * 1024) {
-            auto kern = k_hash_f64_pt<LOGN>;
+            static const bool pk32 = getenv("FCLSH_HASH_PK32") != nullptr; // A/B: 32-bit positions
+            auto kern = (!pk32 && fs.row_words * 8 <= 2048) ? k_hash_f64_pt<LOGN, true> : k_hash_f64_pt<LOGN, false>;
             const int per_sm = resident_ctas(kern, 32 * PW, smem_pt, fs.device);
             if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
             const uint64_t groups = (prm.n + (32 / G) - 1) / (32 / G);
