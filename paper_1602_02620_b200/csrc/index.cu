@@ -91,6 +91,17 @@ constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 #ifndef FCLSH_FUSED_U
 #define FCLSH_FUSED_U 2
 #endif
+#ifndef FCLSH_DENSE_U
+#define FCLSH_DENSE_U 2
+#endif
+#ifndef FCLSH_DENSE_RUN
+#define FCLSH_DENSE_RUN 2
+#endif
+#ifndef FCLSH_DENSE_MINB
+#define FCLSH_DENSE_MINB 2
+#endif
+constexpr int kDenseU = FCLSH_DENSE_U;     // home buckets per thread in flight in the CTA kernel
+constexpr int kDenseRun = FCLSH_DENSE_RUN; // buckets read at a time along a spilled run (CTA kernel)
 constexpr int kFusedU = FCLSH_FUSED_U; // tables per lane in flight in the warp kernel
 constexpr int kFusedCap = FCLSH_FUSED_CAP; // warp-kernel id-set slots (3/4 of it: distinct ids; more: the CTA kernel)
 
@@ -121,7 +132,30 @@ struct Tables {
     uint64_t cells;            // CSR cells per table
     uint64_t nbuckets;         // buckets per table
     uint32_t shift;            // CSR: cell = key >> shift; buckets: home = key >> shift
+    const uint32_t* filter;    // buckets: per-table key filter (null: none)
+    uint32_t filter_log;       // filter bits per table = 2^filter_log
 };
+
+// Key filter of the bucket tables: one bit per residue key mod 2^filter_log
+// per table (about one bit per posting), kept in L2 (~64 MB for cfg2) with an
+// evict_last policy. A probe whose bit is clear has no posting, so its random
+// DRAM read of the home bucket is skipped (cfg2: ~80 % of probes miss, and a
+// clear bit rejects ~37 % of them). No false negatives: every inserted
+// posting sets its bit.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t ld_filter(const uint32_t* a, uint64_t pol) {
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ const uint32_t* filter_word(const Tables<T>& tb, uint32_t t, uint64_t key) {
+    return tb.filter + (uint64_t(t) << (tb.filter_log - 5)) + ((key & ((uint64_t(1) << tb.filter_log) - 1)) >> 5);
+}
 
 // First position in [a, e) of a CSR cell (sorted by (key, id)) whose key is
 // >= key. Clustered data makes some cells long (a run of one popular key),
@@ -206,7 +240,8 @@ __global__ void __launch_bounds__(256) k_keys_table_major(const K* __restrict__ 
 // keys are table-major for one part: key of (row i, table t) at keys[t*n + i]
 template <typename T>
 __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t t0, uint32_t tg,
-                                uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets) {
+                                uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets,
+                                uint32_t* __restrict__ filter, uint32_t filter_log) {
     // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
     // their postings are inserted (all 511 at once thrash it: 43 GB of DRAM
     // reads for 8.6 GB of tables)
@@ -217,6 +252,10 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
         typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
         const uint64_t key = keys[uint64_t(t) * n + i];
         const typename T::E e = T::make(key, uint32_t(i));
+        if (filter) {
+            const uint64_t r = key & ((uint64_t(1) << filter_log) - 1);
+            atomicOr(filter + (uint64_t(t) << (filter_log - 5)) + (r >> 5), 1u << (r & 31));
+        }
         uint64_t b = key >> shift;
         for (;;) {
             typename T::E* bp = bt + b * kSlots;
@@ -583,6 +622,201 @@ __global__ void __launch_bounds__(256) k_query_fused(
     }
 }
 
+// K3+K4+K5 fused, one warp per query, without shared memory: the distinct
+// ids live in registers across the warp (lane k holds the k-th distinct id),
+// so the whole unified L1/shared array is L1 for the lines of the probes in
+// flight (rand_bench: any shared-memory carveout lowers the random-read rate
+// by ~12 %). Collisions are offered to the list in warp-uniform steps, each
+// lane offering at most one id per step: an offered id is compared with the
+// nd listed ids (broadcast by shuffles), ids new to the list are deduplicated
+// among the lanes with a match-any, and the lowest lane of each group appends
+// it. Every offered id is a collision, every append a candidate (the
+// reference's counters). More than 32 distinct ids or more than slot_cap
+// results: the query is handed to the CTA kernel, which recomputes all of its
+// outputs. The found (id << 32 | dist) are one per lane, sorted by a shuffle
+// bitonic network with ~0 padding.
+#ifndef FCLSH_WARP_MINB
+#define FCLSH_WARP_MINB 6
+#endif
+template <typename T, int LAYOUT, int U>
+__global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
+    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
+    const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
+    uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
+    unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
+    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
+    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum,
+    const unsigned long long* __restrict__ desc) {
+    using E = typename T::E;
+    constexpr unsigned kAll = 0xffffffffu;
+    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
+    const int lane = threadIdx.x & 31;
+    const uint64_t fpol = l2_evict_last_policy();
+    pdl_trigger();
+    pdl_wait(); // the batch's keys (hash kernel) are complete from here on
+    auto fetch = [&]() -> uint64_t {
+        unsigned int v = 0;
+        if (lane == 0) v = atomicAdd(qnext, 1u);
+        return __shfl_sync(kAll, v, 0);
+    };
+    for (uint64_t q = fetch(); q < nq; q = fetch()) {
+        const typename T::K* qk = qkeys + q * tables;
+        uint32_t list = kEmpty; // this lane's distinct id (lane < nd)
+        uint32_t nd = 0;        // distinct ids so far (warp-uniform)
+        bool over = false;      // more than 32 distinct ids (warp-uniform)
+        uint32_t coll = 0;      // this lane's postings
+        // one warp-uniform step: each lane offers at most one colliding id
+        auto offer = [&](bool has, uint32_t id) {
+            coll += has;
+            if (!__any_sync(kAll, has) || over) return;
+            bool seen = false;
+            for (uint32_t k = 0; k < nd; ++k) seen |= __shfl_sync(kAll, list, k) == id;
+            const bool fresh = has && !seen;
+            const uint32_t grp = __match_any_sync(kAll, fresh ? id : kEmpty);
+            const uint32_t lead = __ballot_sync(kAll, fresh && __ffs(grp) - 1 == lane);
+            if (!lead) return;
+            if (nd + __popc(lead) > 32) {
+                over = true;
+                return;
+            }
+            for (uint32_t b = lead; b; b &= b - 1) {
+                const uint32_t v = __shfl_sync(kAll, id, __ffs(b) - 1);
+                if (uint32_t(lane) == nd) list = v;
+                ++nd;
+            }
+        };
+        for (uint32_t t0 = 0; t0 < tables && !over; t0 += 32 * U) {
+            uint64_t key[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t t = t0 + u * 32 + lane;
+                key[u] = t < tables ? uint64_t(qk[t]) : 0ull;
+            }
+            if constexpr (LAYOUT == kLayoutCsr) {
+                uint32_t s[U], e[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) { // U directory lookups in flight
+                    const uint32_t t = t0 + u * 32 + lane;
+                    if (t < tables) {
+                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key[u] >> tb.shift);
+                        s[u] = __ldg(d);
+                        e[u] = __ldg(d + 1);
+                    } else {
+                        s[u] = e[u] = 0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const E* et = tb.data + uint64_t(t0 + u * 32 + lane) * tb.n;
+                    uint32_t a = cell_lower_bound<T>(et, s[u], e[u], key[u]);
+                    bool has = a < e[u] && T::key(et[a]) == key[u];
+                    while (__any_sync(kAll, has)) {
+                        offer(has, has ? T::id(et[a]) : 0u);
+                        if (has) {
+                            ++a;
+                            has = a < e[u] && T::key(et[a]) == key[u];
+                        }
+                    }
+                }
+            } else {
+                bool pass[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) pass[u] = t0 + u * 32 + lane < tables;
+                if (tb.filter) { // a clear filter bit: no posting has this key, no bucket read
+                    uint32_t fw[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        fw[u] = pass[u] ? ld_filter(filter_word(tb, t0 + u * 32 + lane, key[u]), fpol) : 0u;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) pass[u] = (fw[u] >> (key[u] & 31)) & 1u;
+                }
+                E sl[U][kSlots];
+#pragma unroll
+                for (int u = 0; u < U; ++u) { // U home buckets in flight
+                    const uint32_t t = t0 + u * 32 + lane;
+                    if (pass[u]) {
+                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool live = pass[u];
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+                        offer(live && !T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u], T::id(sl[u][j]));
+                    // the run continues into the next bucket (~3 %)
+                    bool cont = live && !T::empty(sl[u][kSlots - 1]);
+                    uint64_t b = (key[u] >> tb.shift) + 1;
+                    const E* base = tb.data + uint64_t(t0 + u * 32 + lane) * tb.nbuckets * kSlots;
+                    while (__any_sync(kAll, cont)) {
+                        E x[kSlots];
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j) x[j] = T::make(~0ull, ~0u);
+                        b &= tb.nbuckets - 1;
+                        if (cont) load_bucket(base + b * kSlots, x);
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j)
+                            offer(cont && !T::empty(x[j]) && T::key(x[j]) == key[u], T::id(x[j]));
+                        cont = cont && !T::empty(x[kSlots - 1]);
+                        ++b;
+                    }
+                }
+            }
+        }
+        const uint64_t m = __reduce_add_sync(kAll, coll);
+        // verify the listed ids, one per lane
+        uint32_t dist = 0;
+        if (!over && uint32_t(lane) < nd) {
+            const uint64_t* r = rows + uint64_t(list) * words;
+            const uint64_t* qr = qrows + q * words;
+            for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+        }
+        const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
+        const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
+        if (over || nfound > slot_cap) {
+            if (lane == 0) {
+                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                found_q[q] = 0; // written by the CTA kernel later
+                src_pos[q] = 0;
+            }
+            continue;
+        }
+        // ascending ids: bitonic sort across the warp (non-passes = +inf)
+        unsigned long long mine = pass ? (static_cast<unsigned long long>(list) << 32) | dist : ~0ull;
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(kAll, mine, j);
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
+                mine = (lower == up) ? lo : hi;
+            }
+        }
+        if (uint32_t(lane) < nfound) {
+            tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
+            tmp_dist[q * slot_cap + lane] = uint32_t(mine);
+        }
+        if (lane == 0) {
+            coll_q[q] = m;
+            cand_q[q] = nd;
+            found_q[q] = nfound;
+            if (hc) {
+                hc[(nq + 1) + q] = m;
+                hc[2 * (nq + 1) + q] = nd;
+                hc[3 * (nq + 1) + q] = nfound;
+            }
+            src_pos[q] = q * slot_cap;
+            if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
+        }
+    }
+}
+
 // Dense queries (clustered data, cfg4): one CTA per query. Dedup is a
 // shared-memory open-addressing id set instead of a sort of the collision
 // list, so the cost follows the distinct candidates (cfg4: ~480) rather than
@@ -597,7 +831,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
 // results do not fit the region, goes to the general path (ovf2), which
 // recomputes all its outputs.
 template <typename T, int LAYOUT, int HS, int FCAP>
-__global__ void __launch_bounds__(512) k_query_dense(
+__global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
     const typename T::K* __restrict__ qkeys, uint32_t tables, const Tables<T> tb, const uint64_t* __restrict__ rows,
     const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius, const uint32_t* __restrict__ ovf,
     const unsigned int* __restrict__ ovf_cnt, uint32_t direct_n, unsigned long long* __restrict__ coll_q,
@@ -605,7 +839,8 @@ __global__ void __launch_bounds__(512) k_query_dense(
     unsigned long long* __restrict__ src_pos, uint64_t src_base, uint32_t* __restrict__ res_id,
     uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
     uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext,
-    unsigned long long* __restrict__ tile_sum, const unsigned long long* __restrict__ desc, uint64_t nq_all) {
+    unsigned long long* __restrict__ tile_sum, const unsigned long long* __restrict__ desc, uint64_t nq_all,
+    uint32_t slot_cap, uint32_t* __restrict__ slot_id, uint32_t* __restrict__ slot_dist) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
@@ -623,16 +858,22 @@ __global__ void __launch_bounds__(512) k_query_dense(
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
     if (blockIdx.x >= ns) return; // at most ns CTAs can get a query (usually ns == 0: nothing handed over)
     __shared__ unsigned int next_s;
-    auto fetch = [&]() -> uint32_t { // dynamic hand-out: query costs vary widely on clustered data
-        if (tid == 0) next_s = atomicAdd(qnext, 1u);
+    // dynamic hand-out (query costs vary widely on clustered data); the next
+    // query is claimed as the current one starts, so the atomic's round trip
+    // overlaps the probes
+    unsigned int claimed = 0; // thread 0
+    auto fetch = [&]() -> uint32_t {
+        if (tid == 0) next_s = claimed;
         __syncthreads();
         return next_s; // rewritten only after the body's barriers
     };
+    if (tid == 0) claimed = atomicAdd(qnext, 1u);
     // the set is cleared once here and afterwards only where a query wrote
     for (uint32_t i = tid; i < HS; i += nt) set[i] = kEmpty;
     for (uint32_t s_ = fetch(); s_ < ns; s_ = fetch()) {
         const uint64_t q = ovf ? ovf[s_] : s_;
         if (tid == 0) {
+            claimed = atomicAdd(qnext, 1u);
             coll_s = cand_s = found_s = 0;
             bad_s = 0;
         }
@@ -640,23 +881,92 @@ __global__ void __launch_bounds__(512) k_query_dense(
         // phase 1: probe, dedup into the set, list each new id's slot
         const typename T::K* qk = qkeys + q * tables;
         uint32_t coll = 0;
-        for (uint32_t t = tid; t < tables; t += nt) {
-            if (bad_s) break;
-            coll += probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), [&](uint32_t id) {
-                if (bad_s) return; // the set holds at most kMaxDistinct + nt ids
-                uint32_t h = (id * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
-                for (;;) {
-                    const uint32_t old = atomicCAS(set + h, kEmpty, id);
-                    if (old == id) return; // seen
-                    if (old == kEmpty) break;
-                    h = (h + 1) & (HS - 1);
+        auto insert = [&](uint32_t id) {
+            if (bad_s) return; // the set holds at most kMaxDistinct + nt ids
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
+            for (;;) {
+                const uint32_t old = atomicCAS(set + h, kEmpty, id);
+                if (old == id) return; // seen
+                if (old == kEmpty) break;
+                h = (h + 1) & (HS - 1);
+            }
+            const uint32_t pos = atomicAdd(&cand_s, 1u);
+            if (pos < kMaxDistinct)
+                clist[pos] = uint16_t(h);
+            else
+                bad_s = 1;
+        };
+        if constexpr (LAYOUT == kLayoutBuckets && kDenseU > 1) {
+            // kDenseU home buckets per thread in flight; a run that spills
+            // past a full bucket is read kDenseRun adjacent buckets at a time
+            // (clustered data: popular keys fill runs of many buckets, and a
+            // bucket-by-bucket walk is a chain of dependent reads)
+            using E = typename T::E;
+            for (uint32_t t0 = tid; t0 < tables; t0 += kDenseU * nt) {
+                if (bad_s) break;
+                E sl[kDenseU][kSlots];
+                uint64_t key[kDenseU];
+                bool pass[kDenseU];
+#pragma unroll
+                for (int u = 0; u < kDenseU; ++u) {
+                    const uint32_t t = t0 + u * nt;
+                    pass[u] = t < tables;
+                    key[u] = pass[u] ? uint64_t(qk[t]) : 0ull;
                 }
-                const uint32_t pos = atomicAdd(&cand_s, 1u);
-                if (pos < kMaxDistinct)
-                    clist[pos] = uint16_t(h);
-                else
-                    bad_s = 1;
-            });
+                if (tb.filter) { // a clear filter bit: no posting has this key
+                    const uint64_t fpol = l2_evict_last_policy();
+                    uint32_t fw[kDenseU];
+#pragma unroll
+                    for (int u = 0; u < kDenseU; ++u)
+                        fw[u] = pass[u] ? ld_filter(filter_word(tb, t0 + u * nt, key[u]), fpol) : 0u;
+#pragma unroll
+                    for (int u = 0; u < kDenseU; ++u) pass[u] = (fw[u] >> (key[u] & 31)) & 1u;
+                }
+#pragma unroll
+                for (int u = 0; u < kDenseU; ++u) {
+                    const uint32_t t = t0 + u * nt;
+                    if (pass[u]) {
+                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kDenseU; ++u) {
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+                        if (!T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u]) {
+                            ++coll;
+                            insert(T::id(sl[u][j]));
+                        }
+                    if (T::empty(sl[u][kSlots - 1])) continue;
+                    const E* base = tb.data + uint64_t(t0 + u * nt) * tb.nbuckets * kSlots;
+                    uint64_t b = (key[u] >> tb.shift) + 1;
+                    for (bool cont = true; cont; b += kDenseRun) {
+                        E x[kDenseRun][kSlots];
+#pragma unroll
+                        for (int k = 0; k < kDenseRun; ++k)
+                            load_bucket(base + ((b + k) & (tb.nbuckets - 1)) * kSlots, x[k]);
+#pragma unroll
+                        for (int k = 0; k < kDenseRun; ++k) {
+                            if (!cont) break;
+#pragma unroll
+                            for (int j = 0; j < kSlots; ++j)
+                                if (!T::empty(x[k][j]) && T::key(x[k][j]) == key[u]) {
+                                    ++coll;
+                                    insert(T::id(x[k][j]));
+                                }
+                            cont = !T::empty(x[k][kSlots - 1]);
+                        }
+                    }
+                }
+            }
+        } else {
+            for (uint32_t t = tid; t < tables; t += nt) {
+                if (bad_s) break;
+                coll += probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), insert);
+            }
         }
         atomicAdd(&coll_s, coll);
         __syncthreads();
@@ -690,7 +1000,7 @@ __global__ void __launch_bounds__(512) k_query_dense(
         if (tid == 0) {
             bool bad = bad_s;
             base_s = 0;
-            if (!bad && nf) {
+            if (!bad && nf > slot_cap) {
                 base_s = atomicAdd(res_cursor, (unsigned long long)nf);
                 bad = base_s + nf > res_cap; // region full
             }
@@ -708,7 +1018,8 @@ __global__ void __launch_bounds__(512) k_query_dense(
                     hc[2 * (nq_all + 1) + q] = cand_s;
                     hc[3 * (nq_all + 1) + q] = nf;
                 }
-                src_pos[q] = src_base + base_s;
+                // up to slot_cap results go to the query's own slots (no bump allocation)
+                src_pos[q] = nf <= slot_cap ? q * slot_cap : src_base + base_s;
                 if (nf) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nf);
             }
         }
@@ -719,11 +1030,13 @@ __global__ void __launch_bounds__(512) k_query_dense(
             for (uint32_t i = nf + tid; i < P; i += nt) fl[i] = ~0ull;
             __syncthreads();
             bitonic_sort<NarrowEntry>(fl, P, P);
-            const uint64_t base = base_s;
+            const bool slots = nf <= slot_cap;
+            uint32_t* const oid = slots ? slot_id + q * slot_cap : res_id + base_s;
+            uint32_t* const odist = slots ? slot_dist + q * slot_cap : res_dist + base_s;
             for (uint32_t k = tid; k < nf; k += nt) {
                 const unsigned long long e = fl[k];
-                res_id[base + k] = uint32_t(e >> 32);
-                res_dist[base + k] = uint32_t(e);
+                oid[k] = uint32_t(e >> 32);
+                odist[k] = uint32_t(e);
             }
         }
         __syncthreads();
@@ -1181,6 +1494,8 @@ Tables<T> view(const DeviceIndex& ix) {
     tb.cells = ix.cells();
     tb.nbuckets = ix.nbuckets;
     tb.shift = ix.key_shift;
+    tb.filter = ix.filter_log ? ix.filter.as<uint32_t>() : nullptr;
+    tb.filter_log = ix.filter_log;
     return tb;
 }
 
@@ -1241,6 +1556,8 @@ void build_all(DeviceIndex& ix) {
         hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, L, kLayoutPointMajor, s, p, 1);
         if (ix.layout == kLayoutBuckets) {
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
+            uint32_t* fl = ix.filter_log ? ix.filter.as<uint32_t>() + ((uint64_t(p) * L) << (ix.filter_log - 5))
+                                         : nullptr;
             // keys table-major, then table groups of ~64 MB of buckets (half the L2)
             K* ktm = static_cast<K*>(keys_tm.ensure(L * n * kb));
             k_keys_table_major<K><<<unsigned(std::min<uint64_t>(((L + 31) / 32) * ((n + 31) / 32),
@@ -1252,7 +1569,8 @@ void build_all(DeviceIndex& ix) {
             for (uint32_t t0 = 0; t0 < L; t0 += tg) {
                 const uint32_t c = uint32_t(std::min<uint64_t>(tg, L - t0));
                 k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(ktm, n, t0, c, ix.key_shift,
-                                                                                      ix.nbuckets, bk);
+                                                                                      ix.nbuckets, bk, fl,
+                                                                                      ix.filter_log);
                 FCLSH_LAUNCHED();
             }
         } else {
@@ -1271,6 +1589,25 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, unsigned long long* tile_sum,
                   const unsigned long long* desc, cudaStream_t s) {
+    // default: the id list in registers (no shared memory, all of L1 for the
+    // probes in flight); FCLSH_FUSED_SHARED=1 selects the shared-set kernel
+    static const bool shared_set = getenv("FCLSH_FUSED_SHARED") != nullptr;
+    if (!shared_set) {
+        auto kern = k_query_warp<T, LAYOUT, kFusedU>;
+        static bool carved = false;
+        if (!carved) {
+            FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            carved = true;
+        }
+        const int per_sm = resident_ctas(kern, 256, 0, ix.device);
+        const uint64_t grid = std::max<uint64_t>(
+            1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
+        launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
+                   ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+                   tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc);
+        FCLSH_LAUNCHED();
+        return;
+    }
     auto kern = k_query_fused<T, LAYOUT, CAP, kFusedU>;
     const size_t smem = (8 + size_t(8) * CAP) * 4; // CAP = set slots per warp
     const int per_sm = resident_ctas(kern, 256, smem, ix.device);
@@ -1293,7 +1630,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 uint64_t src_base, uint32_t* res_id, uint32_t* res_dist, uint64_t res_cap,
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
                 uint64_t max_grid, unsigned long long* tile_sum, const unsigned long long* desc, uint64_t nq_all,
-                cudaStream_t s) {
+                uint32_t slot_cap, uint32_t* slot_id, uint32_t* slot_dist, cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
     const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
@@ -1304,7 +1641,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     launch_pdl(kern, unsigned(grid), kDenseThreads, smem, s, qkeys, uint32_t(ix.tables), view<T>(ix),
                ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q,
                found_q, src_pos, src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum, desc,
-               nq_all);
+               nq_all, slot_cap, slot_id, slot_dist);
     FCLSH_LAUNCHED();
 }
 
@@ -1438,7 +1775,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
                                 found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, d_desc, nq, s);
+                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, d_desc, nq, slot_cap, tmp_id,
+                                tmp_dist, s);
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
         launch_pdl(k_scan_compact, unsigned(ntiles * kScanSplit), 1024, 0, s, nq,
@@ -1685,8 +2023,33 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
         ix->key_shift = kbits - b;
     }
 
+    // key filter (buckets): about one bit per posting, at most kFilterMax
+    // bytes in all so that it stays in L2; below ~0.75 bits per posting it
+    // rejects too few probes to pay for its own read. FCLSH_FILTER=0: none.
+    ix->filter_log = 0;
+    if (layout == kLayoutBuckets && !(getenv("FCLSH_FILTER") && getenv("FCLSH_FILTER")[0] == '0')) {
+        constexpr uint64_t kFilterMax = uint64_t(80) << 20;
+        uint32_t fl = std::max<uint32_t>(5, bit_length(n - 1));
+        while (fl > 5 && ix->tables * (uint64_t(1) << fl) / 8 > kFilterMax) --fl;
+        if ((uint64_t(1) << fl) * 4 >= n * 3 && ix->tables * (uint64_t(1) << fl) / 8 <= kFilterMax) ix->filter_log = fl;
+    }
     try {
         ix->rows.ensure(n * W * 8);
+        if (ix->filter_log) {
+            const uint64_t fbytes = ix->tables * (uint64_t(1) << ix->filter_log) / 8;
+            ix->filter.ensure(fbytes);
+            FCLSH_CUDA(cudaMemsetAsync(ix->filter.p, 0, fbytes, ix->stream));
+            // room for the filter's evict_last lines in the persisting part of L2
+            int maxp = 0;
+            if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, opt.device) == cudaSuccess &&
+                maxp > 0) {
+                size_t cur = 0;
+                cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                const size_t want = std::min<size_t>(size_t(maxp), size_t(fbytes));
+                if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            }
+            cudaGetLastError();
+        }
         if (layout == kLayoutBuckets) {
             ix->entries.ensure(bkt_size(bb));
         } else {

@@ -46,6 +46,10 @@ struct DeviceIndex {
     double build_ms = 0;
     std::unique_ptr<DeviceFamilySet> fs;
     DevBuf rows, entries, dir;
+    // per-table key filter (buckets layout): bit (key mod 2^filter_log) of
+    // table t set iff some posting of t has that residue; 0: no filter
+    DevBuf filter;
+    uint32_t filter_log = 0;
 
     // query workspace (grow-only)
     DevBuf q_rows, q_keys, r_start, r_count, counters, coll_off, coll_sel, fill, cand, cand_sorted, src_pos,
