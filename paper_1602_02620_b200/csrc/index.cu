@@ -114,6 +114,22 @@ __device__ __forceinline__ void load_bucket(const unsigned long long* bp, unsign
         : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3])
         : "l"(bp));
 }
+#ifndef FCLSH_BUCKET_EF
+#define FCLSH_BUCKET_EF 1
+#endif
+// home-bucket read of the warp kernel: never reused within a batch, so with
+// FCLSH_BUCKET_EF its L2 line is marked evict_first (keeps the key filter)
+__device__ __forceinline__ void load_bucket_probe(const unsigned long long* bp, unsigned long long (&x)[kSlots],
+                                                  uint64_t pol) {
+#if FCLSH_BUCKET_EF
+    asm("ld.global.nc.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3])
+        : "l"(bp), "l"(pol));
+#else
+    (void)pol;
+    load_bucket(bp, x);
+#endif
+}
 __device__ __forceinline__ void load_bucket(const ulonglong2* bp, ulonglong2 (&x)[kSlots]) {
     asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
         : "=l"(x[0].x), "=l"(x[0].y), "=l"(x[1].x), "=l"(x[1].y)
@@ -133,12 +149,13 @@ struct Tables {
     uint64_t nbuckets;         // buckets per table
     uint32_t shift;            // CSR: cell = key >> shift; buckets: home = key >> shift
     const uint32_t* filter;    // buckets: per-table key filter (null: none)
-    uint32_t filter_log;       // filter bits per table = 2^filter_log
+    uint32_t filter_words;     // filter words (32 bits) per table
+    uint32_t filter_shift;     // 64 - key bits: key << filter_shift is a 64-bit fraction
 };
 
-// Key filter of the bucket tables: one bit per residue key mod 2^filter_log
-// per table (about one bit per posting), kept in L2 (~64 MB for cfg2) with an
-// evict_last policy. A probe whose bit is clear has no posting, so its random
+// Key filter of the bucket tables: M = 32 * filter_words bits per table
+// (about one per posting); key k maps to bit floor(k * M / 2^kbits) (keys are
+// uniform in [0, P)). Kept in L2 (~64 MB for cfg2) with an evict_last policy. A probe whose bit is clear has no posting, so its random
 // DRAM read of the home bucket is skipped (cfg2: ~80 % of probes miss, and a
 // clear bit rejects ~37 % of them). No false negatives: every inserted
 // posting sets its bit.
@@ -147,14 +164,27 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void load_bucket_probe(const ulonglong2* bp, ulonglong2 (&x)[kSlots], uint64_t) {
+    load_bucket(bp, x);
+}
 __device__ __forceinline__ uint32_t ld_filter(const uint32_t* a, uint64_t pol) {
     uint32_t v;
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
     return v;
 }
+__device__ __forceinline__ uint32_t filter_bit(uint64_t key, uint32_t words, uint32_t shift) {
+    return uint32_t(__umul64hi(key << shift, uint64_t(words) * 32));
+}
+// filter test of (table t, key): one L2 word read (evict_last policy)
 template <typename T>
-__device__ __forceinline__ const uint32_t* filter_word(const Tables<T>& tb, uint32_t t, uint64_t key) {
-    return tb.filter + (uint64_t(t) << (tb.filter_log - 5)) + ((key & ((uint64_t(1) << tb.filter_log) - 1)) >> 5);
+__device__ __forceinline__ bool filter_pass(const Tables<T>& tb, uint32_t t, uint64_t key, uint64_t pol) {
+    const uint32_t r = filter_bit(key, tb.filter_words, tb.filter_shift);
+    return (ld_filter(tb.filter + uint64_t(t) * tb.filter_words + (r >> 5), pol) >> (r & 31)) & 1u;
 }
 
 // First position in [a, e) of a CSR cell (sorted by (key, id)) whose key is
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(256) k_keys_table_major(const K* __restrict__ 
 template <typename T>
 __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t t0, uint32_t tg,
                                 uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets,
-                                uint32_t* __restrict__ filter, uint32_t filter_log) {
+                                uint32_t* __restrict__ filter, uint32_t filter_words, uint32_t filter_shift) {
     // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
     // their postings are inserted (all 511 at once thrash it: 43 GB of DRAM
     // reads for 8.6 GB of tables)
@@ -253,8 +283,8 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
         const uint64_t key = keys[uint64_t(t) * n + i];
         const typename T::E e = T::make(key, uint32_t(i));
         if (filter) {
-            const uint64_t r = key & ((uint64_t(1) << filter_log) - 1);
-            atomicOr(filter + (uint64_t(t) << (filter_log - 5)) + (r >> 5), 1u << (r & 31));
+            const uint32_t r = filter_bit(key, filter_words, filter_shift);
+            atomicOr(filter + uint64_t(t) * filter_words + (r >> 5), 1u << (r & 31));
         }
         uint64_t b = key >> shift;
         for (;;) {
@@ -653,6 +683,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     const int lane = threadIdx.x & 31;
     const uint64_t fpol = l2_evict_last_policy();
+    const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
     pdl_wait(); // the batch's keys (hash kernel) are complete from here on
     auto fetch = [&]() -> uint64_t {
@@ -724,19 +755,16 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
 #pragma unroll
                 for (int u = 0; u < U; ++u) pass[u] = t0 + u * 32 + lane < tables;
                 if (tb.filter) { // a clear filter bit: no posting has this key, no bucket read
-                    uint32_t fw[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        fw[u] = pass[u] ? ld_filter(filter_word(tb, t0 + u * 32 + lane, key[u]), fpol) : 0u;
-#pragma unroll
-                    for (int u = 0; u < U; ++u) pass[u] = (fw[u] >> (key[u] & 31)) & 1u;
+                    for (int u = 0; u < U; ++u) pass[u] = pass[u] && filter_pass(tb, t0 + u * 32 + lane, key[u], fpol);
                 }
                 E sl[U][kSlots];
 #pragma unroll
                 for (int u = 0; u < U; ++u) { // U home buckets in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (pass[u]) {
-                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
+                        load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u],
+                                          bpol);
                     } else {
 #pragma unroll
                         for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
@@ -915,12 +943,8 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
                 }
                 if (tb.filter) { // a clear filter bit: no posting has this key
                     const uint64_t fpol = l2_evict_last_policy();
-                    uint32_t fw[kDenseU];
 #pragma unroll
-                    for (int u = 0; u < kDenseU; ++u)
-                        fw[u] = pass[u] ? ld_filter(filter_word(tb, t0 + u * nt, key[u]), fpol) : 0u;
-#pragma unroll
-                    for (int u = 0; u < kDenseU; ++u) pass[u] = (fw[u] >> (key[u] & 31)) & 1u;
+                    for (int u = 0; u < kDenseU; ++u) pass[u] = pass[u] && filter_pass(tb, t0 + u * nt, key[u], fpol);
                 }
 #pragma unroll
                 for (int u = 0; u < kDenseU; ++u) {
@@ -1494,8 +1518,9 @@ Tables<T> view(const DeviceIndex& ix) {
     tb.cells = ix.cells();
     tb.nbuckets = ix.nbuckets;
     tb.shift = ix.key_shift;
-    tb.filter = ix.filter_log ? ix.filter.as<uint32_t>() : nullptr;
-    tb.filter_log = ix.filter_log;
+    tb.filter = ix.filter_words ? ix.filter.as<uint32_t>() : nullptr;
+    tb.filter_words = ix.filter_words;
+    tb.filter_shift = ix.filter_shift;
     return tb;
 }
 
@@ -1556,8 +1581,7 @@ void build_all(DeviceIndex& ix) {
         hash_rows(*ix.fs, ix.rows.as<uint64_t>(), n, keys.p, kb, L, kLayoutPointMajor, s, p, 1);
         if (ix.layout == kLayoutBuckets) {
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
-            uint32_t* fl = ix.filter_log ? ix.filter.as<uint32_t>() + ((uint64_t(p) * L) << (ix.filter_log - 5))
-                                         : nullptr;
+            uint32_t* fl = ix.filter_words ? ix.filter.as<uint32_t>() + uint64_t(p) * L * ix.filter_words : nullptr;
             // keys table-major, then table groups of ~64 MB of buckets (half the L2)
             K* ktm = static_cast<K*>(keys_tm.ensure(L * n * kb));
             k_keys_table_major<K><<<unsigned(std::min<uint64_t>(((L + 31) / 32) * ((n + 31) / 32),
@@ -1570,7 +1594,8 @@ void build_all(DeviceIndex& ix) {
                 const uint32_t c = uint32_t(std::min<uint64_t>(tg, L - t0));
                 k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(ktm, n, t0, c, ix.key_shift,
                                                                                       ix.nbuckets, bk, fl,
-                                                                                      ix.filter_log);
+                                                                                      ix.filter_words,
+                                                                                      ix.filter_shift);
                 FCLSH_LAUNCHED();
             }
         } else {
@@ -2023,20 +2048,24 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
         ix->key_shift = kbits - b;
     }
 
-    // key filter (buckets): about one bit per posting, at most kFilterMax
-    // bytes in all so that it stays in L2; below ~0.75 bits per posting it
-    // rejects too few probes to pay for its own read. FCLSH_FILTER=0: none.
-    ix->filter_log = 0;
+    // key filter (buckets): FCLSH_FILTER_BPK bits per posting (default 1),
+    // at most FCLSH_FILTER_MB (default 80) MiB in all so that it stays in L2;
+    // below 3/4 bit per posting it rejects too few probes to pay for its own
+    // read. FCLSH_FILTER=0: none.
+    ix->filter_words = 0;
+    ix->filter_shift = 64 - kbits;
     if (layout == kLayoutBuckets && !(getenv("FCLSH_FILTER") && getenv("FCLSH_FILTER")[0] == '0')) {
-        constexpr uint64_t kFilterMax = uint64_t(80) << 20;
-        uint32_t fl = std::max<uint32_t>(5, bit_length(n - 1));
-        while (fl > 5 && ix->tables * (uint64_t(1) << fl) / 8 > kFilterMax) --fl;
-        if ((uint64_t(1) << fl) * 4 >= n * 3 && ix->tables * (uint64_t(1) << fl) / 8 <= kFilterMax) ix->filter_log = fl;
+        const double bpk = getenv("FCLSH_FILTER_BPK") ? atof(getenv("FCLSH_FILTER_BPK")) : 1.0;
+        const double mb = getenv("FCLSH_FILTER_MB") ? atof(getenv("FCLSH_FILTER_MB")) : 80.0;
+        const uint64_t cap_words = uint64_t(mb * 1048576.0 / 4.0) / ix->tables;
+        const uint64_t want_words = (uint64_t(double(n) * bpk) + 31) / 32;
+        const uint64_t words = std::min<uint64_t>({cap_words, want_words, uint64_t(1) << 26});
+        if (words * 32 * 4 >= n * 3) ix->filter_words = uint32_t(words);
     }
     try {
         ix->rows.ensure(n * W * 8);
-        if (ix->filter_log) {
-            const uint64_t fbytes = ix->tables * (uint64_t(1) << ix->filter_log) / 8;
+        if (ix->filter_words) {
+            const uint64_t fbytes = ix->tables * ix->filter_words * 4;
             ix->filter.ensure(fbytes);
             FCLSH_CUDA(cudaMemsetAsync(ix->filter.p, 0, fbytes, ix->stream));
             // room for the filter's evict_last lines in the persisting part of L2

@@ -46,10 +46,11 @@ struct DeviceIndex {
     double build_ms = 0;
     std::unique_ptr<DeviceFamilySet> fs;
     DevBuf rows, entries, dir;
-    // per-table key filter (buckets layout): bit (key mod 2^filter_log) of
-    // table t set iff some posting of t has that residue; 0: no filter
+    // per-table key filter (buckets layout, index.cu): filter_words 32-bit
+    // words per table, bit floor(key * 32 * filter_words / 2^kbits) set iff
+    // some posting of the table maps there; 0 words: no filter
     DevBuf filter;
-    uint32_t filter_log = 0;
+    uint32_t filter_words = 0, filter_shift = 0;
 
     // query workspace (grow-only)
     DevBuf q_rows, q_keys, r_start, r_count, counters, coll_off, coll_sel, fill, cand, cand_sorted, src_pos,
