@@ -321,11 +321,14 @@ def main():
     roofline = None
     if dom_bytes is not None:
         ach = dom_bytes / (stage_avg[dominant] / 1e3) / 1e9
-        traffic, tsrc = measured_traffic("k_query_fused") if dominant == "fused" else (None, None)
-        roofline = {"bound": "hbm", "kernel": "k_query_fused" if dominant == "fused" else dominant,
+        traffic, tsrc = measured_traffic("k_query_warp") if dominant == "fused" else (None, None)
+        roofline = {"bound": "hbm", "kernel": "k_query_warp" if dominant == "fused" else dominant,
                     "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                     "traffic_source": tsrc, "peak_source": peak_src, "algorithmic_bytes_per_launch": dom_bytes,
-                    "duration_ms": stage_avg[dominant]}
+                    "duration_ms": stage_avg[dominant],
+                    "bytes_note": "one 32-B bucket sector per (query, table) probe, also for the ~30 % of probes "
+                                  "whose bucket read the L2 key filter skips (the reference's lookup count); "
+                                  "traffic = measured DRAM bytes per launch"}
     stage_rooflines = {k: {"ms": stage_avg[k], "GB/s": algo[k] / (stage_avg[k] / 1e3) / 1e9,
                            "frac": algo[k] / (stage_avg[k] / 1e3) / 1e9 / hbm}
                        for k in algo if stage_avg.get(k, 0) > 0}
