@@ -1619,10 +1619,11 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     static const bool shared_set = getenv("FCLSH_FUSED_SHARED") != nullptr;
     if (!shared_set) {
         auto kern = k_query_warp<T, LAYOUT, kFusedU>;
-        static bool carved = false;
-        if (!carved) {
+        static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
+        const uint64_t bit = uint64_t(1) << (ix.device & 63);
+        if (!(carved.load(std::memory_order_acquire) & bit)) {
             FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-            carved = true;
+            carved.fetch_or(bit, std::memory_order_acq_rel);
         }
         const int per_sm = resident_ctas(kern, 256, 0, ix.device);
         const uint64_t grid = std::max<uint64_t>(
@@ -2059,8 +2060,9 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
         const double mb = getenv("FCLSH_FILTER_MB") ? atof(getenv("FCLSH_FILTER_MB")) : 80.0;
         const uint64_t cap_words = uint64_t(mb * 1048576.0 / 4.0) / ix->tables;
         const uint64_t want_words = (uint64_t(double(n) * bpk) + 31) / 32;
+        const double min_bpk = getenv("FCLSH_FILTER_MIN") ? atof(getenv("FCLSH_FILTER_MIN")) : 0.75;
         const uint64_t words = std::min<uint64_t>({cap_words, want_words, uint64_t(1) << 26});
-        if (words * 32 * 4 >= n * 3) ix->filter_words = uint32_t(words);
+        if (words > 0 && double(words) * 32 >= double(n) * min_bpk) ix->filter_words = uint32_t(words);
     }
     try {
         ix->rows.ensure(n * W * 8);

@@ -237,3 +237,21 @@ def test_query_c_r_nn_matches_the_reference(layout, override, radius, budget):
     none = want_b[:, 0] == 0xFFFFFFFF
     assert (bid[none] == -1).all() and (bd[none] == -1).all()
     assert (bid[~none] == want_b[~none, 0]).all() and (bd[~none] == want_b[~none, 1]).all()
+
+
+@pytest.mark.parametrize("env", [{"FCLSH_FILTER": "0"}, {"FCLSH_FILTER_BPK": "0.75"}, {"FCLSH_FILTER_BPK": "1"},
+                                 {"FCLSH_FILTER_BPK": "8", "FCLSH_FILTER_MB": "512"}])
+@pytest.mark.parametrize("prime", [M31, M61])
+def test_key_filter_sizes_match_oracle(oracle, monkeypatch, env, prime):
+    """The L2 key filter of the bucket tables (index.cu, filter_pass) only
+    skips bucket reads of keys no posting has: off, near its smallest size
+    (many false positives), default and oversized, with 32- and 61-bit keys
+    (filter_shift 33 / 3), the ids and every counter equal the reference's.
+    Uniform queries (no near neighbour) are mostly filter rejections."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(len(env) * 7 + prime % 13)
+    d = 256
+    rows = random_rows(rng, 5000, d)
+    q = np.concatenate([planted_queries(rng, rows, d, 150, 8), random_rows(rng, 50, d)])
+    check_against_oracle(oracle, rows, q, d, 8, (0, 1), prime, layouts=("buckets",))
