@@ -417,7 +417,20 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         FCLSH_CUDA(cudaSetDevice(ix.device));
         const uint64_t W = ix.row_words;
         uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
-        if (nq) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
+        // Rows in pinned (page-locked, device-mapped) host memory are hashed
+        // in place: the hash kernel reads them over PCIe and writes the
+        // device copy the verify reads, so the batch has no separate H2D
+        // copy. Pageable rows: one cudaMemcpyAsync. FCLSH_NO_ZERO_COPY=1: copy always.
+        const uint64_t* hsrc = nullptr;
+        static const bool no_zc = getenv("FCLSH_NO_ZERO_COPY") != nullptr;
+        if (nq && !no_zc) {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, q_rows) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer)
+                hsrc = static_cast<const uint64_t*>(pa.devicePointer);
+            cudaGetLastError();
+        }
+        if (nq && !hsrc) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
         // one pinned block per result: [header | fclsh_result | counters | id | distance | query].
         // Sized for a guess of the result count, so the counters can be read
         // back while the batch runs; a larger total takes a larger block.
@@ -452,7 +465,7 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         QueryOutput o;
         try {
             static const bool no_dest = getenv("FCLSH_NO_HOST_DEST") != nullptr; // A/B: D2H copies instead
-            o = query_device(ix, dq, nq, radius, s, {}, dest.counters && !no_dest ? &dest : nullptr);
+            o = query_device(ix, dq, nq, radius, s, {}, dest.counters && !no_dest ? &dest : nullptr, hsrc);
         } catch (...) {
             cudaStreamSynchronize(s);
             pinned_pool().give(blk);

@@ -54,6 +54,7 @@ struct FastParams {
     uint32_t part_words;   // uint2 per part in fam
     uint32_t lane_entries; // M (general path)
     const uint2* fam;
+    uint64_t* rows_copy; // optional: every row also written here (k_hash_f64_pt)
     void* keys;
     uint64_t key_stride;
     uint64_t L;
@@ -871,6 +872,10 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
         fetch(grp + nwarps, rw + ((it + 1) & 1) * wrow);
         cp_async_wait_one();
         __syncwarp();
+        if (p.rows_copy) { // this group's rows, staged, also to the device copy
+            const uint64_t base = grp * wrow, lim = p.n * p.row_words;
+            for (uint32_t i = lane; i < wrow && base + i < lim; i += 32) p.rows_copy[base + i] = rw[(it & 1) * wrow + i];
+        }
         const uint32_t* myrow = reinterpret_cast<const uint32_t*>(rw + (it & 1) * wrow + slot * p.row_words);
         const uint64_t p0 = grp * SPW;
         const uint64_t my_point = p0 + slot;
@@ -992,8 +997,16 @@ size_t fast_smem_bytes(const DeviceFamilySet& fs) {
 }
 
 template <int LOGN, bool DIRECT>
-void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream) {
+void launch_fast(DeviceFamilySet& fs, const FastParams& prm_in, cudaStream_t stream) {
     constexpr int G = lanes_for(LOGN);
+    FastParams prm = prm_in;
+    // kernels other than k_hash_f64_pt do not copy the rows: copy first, hash the copy
+    auto copy_first = [&]() {
+        if (!prm.rows_copy) return;
+        FCLSH_CUDA(cudaMemcpyAsync(prm.rows_copy, prm.rows, prm.n * prm.row_words * 8, cudaMemcpyDefault, stream));
+        prm.rows = prm.rows_copy;
+        prm.rows_copy = nullptr;
+    };
     constexpr int PT = 256 / G;
     const size_t smem = fast_smem_bytes<LOGN, DIRECT>(fs);
     if constexpr (G > 1) {
@@ -1018,6 +1031,7 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
             FCLSH_LAUNCHED();
             return;
         }
+        copy_first();
         const size_t smem_f64 = size_t(WARPS) * 32 * (E + 2) * 8 + size_t(WARPS) * (32 / G) * fs.row_words * 8 +
                                 size_t(fs.parts) * (1 << LOGN) / 2 * 24;
         if (DIRECT && !use_int && prm.layout == kLayoutPointMajor && smem_f64 <= 227 * 1024) {
@@ -1042,6 +1056,7 @@ void launch_fast(DeviceFamilySet& fs, const FastParams& prm, cudaStream_t stream
             return;
         }
     }
+    copy_first();
     auto kern = k_hash_m31<LOGN, DIRECT>;
     const int per_sm = resident_ctas(kern, 256, smem, fs.device);
     if (per_sm < 1) throw ResourceError("hash: kernel does not fit on an SM (shared memory)");
@@ -1195,7 +1210,7 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Family& f, int dev
 
 void hash_rows(DeviceFamilySet& fs, const uint64_t* d_rows, uint64_t n, void* d_keys,
                uint32_t key_bytes, uint64_t key_stride, int layout, cudaStream_t stream,
-               uint32_t part_begin, uint32_t part_count) {
+               uint32_t part_begin, uint32_t part_count, uint64_t* rows_copy) {
     if (part_count == 0) part_count = fs.parts - part_begin;
     if (part_begin + part_count > fs.parts) throw UsageError("hash: part range out of bounds");
     if (key_bytes != 4 && key_bytes != 8) throw UsageError("hash: key_bytes must be 4 or 8");
@@ -1207,9 +1222,16 @@ void hash_rows(DeviceFamilySet& fs, const uint64_t* d_rows, uint64_t n, void* d_
         throw UsageError("hash: key_stride below the table count");
     if (n == 0) return;
     FCLSH_CUDA(cudaSetDevice(fs.device));
+    if (rows_copy && !fs.fast) {
+        // only k_hash_f64_pt copies as it goes: copy first, hash the copy
+        FCLSH_CUDA(cudaMemcpyAsync(rows_copy, d_rows, n * fs.row_words * 8, cudaMemcpyDefault, stream));
+        d_rows = rows_copy;
+        rows_copy = nullptr;
+    }
     if (fs.fast) {
         FastParams prm{};
         prm.rows = d_rows;
+        prm.rows_copy = rows_copy;
         prm.n = n;
         prm.row_words = fs.row_words;
         prm.parts = part_count;

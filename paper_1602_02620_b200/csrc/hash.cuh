@@ -63,6 +63,10 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Family& f, int dev
 // = all); table indices in the output are relative to part_begin.
 void hash_rows(DeviceFamilySet& fs, const uint64_t* d_rows, uint64_t n, void* d_keys,
                uint32_t key_bytes, uint64_t key_stride, int layout, cudaStream_t stream,
-               uint32_t part_begin = 0, uint32_t part_count = 0);
+               uint32_t part_begin = 0, uint32_t part_count = 0, uint64_t* rows_copy = nullptr);
+// rows_copy (optional): the rows are also written there (n * row_words
+// words); the point-major FP64 kernel does it as it stages each row, so a
+// query batch can be hashed straight from mapped pinned host memory while
+// its device copy (for the verify) is made on the way.
 
 } // namespace fclsh_b200

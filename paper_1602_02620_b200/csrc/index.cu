@@ -1688,7 +1688,8 @@ void wait_published(const unsigned long long* h_pub, unsigned long long seq, cud
 
 template <typename T, int LAYOUT>
 QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s,
-                       const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest) {
+                       const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest,
+                       const uint64_t* hash_src) {
     using K = typename T::K;
     QueryOutput out;
     out.nq = nq;
@@ -1792,7 +1793,9 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
                                    ix.side));
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
-        hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
+        // hash_src (mapped pinned host rows): hashed from there, copied to d_q on the way
+        hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
+                  hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
         rec(1);
         FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
@@ -1840,7 +1843,8 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                               cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
                                               ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq,
                                               reinterpret_cast<const void*>(uintptr_t(timing)),
-                                              reinterpret_cast<const void*>(uintptr_t(dense_grid)), tile_sum};
+                                              reinterpret_cast<const void*>(uintptr_t(dense_grid)), tile_sum,
+                                              hash_src};
         if (ix.gexec && key == ix.gkey) {
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
@@ -2165,7 +2169,8 @@ void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t 
 }
 
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
-                         const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest) {
+                         const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest,
+                         const uint64_t* hash_src) {
     if (radius > ix.radius) // index.cpp:147-153
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
@@ -2181,11 +2186,11 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
     }
     QueryOutput o;
     if (ix.wide)
-        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest)
-                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest);
+        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest, hash_src)
+                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest, hash_src);
     else
-        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest)
-                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest);
+        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest, hash_src)
+                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest, hash_src);
     if (join) {
         FCLSH_CUDA(cudaEventRecord(ix.ev_out, s));
         FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));

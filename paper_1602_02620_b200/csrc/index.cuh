@@ -137,7 +137,10 @@ struct HostDest {
 // values complete in stream order), d_query / d_id / d_dist and total are not.
 QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                          cudaStream_t stream, const std::function<void(const QueryOutput&)>& before_wait = {},
-                         const HostDest* dest = nullptr);
+                         const HostDest* dest = nullptr, const uint64_t* hash_src = nullptr);
+// hash_src (optional): the same rows in mapped pinned host memory (device
+// view); the hash kernel reads them there and writes d_q as it goes, so no
+// separate host-to-device copy of the batch is needed
 
 // query_c_r_nn (index.cpp:190-235) for nq device rows: d_counters [nq][3]
 // {collisions, candidates, found}, d_best [nq][2] {id, distance} (all-ones

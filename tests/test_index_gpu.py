@@ -255,3 +255,27 @@ def test_key_filter_sizes_match_oracle(oracle, monkeypatch, env, prime):
     rows = random_rows(rng, 5000, d)
     q = np.concatenate([planted_queries(rng, rows, d, 150, 8), random_rows(rng, 50, d)])
     check_against_oracle(oracle, rows, q, d, 8, (0, 1), prime, layouts=("buckets",))
+
+
+@pytest.mark.parametrize("d,radius,override", [(256, 8, (0, 1)), (128, 4, (0, 1)), (512, 12, (2, 2))])
+def test_pinned_rows_hashed_in_place(oracle, d, radius, override):
+    """fclsh_query with rows in pinned host memory hashes them in place (the
+    hash kernel reads them over PCIe and writes the device copy the verify
+    reads; other hash kernels copy first): results and counters equal the
+    pageable-rows call and the reference, batch after batch (graph replay)."""
+    import torch
+    rng = np.random.default_rng(d + radius)
+    rows = random_rows(rng, 4000, d)
+    q = planted_queries(rng, rows, d, 300, radius + 2)
+    force = F.PlanOverride(F.PlanKind(override[0]), override[1])
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, force)
+    ix = F.build_index(rows, radius, plan, 22, prime=M31)
+    pinned = torch.from_numpy(q.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    want = ix.query_r_nn(q, radius)
+    oi = oracle.index_build(rows, d, radius, 11, 22, override=override, prime=M31, threads=4)
+    counters, offsets, ids = oi.query(q, radius, threads=4)
+    assert (want.id == ids).all() and (want.offsets == offsets).all()
+    for _ in range(3):
+        got = ix.query_r_nn(pinned, radius)
+        assert (got.triples() == want.triples()).all()
+        assert (np.stack([got.collisions, got.candidates, got.found], 1) == counters).all()
