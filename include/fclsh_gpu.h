@@ -24,8 +24,10 @@
  *    fclsh_last_error() returns the message of the last failure on the
  *    calling thread, with the reference's wording where one exists.
  *  - Device (`d_`) pointers must be device memory on the handle's device.
- *  - Handles are bound to one device; calls on one handle serialize. Distinct
- *    handles may be driven from distinct host threads.
+ *  - Handles are bound to one device; calls on one handle serialize (the
+ *    library locks each handle: concurrent callers take turns). Distinct
+ *    handles may be driven from distinct host threads. Device result
+ *    pointers returned by a handle stay valid until its next query.
  */
 #ifndef FCLSH_GPU_H
 #define FCLSH_GPU_H
@@ -241,8 +243,9 @@ int fclsh_query_device(fclsh_index* ix, const uint64_t* d_q_rows, uint64_t nq, u
  * walk the buckets in table order and stop after posting_budget postings
  * (< 0: the reference's default 3L), return the closest point retrieved
  * (ties: the lowest id). counters[nq][3] = {collisions, candidates, found},
- * best[nq][2] = {id, distance}, both UINT32_MAX when nothing was retrieved.
- * Budgets above 12288 are rejected (the CTA's shared set). Synchronous. */
+ * best[nq][2] = {id (+ id_offset), distance}, both UINT32_MAX when nothing
+ * was retrieved. Any budget (budgets above 12288 distinct ids, or a cut
+ * bucket above 4096 postings, run from a global-memory id set). Synchronous. */
 int fclsh_query_c_r_nn(fclsh_index* ix, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
                        int64_t posting_budget, uint64_t* counters, uint32_t* best);
 
@@ -329,6 +332,77 @@ int fclsh_scan_truth(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const u
 int fclsh_distance_histogram(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n, const uint64_t* d_q_rows,
                              uint64_t nq, uint64_t dims, uint64_t sample_per_query, uint64_t seed, void* stream,
                              uint64_t* counts);
+
+/* --------------------------------------------------------------- cluster ---
+ * A point-sharded index over the GPUs of one box (the
+ * reference is single-process and single-threaded, so this has
+ * no reference counterpart beyond query_r_nn's results). The n points are cut
+ * into world x shards_per_rank contiguous, balanced id ranges (shard g owns
+ * [g*n/S, (g+1)*n/S)); each shard is an index (fclsh_index_build semantics,
+ * the same plan, seed and families, ids offset by the shard start), rank r
+ * holds shards [r*spr, (r+1)*spr) on its GPU. A query batch is broadcast
+ * from rank 0 (ncclBroadcast), answered by every shard concurrently, merged
+ * per GPU, sent to rank 0 (ncclAllGather of the totals, grouped
+ * ncclSend/ncclRecv) and merged there: triples in (query, id) order and
+ * counters summed, i.e. exactly fclsh_query's result on one index over all
+ * points (every posting and id lives in one shard). NCCL (libnccl.so.2) is
+ * loaded at run time, only when world > 1 (FCLSH_CLUSTER_NCCL=1: also at 1).
+ *
+ * Two ways to form one:
+ *  - fclsh_cluster_create: this process drives ndev GPUs (ncclCommInitAll);
+ *    shards_per_device >= 1, so S shards fit on fewer GPUs (S = 8 on one GPU
+ *    runs the 8-GPU layout on a single device);
+ *  - fclsh_cluster_create_rank: one process per GPU (torchrun): rank 0 calls
+ *    fclsh_cluster_unique_id, sends the id to the others out of band, and
+ *    every rank calls this with it (ncclCommInitRank).
+ * Build and query are collective: every process calls them, in the same
+ * order. Calls on one handle serialize. At most 64 shards in all. */
+typedef struct fclsh_cluster fclsh_cluster;
+#define FCLSH_CLUSTER_ID_BYTES 128
+#define FCLSH_ROWS_GLOBAL 0 /* rows = all n points */
+#define FCLSH_ROWS_LOCAL 1  /* rows = only the contiguous range of this process's shards */
+
+int fclsh_cluster_unique_id(unsigned char* id /* [FCLSH_CLUSTER_ID_BYTES] */);
+int fclsh_cluster_create(const int* devices, uint32_t ndev, uint32_t shards_per_device, fclsh_cluster** out);
+int fclsh_cluster_create_rank(const unsigned char* id, uint32_t world, uint32_t rank, int device,
+                              uint32_t shards_per_rank, fclsh_cluster** out);
+/* build_index over the sharded points (index.hpp:70-71). opt->device is
+ * ignored (each rank builds on its own GPU); opt->id_offset is added to every
+ * id. rows: host memory, or device memory (rows_on_device) readable from every
+ * GPU of this process. */
+int fclsh_cluster_build(fclsh_cluster* cl, const uint64_t* rows, int rows_on_device, int rows_scope, uint64_t n,
+                        uint64_t dims, uint32_t radius, const fclsh_plan* plan, uint64_t rng_seed,
+                        const fclsh_index_options* opt);
+typedef struct {
+    uint32_t world;           /* ranks (GPUs) */
+    uint32_t rank;            /* rank of this handle's first GPU */
+    uint32_t local_ranks;     /* GPUs this process drives */
+    uint32_t shards_per_rank;
+    uint32_t total_shards;
+    int32_t device;           /* this handle's first GPU */
+    int32_t uses_nccl;
+    uint64_t n, dims;
+    uint32_t radius;
+    uint64_t table_count;        /* per shard */
+    uint64_t local_points;       /* points held by this process */
+    uint64_t local_entry_count;  /* postings held by this process */
+    uint64_t local_device_bytes;
+    uint32_t local_bucket_shards; /* shards in the bucket layout (the rest: CSR) */
+    double build_ms;              /* slowest rank's device build time */
+} fclsh_cluster_info;
+int fclsh_cluster_info_get(const fclsh_cluster* cl, fclsh_cluster_info* out);
+/* query_r_nn over the whole cluster, host rows in (read on rank 0 only), host
+ * result out on rank 0 (*out = NULL on the other ranks); free with
+ * fclsh_result_free. Synchronous. */
+int fclsh_cluster_query(fclsh_cluster* cl, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
+                        fclsh_result** out);
+/* Device rows in (on rank 0's GPU), device result on rank 0's GPU valid until
+ * the next batch (all-zero *out on other ranks). `stream` is a stream on this
+ * process's first GPU: the batch starts after the work queued on it and the
+ * results are ordered before what is queued on it afterwards. */
+int fclsh_cluster_query_device(fclsh_cluster* cl, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
+                               void* stream, fclsh_device_result* out);
+void fclsh_cluster_destroy(fclsh_cluster* cl);
 
 /* Number of kernels the library launched on this thread since the last
  * reset (launch accounting for the bench). */

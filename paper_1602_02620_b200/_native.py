@@ -57,6 +57,14 @@ class DeviceResult(C.Structure):
                 ("d_offsets", vp), ("d_collisions", vp), ("d_candidates", vp), ("d_found", vp)]
 
 
+class ClusterInfo(C.Structure):
+    _fields_ = [("world", C.c_uint32), ("rank", C.c_uint32), ("local_ranks", C.c_uint32),
+                ("shards_per_rank", C.c_uint32), ("total_shards", C.c_uint32), ("device", C.c_int32),
+                ("uses_nccl", C.c_int32), ("n", C.c_uint64), ("dims", C.c_uint64), ("radius", C.c_uint32),
+                ("table_count", C.c_uint64), ("local_points", C.c_uint64), ("local_entry_count", C.c_uint64),
+                ("local_device_bytes", C.c_uint64), ("local_bucket_shards", C.c_uint32), ("build_ms", C.c_double)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "fclsh_version": (C.c_char_p, []),
@@ -105,6 +113,16 @@ SIGNATURES = {
                                    C.POINTER(DeviceResult)]),
     "fclsh_distance_histogram": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                            vp, u64p]),
+    "fclsh_cluster_unique_id": (C.c_int, [C.c_char_p]),
+    "fclsh_cluster_create": (C.c_int, [C.POINTER(C.c_int), C.c_uint32, C.c_uint32, C.POINTER(vp)]),
+    "fclsh_cluster_create_rank": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_int, C.c_uint32,
+                                            C.POINTER(vp)]),
+    "fclsh_cluster_build": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, vp, C.c_uint64,
+                                      C.POINTER(IndexOptions)]),
+    "fclsh_cluster_info_get": (C.c_int, [vp, C.POINTER(ClusterInfo)]),
+    "fclsh_cluster_query": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.POINTER(C.POINTER(Result))]),
+    "fclsh_cluster_query_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, C.POINTER(DeviceResult)]),
+    "fclsh_cluster_destroy": (None, [vp]),
     "fclsh_launch_count": (C.c_uint64, []),
     "fclsh_launch_count_reset": (None, []),
     "fclsh_gen_bernoulli": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]),

@@ -15,9 +15,12 @@ counters are summed:
   rank 1's, ..." is already the global ascending id order; the device merge
   (fclsh_merge_shards) places every run without a sort.
 
-The exchange (`exchange`) is backend-agnostic torch.distributed (NCCL over
-NVLink on GPUs; gloo on CPU for the multi-process tests); the merge and the
-per-shard query are the library's CUDA kernels.
+The product path is the library's fclsh_cluster (C++ over NCCL,
+csrc/cluster_host.cpp): `rank_cluster` forms one rank of it under torchrun,
+F.Cluster(devices=[...]) drives several GPUs from one process. `exchange`
+restates the same exchange in torch.distributed terms; the multi-process
+gloo test (tests/test_cluster_gloo.py) checks on CPU the invariants the
+library's merge relies on (shard-additive counters, rank order = id order).
 """
 from __future__ import annotations
 
@@ -72,32 +75,17 @@ def exchange(triples: torch.Tensor, total: int, offsets: torch.Tensor, counters:
     return Exchanged(totals, all_off, all_trip, summed)
 
 
-class ShardedQueryGather:
-    """Per-step gather of a shard's device results to a merged device result.
-
-    Used by bench.py under torchrun: after `ix.query_device(...)` on every
-    rank, `gather(r)` exchanges over NCCL and (on every rank) merges with the
-    device kernel; returns (triples [3, total], offsets [nq+1], counters [3, nq])."""
-
-    def __init__(self, rank: int, world: int, device: torch.device):
-        self.rank, self.world, self.device = rank, world, device
-
-    def gather(self, r: F.DeviceQueryResults, stream=None):
-        dev = self.device
-        nq = r.nq
-        trip = torch.empty((3, max(1, r.total)), dtype=torch.int32, device=dev)
-        off = torch.empty(nq + 1, dtype=torch.int64, device=dev)
-        cnt = torch.empty((3, nq), dtype=torch.int64, device=dev)
-        r.copy_to(trip, off, cnt, device=dev.index or 0, stream=stream)
-        ex = exchange(trip, r.total, off, cnt)
-        total = sum(ex.totals)
-        out = torch.empty((3, max(1, total)), dtype=torch.int32, device=dev)
-        out_off = torch.empty(nq + 1, dtype=torch.int64, device=dev)
-        F.merge_shards(ex.offsets, ex.triples, out, out_off, device=dev.index or 0, stream=stream)
-        return out[:, :total], out_off, ex.counters
-
-
-def broadcast_queries(q: torch.Tensor, src: int = 0) -> torch.Tensor:
-    """The query batch travels from `src` to every rank."""
-    dist.broadcast(q, src=src)
-    return q
+def rank_cluster(shards_per_rank: int = 1, device: int | None = None, group=None) -> F.Cluster:
+    """One rank of a multi-process fclsh_cluster (one process per GPU, e.g.
+    under torchrun): rank 0 draws the NCCL id and torch.distributed (any
+    backend; gloo is enough) carries it to the other ranks, then every rank
+    joins with ncclCommInitRank inside the library."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if device is None:
+        device = torch.cuda.current_device()
+    uid = bytes(F.CLUSTER_ID_BYTES)
+    if world > 1:
+        box = [F.cluster_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = box[0]
+    return F.Cluster(rank=rank, world=world, device=device, uid=uid, shards_per_rank=shards_per_rank)

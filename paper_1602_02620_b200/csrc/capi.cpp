@@ -19,6 +19,7 @@
 #include "dataset.hpp"
 #include "index.cuh"
 #include "scan.hpp"
+#include "cluster.hpp"
 
 namespace fclsh_b200 {
 void gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
@@ -95,9 +96,18 @@ struct fclsh_scan {
     ScanState st;
 };
 
+struct fclsh_cluster {
+    std::unique_ptr<Cluster> cl;
+    DevBuf q_host_rows; // one-shard fast path: device staging for the host call
+};
+
 struct fclsh_index {
     std::unique_ptr<DeviceIndex> ix;
     DevBuf q_host_rows; // device staging for fclsh_query
+    // Calls on one handle serialize (the header's contract): the query entry
+    // points share the index's scratch, result buffers, captured graph and
+    // publish handshake, so concurrent callers take turns here.
+    mutable std::mutex mu;
 };
 
 namespace {
@@ -193,6 +203,104 @@ class PinnedPool {
 PinnedPool& pinned_pool() {
     static PinnedPool* pool = new PinnedPool; // never destroyed: CUDA may be torn down first at exit
     return *pool;
+}
+
+// One pinned block per result: [header | fclsh_result | offsets | collisions
+// | candidates | found | id | distance | query], room for `ids` triples.
+fclsh_result* new_result(uint64_t nq, uint64_t ids, unsigned char** blk_out) {
+    const uint64_t qb = (nq + 1) * 8;
+    const uint64_t tb = std::max<uint64_t>(1, ids) * 4;
+    const size_t bytes = kResultHeader + sizeof(fclsh_result) + 4 * qb + 3 * (tb + 16);
+    unsigned char* blk = static_cast<unsigned char*>(pinned_pool().take(bytes));
+    fclsh_result* r = reinterpret_cast<fclsh_result*>(blk + kResultHeader);
+    std::memset(r, 0, sizeof(fclsh_result));
+    unsigned char* p = blk + kResultHeader + ((sizeof(fclsh_result) + 15) & ~size_t(15));
+    r->nq = nq;
+    r->offsets = reinterpret_cast<uint64_t*>(p); // device layout: offsets | collisions | candidates | found
+    r->collisions = r->offsets + (nq + 1);
+    r->candidates = r->offsets + 2 * (nq + 1);
+    r->found = r->offsets + 3 * (nq + 1);
+    p += 4 * qb;
+    r->id = reinterpret_cast<uint32_t*>(p);
+    r->distance = reinterpret_cast<uint32_t*>(p + ((tb + 15) & ~uint64_t(15)));
+    r->query = reinterpret_cast<uint32_t*>(p + 2 * ((tb + 15) & ~uint64_t(15)));
+    r->time_hash_ms = r->time_probe_ms = r->time_verify_ms = -1;
+    if (blk_out) *blk_out = blk;
+    return r;
+}
+
+// query_r_nn for host rows on one index, host result out (fclsh_query and
+// the one-shard cluster): see fclsh_query in the header.
+fclsh_result* query_host(DeviceIndex& ix, DevBuf& staging, const uint64_t* q_rows, uint64_t nq, uint32_t radius) {
+    FCLSH_CUDA(cudaSetDevice(ix.device));
+    const uint64_t W = ix.row_words;
+    uint64_t* dq = static_cast<uint64_t*>(staging.ensure(std::max<uint64_t>(1, nq) * W * 8));
+    // Rows in pinned (page-locked, device-mapped) host memory are hashed
+    // in place: the hash kernel reads them over PCIe and writes the
+    // device copy the verify reads, so the batch has no separate H2D
+    // copy. Pageable rows: one cudaMemcpyAsync. FCLSH_NO_ZERO_COPY=1: copy always.
+    const uint64_t* hsrc = nullptr;
+    static const bool no_zc = getenv("FCLSH_NO_ZERO_COPY") != nullptr;
+    if (nq && !no_zc) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, q_rows) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer)
+            hsrc = static_cast<const uint64_t*>(pa.devicePointer);
+        cudaGetLastError();
+    }
+    if (nq && !hsrc) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
+    // one pinned block per result: [header | fclsh_result | counters | id | distance | query].
+    // Sized for a guess of the result count, so the counters can be read
+    // back while the batch runs; a larger total takes a larger block.
+    const uint64_t qb = (nq + 1) * 8;
+    cudaStream_t s = ix.stream;
+    unsigned char* blk = nullptr;
+    fclsh_result* r = nullptr;
+    uint64_t cap = 0;
+    auto layout = [&](uint64_t ids) {
+        r = new_result(nq, ids, &blk);
+        cap = ids;
+    };
+    layout(std::max<uint64_t>(1024, ix.last_total + ix.last_total / 4));
+    // the batch kernel writes counters and results straight into the block
+    HostDest dest{PinnedPool::device_view(blk, reinterpret_cast<unsigned long long*>(r->offsets)),
+                  PinnedPool::device_view(blk, r->query), PinnedPool::device_view(blk, r->id),
+                  PinnedPool::device_view(blk, r->distance), cap};
+    QueryOutput o;
+    try {
+        static const bool no_dest = getenv("FCLSH_NO_HOST_DEST") != nullptr; // A/B: D2H copies instead
+        o = query_device(ix, dq, nq, radius, s, dest.counters && !no_dest ? &dest : nullptr, hsrc);
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        pinned_pool().give(blk);
+        throw;
+    }
+    bool copies = false;
+    const bool grew = o.total > cap;
+    if (grew) { // more results than the guess: a larger block
+        pinned_pool().give(blk); // (no copy or kernel targets it any more: the batch was published)
+        layout(o.total);
+    }
+    if (!o.host_counters || grew) {
+        FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
+        copies = true;
+    }
+    r->total = o.total;
+    if (o.total && (!o.host_results || grew)) {
+        FCLSH_CUDA(cudaMemcpyAsync(r->query, o.d_query, o.total * 4, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
+        copies = true;
+    }
+    if (copies) stream_spin_wait(s);
+    r->time_hash_ms = r->time_probe_ms = r->time_verify_ms = -1; // stage timing off: not measured
+    if (ix.stage_timing) {
+        ix.collect_stages();
+        r->time_hash_ms = ix.t_hash_ms;
+        r->time_probe_ms = ix.t_probe_ms;
+        r->time_verify_ms = ix.t_verify_ms;
+    }
+    return r;
 }
 
 } // namespace
@@ -413,90 +521,8 @@ int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t 
         need(ixh, "index");
         need(out, "out");
         if (nq) need(q_rows, "q_rows");
-        DeviceIndex& ix = *ixh->ix;
-        FCLSH_CUDA(cudaSetDevice(ix.device));
-        const uint64_t W = ix.row_words;
-        uint64_t* dq = static_cast<uint64_t*>(ixh->q_host_rows.ensure(std::max<uint64_t>(1, nq) * W * 8));
-        // Rows in pinned (page-locked, device-mapped) host memory are hashed
-        // in place: the hash kernel reads them over PCIe and writes the
-        // device copy the verify reads, so the batch has no separate H2D
-        // copy. Pageable rows: one cudaMemcpyAsync. FCLSH_NO_ZERO_COPY=1: copy always.
-        const uint64_t* hsrc = nullptr;
-        static const bool no_zc = getenv("FCLSH_NO_ZERO_COPY") != nullptr;
-        if (nq && !no_zc) {
-            cudaPointerAttributes pa{};
-            if (cudaPointerGetAttributes(&pa, q_rows) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-                pa.devicePointer)
-                hsrc = static_cast<const uint64_t*>(pa.devicePointer);
-            cudaGetLastError();
-        }
-        if (nq && !hsrc) FCLSH_CUDA(cudaMemcpyAsync(dq, q_rows, nq * W * 8, cudaMemcpyHostToDevice, ix.stream));
-        // one pinned block per result: [header | fclsh_result | counters | id | distance | query].
-        // Sized for a guess of the result count, so the counters can be read
-        // back while the batch runs; a larger total takes a larger block.
-        const uint64_t qb = (nq + 1) * 8;
-        cudaStream_t s = ix.stream;
-        unsigned char* blk = nullptr;
-        fclsh_result* r = nullptr;
-        uint64_t cap = 0;
-        auto layout = [&](uint64_t ids) {
-            const uint64_t tb = std::max<uint64_t>(1, ids) * 4;
-            const size_t bytes = kResultHeader + sizeof(fclsh_result) + 4 * qb + 3 * (tb + 16);
-            blk = static_cast<unsigned char*>(pinned_pool().take(bytes));
-            r = reinterpret_cast<fclsh_result*>(blk + kResultHeader);
-            std::memset(r, 0, sizeof(fclsh_result));
-            unsigned char* p = blk + kResultHeader + ((sizeof(fclsh_result) + 15) & ~size_t(15));
-            r->nq = nq;
-            r->offsets = reinterpret_cast<uint64_t*>(p); // device layout: offsets | collisions | candidates | found
-            r->collisions = r->offsets + (nq + 1);
-            r->candidates = r->offsets + 2 * (nq + 1);
-            r->found = r->offsets + 3 * (nq + 1);
-            p += 4 * qb;
-            r->id = reinterpret_cast<uint32_t*>(p);
-            r->distance = reinterpret_cast<uint32_t*>(p + ((tb + 15) & ~uint64_t(15)));
-            r->query = reinterpret_cast<uint32_t*>(p + 2 * ((tb + 15) & ~uint64_t(15)));
-            cap = ids;
-        };
-        layout(std::max<uint64_t>(1024, ix.last_total + ix.last_total / 4));
-        // the batch kernel writes counters and results straight into the block
-        HostDest dest{PinnedPool::device_view(blk, reinterpret_cast<unsigned long long*>(r->offsets)),
-                      PinnedPool::device_view(blk, r->query), PinnedPool::device_view(blk, r->id),
-                      PinnedPool::device_view(blk, r->distance), cap};
-        QueryOutput o;
-        try {
-            static const bool no_dest = getenv("FCLSH_NO_HOST_DEST") != nullptr; // A/B: D2H copies instead
-            o = query_device(ix, dq, nq, radius, s, {}, dest.counters && !no_dest ? &dest : nullptr, hsrc);
-        } catch (...) {
-            cudaStreamSynchronize(s);
-            pinned_pool().give(blk);
-            throw;
-        }
-        bool copies = false;
-        const bool grew = o.total > cap;
-        if (grew) { // more results than the guess: a larger block
-            pinned_pool().give(blk); // (no copy or kernel targets it any more: the batch was published)
-            layout(o.total);
-        }
-        if (!o.host_counters || grew) {
-            FCLSH_CUDA(cudaMemcpyAsync(r->offsets, o.d_offsets, 4 * qb, cudaMemcpyDeviceToHost, s));
-            copies = true;
-        }
-        r->total = o.total;
-        if (o.total && (!o.host_results || grew)) {
-            FCLSH_CUDA(cudaMemcpyAsync(r->query, o.d_query, o.total * 4, cudaMemcpyDeviceToHost, s));
-            FCLSH_CUDA(cudaMemcpyAsync(r->id, o.d_id, o.total * 4, cudaMemcpyDeviceToHost, s));
-            FCLSH_CUDA(cudaMemcpyAsync(r->distance, o.d_dist, o.total * 4, cudaMemcpyDeviceToHost, s));
-            copies = true;
-        }
-        if (copies) stream_spin_wait(s);
-        r->time_hash_ms = r->time_probe_ms = r->time_verify_ms = -1; // stage timing off: not measured
-        if (ix.stage_timing) {
-            ix.collect_stages();
-            r->time_hash_ms = ix.t_hash_ms;
-            r->time_probe_ms = ix.t_probe_ms;
-            r->time_verify_ms = ix.t_verify_ms;
-        }
-        *out = r;
+        std::lock_guard<std::mutex> lk(ixh->mu);
+        *out = query_host(*ixh->ix, ixh->q_host_rows, q_rows, nq, radius);
     });
 }
 
@@ -514,6 +540,7 @@ int fclsh_query_c_r_nn(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, ui
             need(counters, "counters");
             need(best, "best");
         }
+        std::lock_guard<std::mutex> lk(ixh->mu);
         DeviceIndex& ix = *ixh->ix;
         FCLSH_CUDA(cudaSetDevice(ix.device));
         const uint64_t W = ix.row_words;
@@ -537,6 +564,7 @@ int fclsh_query_device(fclsh_index* ixh, const uint64_t* d_q_rows, uint64_t nq, 
         need(ixh, "index");
         need(out, "out");
         if (nq) need(d_q_rows, "d_q_rows");
+        std::lock_guard<std::mutex> lk(ixh->mu);
         QueryOutput o = query_device(*ixh->ix, d_q_rows, nq, radius, static_cast<cudaStream_t>(stream));
         out->nq = nq;
         out->total = o.total;
@@ -590,6 +618,7 @@ int fclsh_query_stage_ms(const fclsh_index* ix, double* ms, int n) {
         return -FCLSH_ERR_USAGE;
     }
     const int k = std::min(n, DeviceIndex::kStages);
+    std::lock_guard<std::mutex> lk(ix->mu);
     const int rc = guarded([&] { ix->ix->collect_stages(); });
     if (rc != FCLSH_OK) return -rc;
     for (int i = 0; i < k; ++i) ms[i] = ix->ix->stage_ms[i];
@@ -601,6 +630,7 @@ int fclsh_query_stage_timing(fclsh_index* ix, int enable) {
         g_err = "fclsh_query_stage_timing: NULL index";
         return FCLSH_ERR_USAGE;
     }
+    std::lock_guard<std::mutex> lk(ix->mu);
     ix->ix->stage_timing = enable != 0;
     return FCLSH_OK;
 }
@@ -610,6 +640,7 @@ int fclsh_query_batch_ms(const fclsh_index* ix, double* ms) {
         g_err = "fclsh_query_batch_ms: NULL argument";
         return FCLSH_ERR_USAGE;
     }
+    std::lock_guard<std::mutex> lk(ix->mu);
     return guarded([&] {
         ix->ix->collect_stages();
         *ms = ix->ix->batch_ms;
@@ -621,6 +652,7 @@ int fclsh_query_path_counts(const fclsh_index* ix, uint64_t* dense, uint64_t* ge
         g_err = "fclsh_query_path_counts: NULL index";
         return -FCLSH_ERR_USAGE;
     }
+    std::lock_guard<std::mutex> lk(ix->mu);
     if (dense) *dense = ix->ix->last_dense;
     if (general) *general = ix->ix->last_overflow;
     return 0;
@@ -726,6 +758,161 @@ int fclsh_distance_histogram(fclsh_scan* sc, const uint64_t* d_rows, uint64_t n,
         distance_histogram_device(sc->st, a, sample_per_query, seed, counts, static_cast<cudaStream_t>(stream));
     });
 }
+
+/* ------------------------------------------------------------- cluster -- */
+
+int fclsh_cluster_unique_id(unsigned char* id) {
+    return guarded([&] {
+        need(id, "id");
+        cluster_unique_id(id);
+    });
+}
+
+int fclsh_cluster_create(const int* devices, uint32_t ndev, uint32_t shards_per_device, fclsh_cluster** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (ndev) need(devices, "devices");
+        auto h = std::make_unique<fclsh_cluster>();
+        h->cl = cluster_create(devices, ndev, shards_per_device);
+        *out = h.release();
+    });
+}
+
+int fclsh_cluster_create_rank(const unsigned char* id, uint32_t world, uint32_t rank, int device,
+                              uint32_t shards_per_rank, fclsh_cluster** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (world > 1) need(id, "id");
+        static const unsigned char zero[FCLSH_CLUSTER_ID_BYTES] = {};
+        auto h = std::make_unique<fclsh_cluster>();
+        h->cl = cluster_create_rank(id ? id : zero, world, rank, device, shards_per_rank);
+        *out = h.release();
+    });
+}
+
+int fclsh_cluster_build(fclsh_cluster* ch, const uint64_t* rows, int rows_on_device, int rows_scope, uint64_t n,
+                        uint64_t dims, uint32_t radius, const fclsh_plan* plan, uint64_t rng_seed,
+                        const fclsh_index_options* opt) {
+    return guarded([&] {
+        need(ch, "cluster");
+        need(plan, "plan");
+        if (n) need(rows, "rows");
+        if (rows_scope != FCLSH_ROWS_GLOBAL && rows_scope != FCLSH_ROWS_LOCAL)
+            throw UsageError("cluster: unknown rows scope");
+        if (dims != plan->p.dims) throw UsageError("index: dataset width does not match the plan");
+        if (n == 0) throw UsageError("index: empty dataset");
+        fclsh_index_options o;
+        fclsh_index_options_default(&o);
+        if (opt) o = *opt;
+        IndexBuildOptions bo;
+        bo.prime = o.prime;
+        bo.include_zero_column = o.include_zero_column != 0;
+        bo.table_budget = o.table_budget;
+        bo.device = o.device;
+        bo.id_offset = o.id_offset;
+        bo.directory_bits = o.directory_bits;
+        bo.layout = o.layout;
+        cluster_build(*ch->cl, rows, rows_on_device != 0, rows_scope == FCLSH_ROWS_GLOBAL, n, dims, radius, plan->p,
+                      rng_seed, bo);
+    });
+}
+
+int fclsh_cluster_info_get(const fclsh_cluster* ch, fclsh_cluster_info* out) {
+    return guarded([&] {
+        need(ch, "cluster");
+        need(out, "out");
+        const Cluster& c = *ch->cl;
+        std::memset(out, 0, sizeof(*out));
+        out->world = c.world;
+        out->rank = c.members.front()->rank;
+        out->local_ranks = uint32_t(c.members.size());
+        out->shards_per_rank = c.shards_per_rank;
+        out->total_shards = c.total_shards();
+        out->device = c.members.front()->device;
+        out->uses_nccl = c.use_nccl ? 1 : 0;
+        out->n = c.n;
+        out->dims = c.dims;
+        out->radius = c.radius;
+        out->build_ms = c.build_ms;
+        for (auto& m : c.members)
+            for (auto& sh : m->shards) {
+                out->table_count = sh.ix->tables;
+                out->local_entry_count += sh.ix->tables * sh.ix->n;
+                out->local_device_bytes += sh.ix->device_bytes();
+                out->local_points += sh.ix->n;
+                if (sh.ix->layout == kLayoutBuckets) ++out->local_bucket_shards;
+            }
+    });
+}
+
+int fclsh_cluster_query(fclsh_cluster* ch, const uint64_t* q_rows, uint64_t nq, uint32_t radius,
+                        fclsh_result** out) {
+    return guarded([&] {
+        need(ch, "cluster");
+        need(out, "out");
+        *out = nullptr;
+        Cluster& c = *ch->cl;
+        ClusterMember* R = c.root();
+        if (nq && R) need(q_rows, "q_rows");
+        if (c.world == 1 && c.shards_per_rank == 1 && c.built) {
+            // one shard in all: the index's own host path (zero-copy rows,
+            // results written into the host block by the batch)
+            std::lock_guard<std::mutex> lk(c.mu);
+            *out = query_host(*R->shards[0].ix, ch->q_host_rows, q_rows, nq, radius);
+            return;
+        }
+        const ClusterResult res = cluster_query(c, q_rows, false, nq, radius, nullptr);
+        if (!res.root) return; // this process holds no result (rank != 0)
+        FCLSH_CUDA(cudaSetDevice(res.device));
+        unsigned char* blk = nullptr;
+        fclsh_result* r = new_result(nq, res.total, &blk);
+        cudaStream_t s = res.stream;
+        try {
+            FCLSH_CUDA(cudaMemcpyAsync(r->offsets, res.off, (nq + 1) * 8, cudaMemcpyDeviceToHost, s));
+            if (nq) {
+                FCLSH_CUDA(cudaMemcpyAsync(r->collisions, res.coll, nq * 8, cudaMemcpyDeviceToHost, s));
+                FCLSH_CUDA(cudaMemcpyAsync(r->candidates, res.cand, nq * 8, cudaMemcpyDeviceToHost, s));
+                FCLSH_CUDA(cudaMemcpyAsync(r->found, res.found, nq * 8, cudaMemcpyDeviceToHost, s));
+            }
+            if (res.total) {
+                FCLSH_CUDA(cudaMemcpyAsync(r->query, res.q, res.total * 4, cudaMemcpyDeviceToHost, s));
+                FCLSH_CUDA(cudaMemcpyAsync(r->id, res.id, res.total * 4, cudaMemcpyDeviceToHost, s));
+                FCLSH_CUDA(cudaMemcpyAsync(r->distance, res.dist, res.total * 4, cudaMemcpyDeviceToHost, s));
+            }
+            stream_spin_wait(s);
+        } catch (...) {
+            cudaStreamSynchronize(s);
+            pinned_pool().give(blk);
+            throw;
+        }
+        r->total = res.total;
+        *out = r;
+    });
+}
+
+int fclsh_cluster_query_device(fclsh_cluster* ch, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
+                               void* stream, fclsh_device_result* out) {
+    return guarded([&] {
+        need(ch, "cluster");
+        need(out, "out");
+        std::memset(out, 0, sizeof(*out));
+        Cluster& c = *ch->cl;
+        if (nq && c.root()) need(d_q_rows, "d_q_rows");
+        const ClusterResult res = cluster_query(c, d_q_rows, true, nq, radius, static_cast<cudaStream_t>(stream));
+        if (!res.root) return;
+        out->nq = nq;
+        out->total = res.total;
+        out->d_query = const_cast<uint32_t*>(res.q);
+        out->d_id = const_cast<uint32_t*>(res.id);
+        out->d_distance = const_cast<uint32_t*>(res.dist);
+        out->d_offsets = reinterpret_cast<uint64_t*>(const_cast<unsigned long long*>(res.off));
+        out->d_collisions = reinterpret_cast<uint64_t*>(const_cast<unsigned long long*>(res.coll));
+        out->d_candidates = reinterpret_cast<uint64_t*>(const_cast<unsigned long long*>(res.cand));
+        out->d_found = reinterpret_cast<uint64_t*>(const_cast<unsigned long long*>(res.found));
+    });
+}
+
+void fclsh_cluster_destroy(fclsh_cluster* c) { delete c; }
 
 uint64_t fclsh_launch_count(void) { return launch_counter(); }
 void fclsh_launch_count_reset(void) { launch_counter() = 0; }

@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstring>
 #include <cmath>
 #include <cstdio>
@@ -147,10 +148,10 @@ struct Tables {
     uint64_t n;                // postings per table
     uint64_t cells;            // CSR cells per table
     uint64_t nbuckets;         // buckets per table
-    uint32_t shift;            // CSR: cell = key >> shift; buckets: home = key >> shift
+    uint32_t shift;            // CSR: cell = (key * kscale) >> shift; buckets: home bucket, the same
+    uint64_t kscale;           // floor(2^64 / P): key * kscale is the key's 64-bit fraction of [0, P)
     const uint32_t* filter;    // buckets: per-table key filter (null: none)
     uint32_t filter_words;     // filter words (32 bits) per table
-    uint32_t filter_shift;     // 64 - key bits: key << filter_shift is a 64-bit fraction
 };
 
 // Key filter of the bucket tables: M = 32 * filter_words bits per table
@@ -177,13 +178,23 @@ __device__ __forceinline__ uint32_t ld_filter(const uint32_t* a, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
     return v;
 }
-__device__ __forceinline__ uint32_t filter_bit(uint64_t key, uint32_t words, uint32_t shift) {
-    return uint32_t(__umul64hi(key << shift, uint64_t(words) * 32));
+__device__ __forceinline__ uint32_t filter_bit(uint64_t key, uint32_t words, uint64_t kscale) {
+    return uint32_t(__umul64hi(key * kscale, uint64_t(words) * 32));
+}
+// Home bucket (CSR: cell) of a key: the top bits of its 64-bit fraction of
+// [0, P), so keys spread evenly over the buckets for any prime (a plain
+// key >> s would leave part of the table empty when P is far below 2^kbits)
+__host__ __device__ __forceinline__ uint64_t home_of(uint64_t key, uint64_t kscale, uint32_t shift) {
+    return (key * kscale) >> shift;
+}
+template <typename T>
+__device__ __forceinline__ uint64_t home_of(uint64_t key, const Tables<T>& tb) {
+    return home_of(key, tb.kscale, tb.shift);
 }
 // filter test of (table t, key): one L2 word read (evict_last policy)
 template <typename T>
 __device__ __forceinline__ bool filter_pass(const Tables<T>& tb, uint32_t t, uint64_t key, uint64_t pol) {
-    const uint32_t r = filter_bit(key, tb.filter_words, tb.filter_shift);
+    const uint32_t r = filter_bit(key, tb.filter_words, tb.kscale);
     return (ld_filter(tb.filter + uint64_t(t) * tb.filter_words + (r >> 5), pol) >> (r & 31)) & 1u;
 }
 
@@ -209,7 +220,7 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
     using E = typename T::E;
     uint32_t cnt = 0;
     if constexpr (LAYOUT == kLayoutCsr) {
-        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key >> tb.shift);
+        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key, tb);
         uint32_t a = __ldg(d);
         const uint32_t e = __ldg(d + 1);
         const E* et = tb.data + uint64_t(t) * tb.n;
@@ -220,7 +231,7 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
             ++cnt;
         }
     } else {
-        uint64_t b = key >> tb.shift;
+        uint64_t b = home_of(key, tb);
         const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
         for (;;) {
             E s[kSlots];
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(256) k_keys_table_major(const K* __restrict__ 
 template <typename T>
 __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t t0, uint32_t tg,
                                 uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets,
-                                uint32_t* __restrict__ filter, uint32_t filter_words, uint32_t filter_shift) {
+                                uint32_t* __restrict__ filter, uint32_t filter_words, uint64_t kscale) {
     // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
     // their postings are inserted (all 511 at once thrash it: 43 GB of DRAM
     // reads for 8.6 GB of tables)
@@ -283,10 +294,10 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
         const uint64_t key = keys[uint64_t(t) * n + i];
         const typename T::E e = T::make(key, uint32_t(i));
         if (filter) {
-            const uint32_t r = filter_bit(key, filter_words, filter_shift);
+            const uint32_t r = filter_bit(key, filter_words, kscale);
             atomicOr(filter + uint64_t(t) * filter_words + (r >> 5), 1u << (r & 31));
         }
-        uint64_t b = key >> shift;
+        uint64_t b = home_of(key, kscale, shift);
         for (;;) {
             typename T::E* bp = bt + b * kSlots;
             bool done = false;
@@ -301,12 +312,12 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
 // CSR build over tables [t0, t0+c) of one part; keys point-major (stride L).
 template <typename K>
 __global__ void k_hist(const K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0, uint32_t c, uint32_t shift,
-                       uint64_t cells, uint32_t* __restrict__ cnt) {
+                       uint64_t kscale, uint64_t cells, uint32_t* __restrict__ cnt) {
     const uint64_t total = n * c;
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = x / c;
         const uint32_t t = uint32_t(x % c);
-        atomicAdd(cnt + uint64_t(t) * (cells + 1) + (uint64_t(keys[i * L + t0 + t]) >> shift), 1u);
+        atomicAdd(cnt + uint64_t(t) * (cells + 1) + home_of(uint64_t(keys[i * L + t0 + t]), kscale, shift), 1u);
     }
 }
 
@@ -348,13 +359,13 @@ __global__ void __launch_bounds__(1024) k_scan_cells(const uint32_t* __restrict_
 
 template <typename T, typename K>
 __global__ void k_scatter(const K* __restrict__ keys, uint64_t n, uint32_t L, uint32_t t0, uint32_t c, uint32_t shift,
-                          uint64_t cells, uint32_t* __restrict__ cursor, typename T::E* __restrict__ entries) {
+                          uint64_t kscale, uint64_t cells, uint32_t* __restrict__ cursor, typename T::E* __restrict__ entries) {
     const uint64_t total = n * c;
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = x / c;
         const uint32_t t = uint32_t(x % c);
         const uint64_t key = keys[i * L + t0 + t];
-        const uint32_t pos = atomicAdd(cursor + uint64_t(t) * (cells + 1) + (key >> shift), 1u);
+        const uint32_t pos = atomicAdd(cursor + uint64_t(t) * (cells + 1) + home_of(key, kscale, shift), 1u);
         entries[uint64_t(t) * n + pos] = T::make(key, uint32_t(i));
     }
 }
@@ -544,7 +555,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
                 for (int u = 0; u < U; ++u) { // U directory lookups in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t < tables) {
-                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key[u] >> tb.shift);
+                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[u], tb);
                         s[u] = __ldg(d);
                         e[u] = __ldg(d + 1);
                     } else {
@@ -564,7 +575,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
                 for (int u = 0; u < U; ++u) { // U home buckets in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t < tables)
-                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
+                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + home_of(key[u], tb)) * kSlots, sl[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -574,7 +585,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
                     for (int j = 0; j < kSlots; ++j)
                         if (!T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u]) push(T::id(sl[u][j]));
                     if (!T::empty(sl[u][kSlots - 1])) // the run continues into the next bucket (~3 %)
-                        probe_run<T>(tb, t, ((key[u] >> tb.shift) + 1) & (tb.nbuckets - 1), key[u], push);
+                        probe_run<T>(tb, t, (home_of(key[u], tb) + 1) & (tb.nbuckets - 1), key[u], push);
                 }
             }
             __syncwarp();
@@ -730,7 +741,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
                 for (int u = 0; u < U; ++u) { // U directory lookups in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (t < tables) {
-                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + (key[u] >> tb.shift);
+                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[u], tb);
                         s[u] = __ldg(d);
                         e[u] = __ldg(d + 1);
                     } else {
@@ -763,7 +774,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
                 for (int u = 0; u < U; ++u) { // U home buckets in flight
                     const uint32_t t = t0 + u * 32 + lane;
                     if (pass[u]) {
-                        load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u],
+                        load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + home_of(key[u], tb)) * kSlots, sl[u],
                                           bpol);
                     } else {
 #pragma unroll
@@ -778,7 +789,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
                         offer(live && !T::empty(sl[u][j]) && T::key(sl[u][j]) == key[u], T::id(sl[u][j]));
                     // the run continues into the next bucket (~3 %)
                     bool cont = live && !T::empty(sl[u][kSlots - 1]);
-                    uint64_t b = (key[u] >> tb.shift) + 1;
+                    uint64_t b = home_of(key[u], tb) + 1;
                     const E* base = tb.data + uint64_t(t0 + u * 32 + lane) * tb.nbuckets * kSlots;
                     while (__any_sync(kAll, cont)) {
                         E x[kSlots];
@@ -950,7 +961,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
                 for (int u = 0; u < kDenseU; ++u) {
                     const uint32_t t = t0 + u * nt;
                     if (pass[u]) {
-                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + (key[u] >> tb.shift)) * kSlots, sl[u]);
+                        load_bucket(tb.data + (uint64_t(t) * tb.nbuckets + home_of(key[u], tb)) * kSlots, sl[u]);
                     } else {
 #pragma unroll
                         for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
@@ -966,7 +977,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
                         }
                     if (T::empty(sl[u][kSlots - 1])) continue;
                     const E* base = tb.data + uint64_t(t0 + u * nt) * tb.nbuckets * kSlots;
-                    uint64_t b = (key[u] >> tb.shift) + 1;
+                    uint64_t b = home_of(key[u], tb) + 1;
                     for (bool cont = true; cont; b += kDenseRun) {
                         E x[kDenseRun][kSlots];
 #pragma unroll
@@ -1082,18 +1093,35 @@ struct NarrowIdOrder {
 // every table's postings, scans the counts to find the table where the
 // budget runs out, then inserts the ids of the tables before it plus the
 // smallest ids of that table into a shared set, and verifies the set.
-template <typename T, int LAYOUT, int HS, int KCAP>
+template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict__ qkeys, uint64_t nq,
                                                  uint32_t tables, const Tables<T> tb,
                                                  const uint64_t* __restrict__ rows,
                                                  const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
                                                  uint64_t budget, unsigned long long* __restrict__ counters,
                                                  uint32_t* __restrict__ best, unsigned int* __restrict__ qnext,
-                                                 unsigned int* __restrict__ err) {
+                                                 unsigned int* __restrict__ err, uint32_t hs_log, uint32_t kcap,
+                                                 uint32_t* __restrict__ gscratch, uint64_t id_offset) {
+    // the id set (2^hs_log slots) and the cut table's ids (kcap) live in
+    // shared memory, or, for budgets beyond it, in this CTA's slice of a
+    // global scratch [set | cut ids | slot list of the inserted ids]
     extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t* set = reinterpret_cast<uint32_t*>(smem);        // HS ids
-    uint32_t* kbuf = set + HS;                                // KCAP ids of the table the budget cuts
-    uint32_t* cnt = kbuf + KCAP;                              // tables: postings per table, then their prefix
+    const uint32_t HS = 1u << hs_log;
+    const uint32_t tpad = (tables + 3) & ~3u;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem); // tables: postings per table, then their prefix
+    uint32_t* set;
+    uint32_t* kbuf;
+    uint32_t* slots = nullptr; // global mode: the slot of every inserted id (verify walks these, not the set)
+    if (gscratch) {
+        uint32_t* g = gscratch + uint64_t(blockIdx.x) * (uint64_t(tpad) + HS + kcap + HS / 2);
+        cnt = g;
+        set = g + tpad;
+        kbuf = set + HS;
+        slots = kbuf + kcap;
+    } else {
+        set = cnt + tpad;
+        kbuf = set + HS;
+    }
     __shared__ unsigned long long wsum[16], best_s;
     __shared__ unsigned int cand_s, found_s, cut_s, cutr_s, kn_s, next_s, bad_s;
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
@@ -1146,14 +1174,15 @@ __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict
         const unsigned long long coll = total < budget ? total : budget;
         // C: ids of the tables walked in full, and of the cut table's smallest ids
         auto insert = [&](uint32_t id) {
-            uint32_t h = (id * 0x9E3779B1u) >> (32 - __builtin_ctz(HS));
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - hs_log);
             for (;;) {
                 const uint32_t old = atomicCAS(set + h, kEmpty, id);
                 if (old == id) return;
                 if (old == kEmpty) break;
                 h = (h + 1) & (HS - 1);
             }
-            atomicAdd(&cand_s, 1u);
+            const uint32_t k = atomicAdd(&cand_s, 1u);
+            if (slots) slots[k] = h;
         };
         for (uint32_t t = tid; t < tables; t += nt) {
             const bool full = t < cut && cnt[t] < budget;
@@ -1162,14 +1191,14 @@ __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict
             } else if (t == cut) {
                 probe_one<T, LAYOUT>(tb, t, uint64_t(qk[t]), [&](uint32_t id) {
                     const uint32_t p = atomicAdd(&kn_s, 1u);
-                    if (p < KCAP) kbuf[p] = id;
+                    if (p < kcap) kbuf[p] = id;
                     else bad_s = 1;
                 });
             }
         }
         __syncthreads();
         if (cut < tables) { // the cut table: ascending ids, the first cutr of them
-            const uint32_t m = min(kn_s, uint32_t(KCAP));
+            const uint32_t m = min(kn_s, kcap);
             uint32_t P = 1;
             while (P < m) P <<= 1;
             for (uint32_t i = m + tid; i < P; i += nt) kbuf[i] = kEmpty;
@@ -1182,10 +1211,12 @@ __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict
         const uint64_t* qr = qrows + q * words;
         uint32_t fnd = 0;
         unsigned long long bst = ~0ull;
-        for (uint32_t i = tid; i < HS; i += nt) {
-            const uint32_t id = set[i];
+        const uint32_t walk = slots ? cand_s : HS; // global mode: the listed slots only
+        for (uint32_t i = tid; i < walk; i += nt) {
+            const uint32_t sl = slots ? slots[i] : i;
+            const uint32_t id = set[sl];
             if (id == kEmpty) continue;
-            set[i] = kEmpty;
+            set[sl] = kEmpty;
             const uint64_t* r = rows + uint64_t(id) * words;
             uint32_t d = 0;
             for (uint32_t w = 0; w < words; ++w) d += __popcll(__ldg(r + w) ^ __ldg(qr + w));
@@ -1200,7 +1231,8 @@ __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict
             counters[3 * q] = coll;
             counters[3 * q + 1] = cand_s;
             counters[3 * q + 2] = found_s;
-            best[2 * q] = best_s == ~0ull ? kEmpty : uint32_t(best_s);
+            // shard ids: reported with the index's id offset, like query_r_nn's
+            best[2 * q] = best_s == ~0ull ? kEmpty : uint32_t(uint32_t(best_s) + id_offset);
             best[2 * q + 1] = best_s == ~0ull ? kEmpty : uint32_t(best_s >> 32);
             if (bad_s) atomicAdd(err, 1u);
         }
@@ -1520,7 +1552,7 @@ Tables<T> view(const DeviceIndex& ix) {
     tb.shift = ix.key_shift;
     tb.filter = ix.filter_words ? ix.filter.as<uint32_t>() : nullptr;
     tb.filter_words = ix.filter_words;
-    tb.filter_shift = ix.filter_shift;
+    tb.kscale = ix.key_scale;
     return tb;
 }
 
@@ -1538,11 +1570,11 @@ void build_csr_tables(DeviceIndex& ix, const void* keys, uint32_t L, uint32_t t0
     auto* entries = static_cast<typename T::E*>(ix.entries.p) + uint64_t(tg0) * n;
     FCLSH_CUDA(cudaMemsetAsync(cnt, 0, cbytes, s));
     const unsigned g = grid_for(n * count, ix.device, 256, 8);
-    k_hist<K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, cells, cnt);
+    k_hist<K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, ix.key_scale, cells, cnt);
     FCLSH_LAUNCHED();
     k_scan_cells<<<count, 1024, 0, s>>>(cnt, cells, dir, cur);
     FCLSH_LAUNCHED();
-    k_scatter<T, K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, cells, cur, entries);
+    k_scatter<T, K><<<g, 256, 0, s>>>(static_cast<const K*>(keys), n, L, t0, count, ix.key_shift, ix.key_scale, cells, cur, entries);
     FCLSH_LAUNCHED();
     // cells longer than kSmallCell: at most n / (kSmallCell+1) per table
     const uint64_t max_big = uint64_t(count) * (n / (kSmallCell + 1) + 1);
@@ -1595,7 +1627,7 @@ void build_all(DeviceIndex& ix) {
                 k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(ktm, n, t0, c, ix.key_shift,
                                                                                       ix.nbuckets, bk, fl,
                                                                                       ix.filter_words,
-                                                                                      ix.filter_shift);
+                                                                                      ix.key_scale);
                 FCLSH_LAUNCHED();
             }
         } else {
@@ -1686,42 +1718,74 @@ void wait_published(const unsigned long long* h_pub, unsigned long long seq, cud
     std::atomic_thread_fence(std::memory_order_acquire);
 }
 
-template <typename T, int LAYOUT>
-QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s,
-                       const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest,
-                       const uint64_t* hash_src) {
+// Every buffer a batch of nq queries touches, sized (grow-only) before any
+// launch so that a captured graph never needs a reallocation. Called again by
+// query_finish_impl: the same sizes return the same pointers.
+template <typename T>
+struct QueryBufs {
     using K = typename T::K;
-    QueryOutput out;
-    out.nq = nq;
+    K* qkeys;
+    unsigned long long *counters, *res_off, *coll_q, *cand_q, *found_q, *src_pos, *res_cursor, *tile_sum;
+    uint32_t *tmp_id, *tmp_dist, *ovf, *ovf2, *cta_id, *cta_dist, *oq, *oi, *od;
+    unsigned int* ovf_cnt;
+    uint64_t ntiles, cta_cap, out_cap;
+    size_t scan_bytes;
+    void* scan_tmp;
+};
+constexpr uint32_t kSlotCap = 32; // results per query in the warp kernel's slots
+
+template <typename T>
+QueryBufs<T> query_bufs(DeviceIndex& ix, uint64_t nq, cudaStream_t s) {
+    using K = typename T::K;
+    QueryBufs<T> b;
     const uint64_t T_ = ix.tables;
-    const bool big = T_ > 600;
-    const uint32_t slot_cap = 32; // results per query in the warp kernel's slots
-    K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
+    b.qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
     // per-query outputs in one block [offsets | collisions | candidates | found],
     // nq + 1 words each, so a host caller reads them back with one copy
-    auto* counters = static_cast<unsigned long long*>(ix.counters.ensure(4 * (nq + 1) * 8));
-    auto* res_off = counters;
-    auto* coll_q = counters + (nq + 1);
-    auto* cand_q = counters + 2 * (nq + 1);
-    auto* found_q = counters + 3 * (nq + 1);
-    auto* src_pos = static_cast<unsigned long long*>(ix.src_pos.ensure((nq + 1) * 8));
-    uint32_t* tmp_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
-    uint32_t* tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * slot_cap) * 4));
-    uint32_t* ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
-    uint32_t* ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
+    b.counters = static_cast<unsigned long long*>(ix.counters.ensure(4 * (nq + 1) * 8));
+    b.res_off = b.counters;
+    b.coll_q = b.counters + (nq + 1);
+    b.cand_q = b.counters + 2 * (nq + 1);
+    b.found_q = b.counters + 3 * (nq + 1);
+    b.src_pos = static_cast<unsigned long long*>(ix.src_pos.ensure((nq + 1) * 8));
+    b.tmp_id = static_cast<uint32_t*>(ix.res_tmp_id.ensure(std::max<uint64_t>(1, nq * kSlotCap) * 4));
+    b.tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * kSlotCap) * 4));
+    b.ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
+    b.ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
     // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
     // query to hand out in the warp / CTA kernel, [8]: k_scan_compact CTAs
     // done; from byte 64 the results per tile of 1024 queries, added by the
     // query kernels for k_scan_compact. One memset clears all of it.
-    const uint64_t ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
-    auto* ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(64 + std::max<uint64_t>(1, ntiles) * 8));
-    auto* res_cursor = reinterpret_cast<unsigned long long*>(ovf_cnt + 2);
-    auto* tile_sum = reinterpret_cast<unsigned long long*>(ovf_cnt + 16);
+    b.ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
+    b.ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(64 + std::max<uint64_t>(1, b.ntiles) * 8));
+    b.res_cursor = reinterpret_cast<unsigned long long*>(b.ovf_cnt + 2);
+    b.tile_sum = reinterpret_cast<unsigned long long*>(b.ovf_cnt + 16);
     // CTA-kernel result region; queries that do not fit go on to the general path
-    const uint64_t cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * slot_cap);
-    uint32_t* cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(cta_cap * 4));
-    uint32_t* cta_dist = static_cast<uint32_t*>(ix.res_cta_dist.ensure(cta_cap * 4));
+    b.cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * kSlotCap);
+    b.cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(b.cta_cap * 4));
+    b.cta_dist = static_cast<uint32_t*>(ix.res_cta_dist.ensure(b.cta_cap * 4));
+    b.out_cap = std::max<uint64_t>(1, nq * kSlotCap + b.cta_cap); // CTA results <= cta_cap
+    b.oq = static_cast<uint32_t*>(ix.out_q.ensure(b.out_cap * 4));
+    b.oi = static_cast<uint32_t*>(ix.out_id.ensure(b.out_cap * 4));
+    b.od = static_cast<uint32_t*>(ix.out_dist.ensure(b.out_cap * 4));
+    b.scan_bytes = 0;
+    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b.scan_bytes, b.found_q, b.res_off, nq + 1, s));
+    b.scan_tmp = ix.cub_tmp.ensure(b.scan_bytes);
+    return b;
+}
+
+// Phase 1 of a batch: enqueue the common path (replayed as a CUDA graph once
+// the shape repeats) on the index's stream and return without waiting.
+template <typename T, int LAYOUT>
+void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t s,
+                        const HostDest* dest, const uint64_t* hash_src) {
+    using K = typename T::K;
+    const uint64_t T_ = ix.tables;
+    const bool big = T_ > 600;
+    const uint32_t slot_cap = kSlotCap;
+    const QueryBufs<T> b = query_bufs<T>(ix, nq, s);
+    K* const qkeys = b.qkeys;
     for (auto& e : ix.ev)
         if (!e) FCLSH_CUDA(cudaEventCreate(&e));
     // CTAs for the hand-over: most batches hand nothing over, and an idle
@@ -1731,15 +1795,6 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
     // Many tables (cfg4: 1022): CTA per query for every query (measured
     // faster than the warp kernel there, clustered or sharded).
     const bool dense_all = big;
-    // Everything the common path touches is sized here, before any launch, so
-    // a captured graph never needs a reallocation.
-    uint64_t out_cap = std::max<uint64_t>(1, nq * slot_cap + cta_cap); // CTA results <= cta_cap
-    uint32_t* oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
-    uint32_t* oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
-    uint32_t* od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
-    size_t scan_bytes = 0;
-    FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, found_q, res_off, nq + 1, s));
-    void* scan_tmp = ix.cub_tmp.ensure(scan_bytes);
     if (!ix.h_pub) {
         // [0] total, [1] [2] overflow counts, [3] sequence, [4..8] HostDest
         FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 128, cudaHostAllocMapped));
@@ -1752,18 +1807,6 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         ix.pub_seq = 0;
     }
     auto* d_seq = ix.pub_seq_dev.as<unsigned long long>();
-    uint32_t* tmp2_id = tmp_id;
-    uint32_t* tmp2_dist = tmp_dist;
-    auto scan_found = [&](void* tmp, size_t bytes) {
-        FCLSH_CUDA(cudaMemsetAsync(found_q + nq, 0, 8, s));
-        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, found_q, res_off, nq + 1, s));
-    };
-    auto compact = [&](unsigned long long* pub) {
-        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(nq, src_pos, res_off, tmp_id, tmp_dist, nq * slot_cap,
-                                                               cta_id, cta_dist, cta_cap, tmp2_id, tmp2_dist,
-                                                               ix.id_offset, oq, oi, od, pub, d_seq, ovf_cnt);
-        FCLSH_LAUNCHED();
-    };
     // The common path: S1 hash (point-major key[q*T + t]), S2+S3 fused warp
     // per query, the CTA-per-query kernel for what it hands over (count read
     // on the device) or for every query, found scan, compaction + publish.
@@ -1789,7 +1832,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         // the destination descriptor (read at run time from pinned memory)
         FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
         FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
-        FCLSH_CUDA(cudaMemsetAsync(ovf_cnt, 0, 64 + ntiles * 8, ix.side));
+        FCLSH_CUDA(cudaMemsetAsync(b.ovf_cnt, 0, 64 + b.ntiles * 8, ix.side));
         FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
                                    ix.side));
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
@@ -1799,29 +1842,26 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         rec(1);
         FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
-            launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                                          tmp_id, tmp_dist, ovf, ovf_cnt, ovf_cnt + 4, tile_sum, d_desc, s);
+            launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
+                                               b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
+                                               b.tile_sum, d_desc, s);
         rec(2);
-        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : ovf, ovf_cnt, nq, coll_q, cand_q,
-                                found_q, src_pos, nq * slot_cap, cta_id, cta_dist, cta_cap, res_cursor, ovf2,
-                                ovf_cnt + 1, ovf_cnt + 5, dense_grid, tile_sum, d_desc, nq, slot_cap, tmp_id,
-                                tmp_dist, s);
+        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : b.ovf, b.ovf_cnt, nq, b.coll_q,
+                                b.cand_q, b.found_q, b.src_pos, nq * slot_cap, b.cta_id, b.cta_dist, b.cta_cap,
+                                b.res_cursor, b.ovf2, b.ovf_cnt + 1, b.ovf_cnt + 5, dense_grid, b.tile_sum, d_desc, nq,
+                                slot_cap, b.tmp_id, b.tmp_dist, s);
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
-        launch_pdl(k_scan_compact, unsigned(ntiles * kScanSplit), 1024, 0, s, nq,
-                   static_cast<const unsigned long long*>(found_q), static_cast<const unsigned long long*>(tile_sum),
-                   res_off, static_cast<const unsigned long long*>(src_pos), static_cast<const uint32_t*>(tmp_id),
-                   static_cast<const uint32_t*>(tmp_dist), nq * slot_cap, static_cast<const uint32_t*>(cta_id),
-                   static_cast<const uint32_t*>(cta_dist), ix.id_offset, oq, oi, od, ix.d_pub, d_seq, ovf_cnt,
-                   static_cast<const unsigned long long*>(coll_q), static_cast<const unsigned long long*>(cand_q),
-                   d_desc);
+        launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit), 1024, 0, s, nq,
+                   static_cast<const unsigned long long*>(b.found_q), static_cast<const unsigned long long*>(b.tile_sum),
+                   b.res_off, static_cast<const unsigned long long*>(b.src_pos),
+                   static_cast<const uint32_t*>(b.tmp_id), static_cast<const uint32_t*>(b.tmp_dist), nq * slot_cap,
+                   static_cast<const uint32_t*>(b.cta_id), static_cast<const uint32_t*>(b.cta_dist), ix.id_offset,
+                   b.oq, b.oi, b.od, ix.d_pub, d_seq, b.ovf_cnt, static_cast<const unsigned long long*>(b.coll_q),
+                   static_cast<const unsigned long long*>(b.cand_q), d_desc);
         FCLSH_LAUNCHED();
         rec(5);
     };
-    struct {
-        unsigned long long total;
-        unsigned int cnt[2];
-    } hs{0, {0, 0}};
     // the host destination for this batch (read by k_scan_compact at run time,
     // so a replayed graph serves any destination)
     const bool host_cnt = nq && dest && dest->counters;
@@ -1834,16 +1874,23 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         h[4] = host_cnt ? dest->cap : 0;
         std::atomic_thread_fence(std::memory_order_release);
     }
+    DeviceIndex::Pending& p = ix.pending;
+    p.nq = nq;
+    p.radius = radius;
+    p.d_q = d_q;
+    p.host_cnt = host_cnt;
+    p.dest_cap = host_cnt ? dest->cap : 0;
+    p.dense_all = dense_all;
     if (nq) {
         // A shape seen twice in a row (same rows pointer, batch size, radius,
         // stream and workspace) is captured once into a CUDA graph and
         // relaunched: one host call instead of ~10 launches per batch.
         const std::vector<const void*> key = {d_q, reinterpret_cast<const void*>(nq),
-                                              reinterpret_cast<const void*>(uintptr_t(radius)), s, qkeys, coll_q,
-                                              cand_q, found_q, res_off, src_pos, tmp_id, tmp_dist, ovf, ovf2,
-                                              ovf_cnt, cta_id, cta_dist, oq, oi, od, scan_tmp, ix.d_pub, d_seq,
-                                              reinterpret_cast<const void*>(uintptr_t(timing)),
-                                              reinterpret_cast<const void*>(uintptr_t(dense_grid)), tile_sum,
+                                              reinterpret_cast<const void*>(uintptr_t(radius)), s, qkeys, b.coll_q,
+                                              b.cand_q, b.found_q, b.res_off, b.src_pos, b.tmp_id, b.tmp_dist, b.ovf,
+                                              b.ovf2, b.ovf_cnt, b.cta_id, b.cta_dist, b.oq, b.oi, b.od, b.scan_tmp,
+                                              ix.d_pub, d_seq, reinterpret_cast<const void*>(uintptr_t(timing)),
+                                              reinterpret_cast<const void*>(uintptr_t(dense_grid)), b.tile_sum,
                                               hash_src};
         if (ix.gexec && key == ix.gkey) {
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
@@ -1878,25 +1925,40 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
             enqueue_common();
             ix.gpending = key;
         }
-        if (before_wait) {
-            QueryOutput early;
-            early.nq = nq;
-            early.d_offsets = reinterpret_cast<uint64_t*>(res_off);
-            early.d_coll = reinterpret_cast<uint64_t*>(coll_q);
-            early.d_cand = reinterpret_cast<uint64_t*>(cand_q);
-            early.d_found = reinterpret_cast<uint64_t*>(found_q);
-            before_wait(early);
-        }
-        wait_published(ix.h_pub, ++ix.pub_seq, s);
+        p.seq = ++ix.pub_seq;
+    } else {
+        FCLSH_CUDA(cudaMemsetAsync(b.res_off, 0, 8, s)); // offsets = [0]
+        for (int e = 0; e < 6; ++e) FCLSH_CUDA(cudaEventRecord(ix.ev[e], s));
+    }
+}
+
+// Phase 2: wait until the batch published its total (mapped host memory),
+// run the general path for what both query kernels handed over, and return
+// the outputs.
+template <typename T, int LAYOUT>
+QueryOutput query_finish_impl(DeviceIndex& ix) {
+    DeviceIndex::Pending& p = ix.pending;
+    const uint64_t nq = p.nq;
+    const uint32_t radius = p.radius;
+    const uint64_t* d_q = p.d_q;
+    cudaStream_t s = ix.stream;
+    const uint64_t T_ = ix.tables;
+    const uint32_t slot_cap = kSlotCap;
+    QueryBufs<T> b = query_bufs<T>(ix, nq, s);
+    QueryOutput out;
+    out.nq = nq;
+    struct {
+        unsigned long long total;
+        unsigned int cnt[2];
+    } hs{0, {0, 0}};
+    if (nq) {
+        wait_published(ix.h_pub, p.seq, s);
         hs.total = ix.h_pub[0];
         hs.cnt[0] = unsigned(ix.h_pub[1]);
         hs.cnt[1] = unsigned(ix.h_pub[2]);
-    } else {
-        FCLSH_CUDA(cudaMemsetAsync(res_off, 0, 8, s)); // offsets = [0]
-        for (int e = 0; e < 6; ++e) FCLSH_CUDA(cudaEventRecord(ix.ev[e], s));
     }
     const unsigned int ns = hs.cnt[1];
-    ovf = ovf2; // what the CTA kernel could not take
+    const uint32_t* ovf = b.ovf2; // what the CTA kernel could not take
     unsigned long long total = hs.total;
     if (ns) {
         // general path for the overflowing queries
@@ -1907,7 +1969,7 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         auto* fill = static_cast<unsigned long long*>(ix.fill.ensure((ns + 1) * 8));
         FCLSH_CUDA(cudaMemsetAsync(coll_s, 0, (ns + 1) * 8, s));
         FCLSH_CUDA(cudaMemsetAsync(fill, 0, (ns + 1) * 8, s));
-        k_count_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), tb, coll_s);
+        k_count_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(b.qkeys, ovf, ns, uint32_t(T_), tb, coll_s);
         FCLSH_LAUNCHED();
         size_t tb_bytes = 0;
         FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb_bytes, coll_s, coll_off, ns + 1, s));
@@ -1917,10 +1979,10 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
         FCLSH_CUDA(cudaStreamSynchronize(s));
         uint32_t* cand = static_cast<uint32_t*>(ix.cand.ensure(std::max<uint64_t>(1, total_coll) * 4));
         uint32_t* sorted = static_cast<uint32_t*>(ix.cand_sorted.ensure(std::max<uint64_t>(1, total_coll) * 4));
-        tmp2_id = static_cast<uint32_t*>(ix.res2_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
-        tmp2_dist = static_cast<uint32_t*>(ix.res2_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        uint32_t* tmp2_id = static_cast<uint32_t*>(ix.res2_id.ensure(std::max<uint64_t>(1, total_coll) * 4));
+        uint32_t* tmp2_dist = static_cast<uint32_t*>(ix.res2_dist.ensure(std::max<uint64_t>(1, total_coll) * 4));
         if (total_coll) {
-            k_gather_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(qkeys, ovf, ns, uint32_t(T_), tb,
+            k_gather_sel<T, LAYOUT><<<grid_for(pairs, ix.device), 256, 0, s>>>(b.qkeys, ovf, ns, uint32_t(T_), tb,
                                                                                 coll_off, fill, cand);
             FCLSH_LAUNCHED();
             size_t sb = 0;
@@ -1930,43 +1992,96 @@ QueryOutput query_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32
                                                           int64_t(total_coll), int64_t(ns), coll_off, coll_off + 1, s));
         }
         k_verify_sel<<<grid_for(uint64_t(ns) * 32, ix.device), 256, 0, s>>>(
-            ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap + cta_cap,
-            tmp2_id, tmp2_dist, coll_q, cand_q, found_q, src_pos);
+            ns, ovf, coll_off, sorted, ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, nq * slot_cap + b.cta_cap,
+            tmp2_id, tmp2_dist, b.coll_q, b.cand_q, b.found_q, b.src_pos);
         FCLSH_LAUNCHED();
         // the overflowing queries' counts are in now: scan and compact again
-        scan_found(scan_tmp, scan_bytes);
-        FCLSH_CUDA(cudaMemcpyAsync(&hs.total, res_off + nq, 8, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaMemsetAsync(b.found_q + nq, 0, 8, s));
+        FCLSH_CUDA(cub::DeviceScan::ExclusiveSum(b.scan_tmp, b.scan_bytes, b.found_q, b.res_off, nq + 1, s));
+        FCLSH_CUDA(cudaMemcpyAsync(&hs.total, b.res_off + nq, 8, cudaMemcpyDeviceToHost, s));
         FCLSH_CUDA(cudaStreamSynchronize(s));
         total = hs.total;
-        if (total > out_cap) {
-            out_cap = total;
-            oq = static_cast<uint32_t*>(ix.out_q.ensure(out_cap * 4));
-            oi = static_cast<uint32_t*>(ix.out_id.ensure(out_cap * 4));
-            od = static_cast<uint32_t*>(ix.out_dist.ensure(out_cap * 4));
+        if (total > b.out_cap) {
+            b.out_cap = total;
+            b.oq = static_cast<uint32_t*>(ix.out_q.ensure(b.out_cap * 4));
+            b.oi = static_cast<uint32_t*>(ix.out_id.ensure(b.out_cap * 4));
+            b.od = static_cast<uint32_t*>(ix.out_dist.ensure(b.out_cap * 4));
         }
-        compact(nullptr);
+        k_compact<<<grid_for(nq * 32, ix.device), 256, 0, s>>>(
+            nq, b.src_pos, b.res_off, b.tmp_id, b.tmp_dist, nq * slot_cap, b.cta_id, b.cta_dist, b.cta_cap, tmp2_id,
+            tmp2_dist, ix.id_offset, b.oq, b.oi, b.od, nullptr, ix.pub_seq_dev.as<unsigned long long>(), b.ovf_cnt);
+        FCLSH_LAUNCHED();
     }
     FCLSH_CUDA(cudaEventRecord(ix.ev[6], s));
     out.total = total;
     out.d_query = ix.out_q.as<uint32_t>();
     out.d_id = ix.out_id.as<uint32_t>();
     out.d_dist = ix.out_dist.as<uint32_t>();
-    out.d_offsets = reinterpret_cast<uint64_t*>(res_off);
-    out.d_coll = reinterpret_cast<uint64_t*>(coll_q);
-    out.d_cand = reinterpret_cast<uint64_t*>(cand_q);
-    out.d_found = reinterpret_cast<uint64_t*>(found_q);
+    out.d_offsets = reinterpret_cast<uint64_t*>(b.res_off);
+    out.d_coll = reinterpret_cast<uint64_t*>(b.coll_q);
+    out.d_cand = reinterpret_cast<uint64_t*>(b.cand_q);
+    out.d_found = reinterpret_cast<uint64_t*>(b.found_q);
     // the general path rewrote counters and results in device memory
-    out.host_counters = host_cnt && !ns;
-    out.host_results = out.host_counters && total <= dest->cap;
+    out.host_counters = p.host_cnt && !ns;
+    out.host_results = out.host_counters && total <= p.dest_cap;
     ix.last_total = total;
-    ix.last_dense = dense_all ? nq : hs.cnt[0];
+    ix.last_dense = p.dense_all ? nq : hs.cnt[0];
     ix.last_overflow = ns;
+    p.active = false;
     return out;
 }
 
 } // namespace
 
+namespace {
+// Device-wide persisting-L2 limit (cudaLimitPersistingL2CacheSize) raised for
+// the key filters of live indexes: the first index on a device records the
+// limit it found, the last one to go restores it.
+struct L2PersistState {
+    int users = 0;
+    size_t saved = 0;
+};
+std::mutex g_l2_mu;
+L2PersistState g_l2[64];
+} // namespace
+
+bool l2_persist_acquire(int device, uint64_t bytes) {
+    if (device < 0 || device >= 64) return false;
+    int maxp = 0;
+    if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) != cudaSuccess || maxp <= 0) {
+        cudaGetLastError();
+        return false;
+    }
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    L2PersistState& st = g_l2[device];
+    size_t cur = 0;
+    if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (st.users == 0) st.saved = cur;
+    const size_t want = std::min<size_t>(size_t(maxp), size_t(bytes));
+    if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) cudaGetLastError();
+    ++st.users;
+    return true;
+}
+
+void l2_persist_release(int device) {
+    if (device < 0 || device >= 64) return;
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    L2PersistState& st = g_l2[device];
+    if (st.users <= 0) return;
+    if (--st.users == 0) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, st.saved) != cudaSuccess) cudaGetLastError();
+        cudaSetDevice(prev);
+    }
+}
+
 DeviceIndex::~DeviceIndex() {
+    if (l2_persist) l2_persist_release(device);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -2046,11 +2161,11 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     ix->layout = layout;
     if (layout == kLayoutBuckets) {
         ix->nbuckets = uint64_t(1) << bb;
-        ix->key_shift = kbits - bb;
+        ix->key_shift = 64 - bb;
         ix->dir_bits = 0;
     } else {
         ix->dir_bits = b;
-        ix->key_shift = kbits - b;
+        ix->key_shift = 64 - b;
     }
 
     // key filter (buckets): FCLSH_FILTER_BPK bits per posting (default 1),
@@ -2058,7 +2173,7 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     // below 3/4 bit per posting it rejects too few probes to pay for its own
     // read. FCLSH_FILTER=0: none.
     ix->filter_words = 0;
-    ix->filter_shift = 64 - kbits;
+    ix->key_scale = ~0ull / opt.prime; // floor((2^64 - 1) / P) = floor(2^64 / P) for odd P
     if (layout == kLayoutBuckets && !(getenv("FCLSH_FILTER") && getenv("FCLSH_FILTER")[0] == '0')) {
         const double bpk = getenv("FCLSH_FILTER_BPK") ? atof(getenv("FCLSH_FILTER_BPK")) : 1.0;
         const double mb = getenv("FCLSH_FILTER_MB") ? atof(getenv("FCLSH_FILTER_MB")) : 80.0;
@@ -2075,15 +2190,9 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
             ix->filter.ensure(fbytes);
             FCLSH_CUDA(cudaMemsetAsync(ix->filter.p, 0, fbytes, ix->stream));
             // room for the filter's evict_last lines in the persisting part of L2
-            int maxp = 0;
-            if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, opt.device) == cudaSuccess &&
-                maxp > 0) {
-                size_t cur = 0;
-                cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-                const size_t want = std::min<size_t>(size_t(maxp), size_t(fbytes));
-                if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-            }
-            cudaGetLastError();
+            // (the device-wide limit is restored when the last index holding a
+            // filter on this device is destroyed)
+            ix->l2_persist = l2_persist_acquire(opt.device, fbytes);
         }
         if (layout == kLayoutBuckets) {
             ix->entries.ensure(bkt_size(bb));
@@ -2115,7 +2224,12 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
 }
 
 namespace {
-constexpr int kCHS = 16384, kCKCAP = 4096; // set slots and cut-table ids of the budgeted query
+constexpr int kCHSLog = 14, kCKCAP = 4096; // shared set slots (2^14) and cut-table ids of the budgeted query
+
+__global__ void k_iota(uint32_t* __restrict__ out, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = uint32_t(i);
+}
 
 template <typename T, int LAYOUT>
 void query_c_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, uint64_t budget,
@@ -2124,20 +2238,70 @@ void query_c_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t ra
     const uint64_t T_ = ix.tables;
     K* qkeys = static_cast<K*>(ix.q_keys.ensure(std::max<uint64_t>(1, nq * T_) * sizeof(K)));
     auto* ctr = static_cast<unsigned int*>(ix.overflow_cnt.ensure(32)); // [6] hand-out, [7] errors
-    FCLSH_CUDA(cudaMemsetAsync(ctr + 6, 0, 8, s));
     hash_rows(*ix.fs, d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s);
-    auto kern = k_query_c<T, LAYOUT, kCHS, kCKCAP>;
-    const size_t smem = size_t(kCHS + kCKCAP + T_) * 4;
-    const int per_sm = resident_ctas(kern, 512, smem, ix.device);
-    if (per_sm < 1) throw ResourceError("query_c_r_nn: too many tables for the device kernel");
-    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(nq, uint64_t(per_sm) * sm_count(ix.device)));
-    kern<<<unsigned(grid), 512, smem, s>>>(qkeys, nq, uint32_t(T_), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
-                                          ix.row_words, radius, budget, counters, best, ctr + 6, ctr + 7);
+    auto kern = k_query_c<T, LAYOUT>;
+    const size_t tbytes = ((T_ + 3) & ~uint64_t(3)) * 4;
+    // shared mode: every distinct id of a walk fits the set at load <= 3/4
+    if (budget <= (uint64_t(1) << kCHSLog) / 4 * 3 && T_ <= 16384) {
+        FCLSH_CUDA(cudaMemsetAsync(ctr + 6, 0, 8, s));
+        const size_t smem = tbytes + ((size_t(1) << kCHSLog) + kCKCAP) * 4;
+        const int per_sm = resident_ctas(kern, 512, smem, ix.device);
+        if (per_sm < 1) throw ResourceError("query_c_r_nn: too many tables for the device kernel");
+        const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(nq, uint64_t(per_sm) * sm_count(ix.device)));
+        kern<<<unsigned(grid), 512, smem, s>>>(qkeys, nq, uint32_t(T_), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
+                                              ix.row_words, radius, budget, counters, best, ctr + 6, ctr + 7,
+                                              uint32_t(kCHSLog), uint32_t(kCKCAP), nullptr, ix.id_offset);
+        FCLSH_LAUNCHED();
+        unsigned int errs = 0;
+        FCLSH_CUDA(cudaMemcpyAsync(&errs, ctr + 7, 4, cudaMemcpyDeviceToHost, s));
+        FCLSH_CUDA(cudaStreamSynchronize(s));
+        if (!errs) return;
+        // a cut bucket longer than the shared buffer: the batch again in global mode
+    }
+    // Global mode (any budget, as the reference's std::optional<uint64_t>,
+    // index.hpp:90-93): per-query collision totals bound the distinct ids of
+    // a walk (<= min(budget, collisions)) and the cut bucket; every CTA gets
+    // a global slice [set (load <= 1/2) | cut ids | inserted slots].
+    uint32_t* sel = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
+    auto* coll = static_cast<unsigned long long*>(ix.coll_sel.ensure(std::max<uint64_t>(1, nq) * 8));
+    k_iota<<<grid_for(nq, ix.device), 256, 0, s>>>(sel, nq);
+    FCLSH_LAUNCHED();
+    FCLSH_CUDA(cudaMemsetAsync(coll, 0, nq * 8, s));
+    k_count_sel<T, LAYOUT><<<grid_for(nq * T_, ix.device), 256, 0, s>>>(qkeys, sel, nq, uint32_t(T_), view<T>(ix),
+                                                                         coll);
+    FCLSH_LAUNCHED();
+    std::vector<unsigned long long> hc(nq);
+    FCLSH_CUDA(cudaMemcpyAsync(hc.data(), coll, nq * 8, cudaMemcpyDeviceToHost, s));
+    FCLSH_CUDA(cudaStreamSynchronize(s));
+    uint64_t maxc = 1;
+    for (auto c : hc) maxc = std::max<uint64_t>(maxc, c);
+    const uint64_t maxd = std::min<uint64_t>(maxc, budget); // distinct ids of one walk
+    if (maxd >= (uint64_t(1) << 30)) throw ResourceError("query_c_r_nn: walk too long for the device id set");
+    uint32_t hs_log = 10;
+    while ((uint64_t(1) << hs_log) < 2 * maxd) ++hs_log;
+    const uint64_t HS = uint64_t(1) << hs_log;
+    uint32_t kcap = 1;
+    while (kcap < maxc && kcap < (uint32_t(1) << 31)) kcap <<= 1; // the cut bucket <= all collisions
+    const uint64_t per_cta = (tbytes / 4 + HS + kcap + HS / 2) * 4;
+    size_t free_b = 0, total_b = 0;
+    FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t fit = std::max<uint64_t>(1, (free_b / 2) / per_cta);
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>({nq, uint64_t(2) * sm_count(ix.device), fit}));
+    DevBuf scratch;
+    try {
+        scratch.ensure(grid * per_cta);
+    } catch (const CudaError& e) {
+        throw ResourceError(std::string("query_c_r_nn: device memory exhausted (") + e.what() + ")");
+    }
+    FCLSH_CUDA(cudaMemsetAsync(ctr + 6, 0, 8, s));
+    kern<<<unsigned(grid), 512, 0, s>>>(qkeys, nq, uint32_t(T_), view<T>(ix), ix.rows.as<uint64_t>(), d_q,
+                                            ix.row_words, radius, budget, counters, best, ctr + 6, ctr + 7, hs_log,
+                                            kcap, scratch.as<uint32_t>(), ix.id_offset);
     FCLSH_LAUNCHED();
     unsigned int errs = 0;
     FCLSH_CUDA(cudaMemcpyAsync(&errs, ctr + 7, 4, cudaMemcpyDeviceToHost, s));
     FCLSH_CUDA(cudaStreamSynchronize(s));
-    if (errs) throw ResourceError("query_c_r_nn: a bucket cut by the posting budget holds more than 4096 postings");
+    if (errs) throw CudaError("query_c_r_nn: cut bucket exceeded its bound");
 }
 } // namespace
 
@@ -2147,10 +2311,6 @@ void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t 
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
     const uint64_t budget = posting_budget < 0 ? 3 * ix.tables : uint64_t(posting_budget); // index.cpp:201
-    if (budget > uint64_t(kCHS) / 4 * 3)
-        throw UsageError("query_c_r_nn: posting budgets above " + std::to_string(kCHS / 4 * 3) +
-                         " are not supported on the device");
-    if (ix.tables > 16384) throw UsageError("query_c_r_nn: more than 16384 tables");
     if (nq == 0) return;
     FCLSH_CUDA(cudaSetDevice(ix.device));
     cudaStream_t s = stream ? stream : ix.stream;
@@ -2168,12 +2328,12 @@ void query_c_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t 
     }
 }
 
-QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
-                         const std::function<void(const QueryOutput&)>& before_wait, const HostDest* dest,
-                         const uint64_t* hash_src) {
+void query_enqueue(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
+                   const HostDest* dest, const uint64_t* hash_src) {
     if (radius > ix.radius) // index.cpp:147-153
         throw UsageError("query radius " + std::to_string(radius) + " exceeds the index radius " +
                          std::to_string(ix.radius));
+    if (ix.pending.active) throw UsageError("query: the previous batch on this index was not finished");
     FCLSH_CUDA(cudaSetDevice(ix.device));
     // Work runs on the index's stream, ordered after / before the caller's.
     cudaStream_t s = ix.stream;
@@ -2184,20 +2344,50 @@ QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint
         FCLSH_CUDA(cudaEventRecord(ix.ev_in, stream));
         FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_in, 0));
     }
+    if (ix.wide) {
+        if (ix.layout == kLayoutBuckets)
+            query_enqueue_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, dest, hash_src);
+        else
+            query_enqueue_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, dest, hash_src);
+    } else {
+        if (ix.layout == kLayoutBuckets)
+            query_enqueue_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, dest, hash_src);
+        else
+            query_enqueue_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, dest, hash_src);
+    }
+    ix.pending.active = true;
+    ix.pending.caller = join ? stream : nullptr;
+}
+
+QueryOutput query_finish(DeviceIndex& ix) {
+    if (!ix.pending.active) throw UsageError("query: no batch in flight on this index");
+    FCLSH_CUDA(cudaSetDevice(ix.device));
+    cudaStream_t caller = ix.pending.caller;
     QueryOutput o;
-    if (ix.wide)
-        o = ix.layout == kLayoutBuckets ? query_impl<WideEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest, hash_src)
-                                        : query_impl<WideEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest, hash_src);
-    else
-        o = ix.layout == kLayoutBuckets ? query_impl<NarrowEntry, kLayoutBuckets>(ix, d_q, nq, radius, s, before_wait, dest, hash_src)
-                                        : query_impl<NarrowEntry, kLayoutCsr>(ix, d_q, nq, radius, s, before_wait, dest, hash_src);
-    if (join) {
-        FCLSH_CUDA(cudaEventRecord(ix.ev_out, s));
-        FCLSH_CUDA(cudaStreamWaitEvent(stream, ix.ev_out, 0));
+    try {
+        if (ix.wide)
+            o = ix.layout == kLayoutBuckets ? query_finish_impl<WideEntry, kLayoutBuckets>(ix)
+                                            : query_finish_impl<WideEntry, kLayoutCsr>(ix);
+        else
+            o = ix.layout == kLayoutBuckets ? query_finish_impl<NarrowEntry, kLayoutBuckets>(ix)
+                                            : query_finish_impl<NarrowEntry, kLayoutCsr>(ix);
+    } catch (...) {
+        ix.pending.active = false;
+        throw;
+    }
+    if (caller) {
+        FCLSH_CUDA(cudaEventRecord(ix.ev_out, ix.stream));
+        FCLSH_CUDA(cudaStreamWaitEvent(caller, ix.ev_out, 0));
     }
     ix.stages_pending = true;
     ix.stages_timed = ix.stage_timing;
     return o;
+}
+
+QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
+                         const HostDest* dest, const uint64_t* hash_src) {
+    query_enqueue(ix, d_q, nq, radius, stream, dest, hash_src);
+    return query_finish(ix);
 }
 
 void DeviceIndex::collect_stages() {

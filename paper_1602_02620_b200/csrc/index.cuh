@@ -3,7 +3,6 @@
 #pragma once
 
 #include <cstdint>
-#include <functional>
 #include <memory>
 #include <vector>
 
@@ -41,16 +40,18 @@ struct DeviceIndex {
     int layout = 0;           // kLayoutCsr or kLayoutBuckets
     uint64_t nbuckets = 0;    // buckets per table (kLayoutBuckets)
     uint32_t dir_bits = 0;    // b (kLayoutCsr)
-    uint32_t key_shift = 0;   // cell / home bucket = key >> key_shift
+    uint32_t key_shift = 0;   // cell / home bucket = (key * key_scale) >> key_shift
+    uint64_t key_scale = 0;   // floor(2^64 / prime)
     uint64_t id_offset = 0;
     double build_ms = 0;
     std::unique_ptr<DeviceFamilySet> fs;
     DevBuf rows, entries, dir;
     // per-table key filter (buckets layout, index.cu): filter_words 32-bit
-    // words per table, bit floor(key * 32 * filter_words / 2^kbits) set iff
+    // words per table, bit floor(key * 32 * filter_words / P) set iff
     // some posting of the table maps there; 0 words: no filter
     DevBuf filter;
-    uint32_t filter_words = 0, filter_shift = 0;
+    uint32_t filter_words = 0;
+    bool l2_persist = false; // holds a share of the device's persisting-L2 limit (restored by the last holder)
 
     // query workspace (grow-only)
     DevBuf q_rows, q_keys, r_start, r_count, counters, coll_off, coll_sel, fill, cand, cand_sorted, src_pos,
@@ -86,6 +87,17 @@ struct DeviceIndex {
     // the batch total (batch_ms) is always measured
     bool stage_timing = false, stages_timed = false;
     double batch_ms = 0;
+    // the batch between query_enqueue and query_finish
+    struct Pending {
+        bool active = false;
+        uint64_t nq = 0;
+        uint32_t radius = 0;
+        const uint64_t* d_q = nullptr;
+        bool host_cnt = false, dense_all = false;
+        uint64_t dest_cap = 0;
+        unsigned long long seq = 0;
+        cudaStream_t caller = nullptr; // joined after the batch (null: none)
+    } pending;
     void collect_stages(); // waits for the last batch, fills stage_ms / t_*_ms (-1 = not measured)
 
     ~DeviceIndex();
@@ -93,6 +105,12 @@ struct DeviceIndex {
     uint64_t entry_bytes() const { return wide ? 16 : 8; }
     uint64_t device_bytes() const { return rows.bytes + entries.bytes + dir.bytes; }
 };
+
+// Raises the device's persisting-L2 limit to cover `bytes` (the key filter)
+// for as long as some index holds it; the last release restores the limit
+// found by the first acquire.
+bool l2_persist_acquire(int device, uint64_t bytes);
+void l2_persist_release(int device);
 
 struct IndexBuildOptions {
     uint64_t prime = kMersenne61;
@@ -132,15 +150,21 @@ struct HostDest {
 };
 
 // query_r_nn for nq device rows; results in index-owned device buffers.
-// before_wait (optional) runs once the batch is enqueued and before the host
-// waits for its total: the offsets / counters pointers are valid (their
-// values complete in stream order), d_query / d_id / d_dist and total are not.
-QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius,
-                         cudaStream_t stream, const std::function<void(const QueryOutput&)>& before_wait = {},
-                         const HostDest* dest = nullptr, const uint64_t* hash_src = nullptr);
+// Split in two so that several indexes (the shards of a cluster) run their
+// batches concurrently: query_enqueue queues the batch on the index's stream
+// (after the work already queued on `stream`) and returns at once;
+// query_finish waits for the batch's published total, runs the general path
+// if any query needs it, joins `stream` and returns the outputs. One batch in
+// flight per index. query_device = both.
+// dest (optional): mapped pinned host destination the batch writes directly.
 // hash_src (optional): the same rows in mapped pinned host memory (device
 // view); the hash kernel reads them there and writes d_q as it goes, so no
-// separate host-to-device copy of the batch is needed
+// separate host-to-device copy of the batch is needed.
+void query_enqueue(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
+                   const HostDest* dest = nullptr, const uint64_t* hash_src = nullptr);
+QueryOutput query_finish(DeviceIndex& ix);
+QueryOutput query_device(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint32_t radius, cudaStream_t stream,
+                         const HostDest* dest = nullptr, const uint64_t* hash_src = nullptr);
 
 // query_c_r_nn (index.cpp:190-235) for nq device rows: d_counters [nq][3]
 // {collisions, candidates, found}, d_best [nq][2] {id, distance} (all-ones

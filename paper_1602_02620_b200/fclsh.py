@@ -345,6 +345,28 @@ def merge_shards(offsets_all, triples_all, out_triples, out_offsets, device: int
                                       C.c_void_p(out_offsets.data_ptr()), device, _stream_ptr(stream)))
 
 
+def _results_from(rp, nq: int) -> "QueryResults":
+    """QueryResults viewing the pinned block behind an fclsh_result (freed
+    with fclsh_result_free once the last view is gone)."""
+    owner = _ResultBlock(rp)
+    r = rp.contents
+    tot = int(r.total)
+
+    def arr(p, cnt, ct, dt):
+        if cnt == 0:
+            return np.zeros(0, dt)
+        buf = (ct * cnt).from_address(C.cast(p, C.c_void_p).value)
+        buf._owner = owner
+        return np.frombuffer(buf, dtype=dt)
+
+    return QueryResults(arr(r.query, tot, C.c_uint32, np.uint32), arr(r.id, tot, C.c_uint32, np.uint32),
+                        arr(r.distance, tot, C.c_uint32, np.uint32),
+                        arr(r.offsets, nq + 1, C.c_uint64, np.uint64),
+                        arr(r.collisions, nq, C.c_uint64, np.uint64),
+                        arr(r.candidates, nq, C.c_uint64, np.uint64), arr(r.found, nq, C.c_uint64, np.uint64),
+                        float(r.time_hash_ms), float(r.time_probe_ms), float(r.time_verify_ms))
+
+
 class IndexSet:
     """IndexSet (index.hpp:42-52) resident on one GPU."""
 
@@ -388,23 +410,7 @@ class IndexSet:
             raise UsageError("query width does not match the index")
         rp = C.POINTER(N.Result)()
         _check(N.lib().fclsh_query(self._h, _ptr(q, N.u64p), nq, radius, C.byref(rp)))
-        owner = _ResultBlock(rp)  # the arrays below are views of its pinned block
-        r = rp.contents
-        tot = int(r.total)
-
-        def arr(p, cnt, ct, dt):
-            if cnt == 0:
-                return np.zeros(0, dt)
-            buf = (ct * cnt).from_address(C.cast(p, C.c_void_p).value)
-            buf._owner = owner  # freed (fclsh_result_free) when the last view is gone
-            return np.frombuffer(buf, dtype=dt)
-
-        return QueryResults(arr(r.query, tot, C.c_uint32, np.uint32), arr(r.id, tot, C.c_uint32, np.uint32),
-                            arr(r.distance, tot, C.c_uint32, np.uint32),
-                            arr(r.offsets, nq + 1, C.c_uint64, np.uint64),
-                            arr(r.collisions, nq, C.c_uint64, np.uint64),
-                            arr(r.candidates, nq, C.c_uint64, np.uint64), arr(r.found, nq, C.c_uint64, np.uint64),
-                            float(r.time_hash_ms), float(r.time_probe_ms), float(r.time_verify_ms))
+        return _results_from(rp, nq)
 
     STAGES = ("hash", "fused", "dense", "found_scan", "compact", "overflow")
 
@@ -502,6 +508,104 @@ def launch_count() -> int:
 
 def launch_count_reset() -> None:
     N.lib().fclsh_launch_count_reset()
+
+
+# ------------------------------------------------------------------ cluster
+
+CLUSTER_ID_BYTES = 128
+
+
+def cluster_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 of a multi-process cluster sends it to the others)."""
+    buf = C.create_string_buffer(CLUSTER_ID_BYTES)
+    _check(N.lib().fclsh_cluster_unique_id(buf))
+    return buf.raw
+
+
+class Cluster:
+    """Point-sharded index over the GPUs of one box (fclsh_cluster_*).
+
+    Cluster(devices=[0, 1, ...], shards_per_rank=k): this process drives every
+    GPU. Cluster(rank=r, world=w, device=d, uid=...): one process per GPU
+    (uid from cluster_unique_id() on rank 0). build / query_r_nn are
+    collective: every process calls them. query_r_nn returns the merged result
+    on rank 0 and None elsewhere."""
+
+    def __init__(self, devices=None, shards_per_rank: int = 1, *, rank: int | None = None, world: int = 1,
+                 device: int = 0, uid: bytes | None = None):
+        h = C.c_void_p()
+        if rank is None:
+            devs = list(devices) if devices is not None else [0]
+            arr = (C.c_int * len(devs))(*devs)
+            _check(N.lib().fclsh_cluster_create(arr, len(devs), shards_per_rank, C.byref(h)))
+        else:
+            _check(N.lib().fclsh_cluster_create_rank(uid, world, rank, device, shards_per_rank, C.byref(h)))
+        self._h = h
+        self.plan = None
+
+    def __del__(self, _free=_release):
+        _free(self, "fclsh_cluster_destroy")
+
+    def info(self) -> dict:
+        i = N.ClusterInfo()
+        _check(N.lib().fclsh_cluster_info_get(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in N.ClusterInfo._fields_}
+
+    @property
+    def is_root(self) -> bool:
+        return self.info()["rank"] == 0
+
+    def build(self, data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, n: int | None = None,
+              local_rows: bool = False, prime: int = M61, include_zero_column: bool = False,
+              table_budget: int = DEFAULT_TABLE_BUDGET, id_offset: int = 0, directory_bits: int = 0,
+              layout: str = "auto") -> "Cluster":
+        """build_index over the sharded points. data_rows: all n points (numpy
+        or a CUDA tensor), or with local_rows=True only this process's range
+        (n = the global count)."""
+        opt = N.IndexOptions()
+        N.lib().fclsh_index_options_default(C.byref(opt))
+        opt.prime = prime
+        opt.include_zero_column = int(include_zero_column)
+        opt.table_budget = table_budget
+        opt.id_offset = id_offset
+        opt.directory_bits = directory_bits
+        opt.layout = {"auto": 0, "csr": 1, "buckets": 2}[layout]
+        if hasattr(data_rows, "data_ptr"):
+            ptr, on_dev, rows_n = C.c_void_p(data_rows.data_ptr()), int(data_rows.is_cuda), data_rows.shape[0]
+        else:
+            data_rows = _u64(data_rows)
+            if data_rows.ndim != 2 or data_rows.shape[1] != words_for(plan.dims):
+                raise UsageError("index: dataset width does not match the plan")
+            ptr, on_dev, rows_n = data_rows.ctypes.data_as(C.c_void_p), 0, data_rows.shape[0]
+        total = rows_n if n is None else n
+        _check(N.lib().fclsh_cluster_build(self._h, ptr, on_dev, 1 if local_rows else 0, total, plan.dims, radius,
+                                           plan._h, rng_seed, C.byref(opt)))
+        self.plan = plan
+        self._keep = data_rows  # (the library copied the rows; kept only for symmetry with IndexSet)
+        return self
+
+    def query_r_nn(self, q_rows, radius: int):
+        """query_r_nn over every shard (host rows in on rank 0; None on other ranks)."""
+        q = _u64(q_rows) if q_rows is not None else np.zeros((0, 1), np.uint64)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        nq = q.shape[0]
+        rp = C.POINTER(N.Result)()
+        _check(N.lib().fclsh_cluster_query(self._h, _ptr(q, N.u64p), nq, radius, C.byref(rp)))
+        if not rp:
+            return None
+        return _results_from(rp, nq)
+
+    def query_device(self, q_rows, radius: int, stream=None, nq: int | None = None):
+        """Device rows in (CUDA tensor on rank 0's GPU), device results on rank 0
+        (DeviceQueryResults; nq == 0 and null pointers on other ranks)."""
+        out = N.DeviceResult()
+        ptr = C.c_void_p(q_rows.data_ptr()) if q_rows is not None else C.c_void_p(0)
+        count = q_rows.shape[0] if q_rows is not None else (nq or 0)
+        _check(N.lib().fclsh_cluster_query_device(self._h, ptr, count, radius, _stream_ptr(stream), C.byref(out)))
+        return DeviceQueryResults(int(out.nq), int(out.total), out.d_query or 0, out.d_id or 0,
+                                  out.d_distance or 0, out.d_offsets or 0, out.d_collisions or 0,
+                                  out.d_candidates or 0, out.d_found or 0, out)
 
 
 # ------------------------------------------------------------------ workloads

@@ -279,3 +279,46 @@ def test_pinned_rows_hashed_in_place(oracle, d, radius, override):
         got = ix.query_r_nn(pinned, radius)
         assert (got.triples() == want.triples()).all()
         assert (np.stack([got.collisions, got.candidates, got.found], 1) == counters).all()
+
+
+@pytest.mark.parametrize("budget", [20000, 10**12])
+@pytest.mark.parametrize("dup", [60, 6000])
+def test_query_c_r_nn_any_budget_and_long_cut_buckets(budget, dup):
+    """Budgets past the shared id set (> 12288) and buckets longer than the
+    shared cut buffer (> 4096 postings: `dup` copies of one row) run from a
+    global-memory set; the reference takes any std::optional<uint64_t> budget
+    (index.hpp:90-93). Also: the shard's id offset is applied to the best id."""
+    from oracle import oracle as O
+    if not O.reference_available():
+        pytest.skip("compiled reference unavailable")
+    ref = O.reference()
+    rng = np.random.default_rng(dup + budget % 97)
+    d, radius = 128, 5
+    rows = random_rows(rng, 9000, d)
+    rows[10:10 + dup] = rows[5]
+    q = np.concatenate([rows[5:6], planted_queries(rng, rows, d, 60, radius + 2)])
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, F.PlanOverride(F.PlanKind.identity, 1))
+    oi = ref.index_build(rows, d, radius, 11, 22, override=(0, 1), prime=M31, threads=4)
+    for b in (budget, 4100, 13000):
+        want_c, want_b = oi.query_c(q, radius, b, threads=4)
+        for layout in LAYOUTS:
+            ix = F.build_index(rows, radius, plan, 22, prime=M31, layout=layout, id_offset=777)
+            counters, bid, bd = ix.query_c_r_nn(q, radius, b)
+            assert (counters == want_c).all(), (b, layout)
+            none = want_b[:, 0] == 0xFFFFFFFF
+            assert (bid[none] == -1).all()
+            assert (bid[~none] == want_b[~none, 0].astype(np.int64) + 777).all()
+            assert (bd[~none] == want_b[~none, 1]).all()
+
+
+@pytest.mark.parametrize("prime", [(1 << 62) + 135, (1 << 40) - 87, 2147483659])
+def test_home_bucket_spread_for_primes_below_a_power_of_two(oracle, prime):
+    """Home buckets and filter bits come from the key's fraction of [0, P)
+    (key * floor(2^64 / P)), so a prime just above a power of two (kbits = 63
+    for 2^62 + 135) still spreads keys over every bucket; results equal the
+    reference either way."""
+    rng = np.random.default_rng(prime % 1000)
+    d = 128
+    rows = random_rows(rng, 4000, d)
+    q = planted_queries(rng, rows, d, 120, 6)
+    check_against_oracle(oracle, rows, q, d, 4, (0, 1), prime, layouts=("buckets", "csr"))
