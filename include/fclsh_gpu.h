@@ -402,6 +402,12 @@ int fclsh_cluster_query(fclsh_cluster* cl, const uint64_t* q_rows, uint64_t nq, 
  * results are ordered before what is queued on it afterwards. */
 int fclsh_cluster_query_device(fclsh_cluster* cl, const uint64_t* d_q_rows, uint64_t nq, uint32_t radius,
                                void* stream, fclsh_device_result* out);
+/* Per-shard stage timing (fclsh_query_stage_timing / _stage_ms /
+ * _path_counts of the shard indexes this process holds, numbered in rank then
+ * shard order from 0). */
+int fclsh_cluster_stage_timing(fclsh_cluster* cl, int enable);
+int fclsh_cluster_stage_ms(const fclsh_cluster* cl, uint32_t local_shard, double* ms, int n);
+int fclsh_cluster_path_counts(const fclsh_cluster* cl, uint32_t local_shard, uint64_t* dense, uint64_t* general);
 void fclsh_cluster_destroy(fclsh_cluster* cl);
 
 /* Number of kernels the library launched on this thread since the last
@@ -411,15 +417,17 @@ void fclsh_launch_count_reset(void);
 
 /* ------------------------------------------------------------- workloads ---
  * Seeded synthetic inputs of the BASELINE configs. Host
- * buffers, multithreaded, counter-based (deterministic for any thread count).
+ * buffers, multithreaded, counter-based (deterministic for any thread count):
+ * rows [row0, row0 + n) of one unbounded stream, so each rank of a cluster
+ * generates just its own slice of a global dataset.
  *   bernoulli: n rows of d i.i.d. Bernoulli(0.5) bits.
  *   clustered: centres rows of Bernoulli(0.5) bits; each of n rows copies a
  *              uniformly drawn centre and flips each bit w.p. flip_p.
  *   planted:   nq queries, each a uniformly drawn data row with k flipped
  *              distinct positions, k uniform in [0, kmax]; src_out gets the
  *              source row id (may be NULL).                                */
-int fclsh_gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
-int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p,
+int fclsh_gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
+int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
                         uint64_t* rows, int threads);
 int fclsh_gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq,
                       uint32_t kmax, uint64_t* qrows, uint32_t* src_out);

@@ -130,8 +130,14 @@ public:
     RnnBatch query_r_nn(const uint64_t* q_rows, uint64_t nq, uint32_t radius) {
         fclsh_result* r = nullptr;
         check(fclsh_query(h_.get(), q_rows, nq, radius, &r));
+        return to_batch(r, nq);
+    }
+
+    // the host result block -> vectors (frees the block)
+    static RnnBatch to_batch(fclsh_result* r, uint64_t nq) {
         std::unique_ptr<fclsh_result, void (*)(fclsh_result*)> guard(r, fclsh_result_free);
         RnnBatch b;
+        if (!r) return b;
         b.query.assign(r->query, r->query + r->total);
         b.id.assign(r->id, r->id + r->total);
         b.distance.assign(r->distance, r->distance + r->total);
@@ -157,5 +163,51 @@ inline Index build_index(const uint64_t* rows, uint64_t n, uint64_t dims, uint32
     check(fclsh_index_build(rows, 0, n, dims, radius, plan.handle(), rng_seed, &o, &h));
     return Index(h);
 }
+
+// A point-sharded index over several GPUs (or several shards on one GPU):
+// the same query_r_nn results as one Index over all points (fclsh_cluster_*).
+class Cluster {
+public:
+    // this process drives `devices`, shards_per_device shards each
+    Cluster(const std::vector<int>& devices, uint32_t shards_per_device) : h_(nullptr, fclsh_cluster_destroy) {
+        fclsh_cluster* h = nullptr;
+        check(fclsh_cluster_create(devices.data(), uint32_t(devices.size()), shards_per_device, &h));
+        h_.reset(h, fclsh_cluster_destroy);
+    }
+    // one rank of a multi-process cluster (id from rank 0's unique_id())
+    Cluster(const unsigned char* id, uint32_t world, uint32_t rank, int device, uint32_t shards_per_rank)
+        : h_(nullptr, fclsh_cluster_destroy) {
+        fclsh_cluster* h = nullptr;
+        check(fclsh_cluster_create_rank(id, world, rank, device, shards_per_rank, &h));
+        h_.reset(h, fclsh_cluster_destroy);
+    }
+    static std::vector<unsigned char> unique_id() {
+        std::vector<unsigned char> id(FCLSH_CLUSTER_ID_BYTES);
+        check(fclsh_cluster_unique_id(id.data()));
+        return id;
+    }
+    void build(const uint64_t* rows, uint64_t n, uint64_t dims, uint32_t radius, const PreprocessPlan& plan,
+               uint64_t rng_seed, uint64_t prime = kMersenne61, bool local_rows = false) {
+        fclsh_index_options o;
+        fclsh_index_options_default(&o);
+        o.prime = prime;
+        check(fclsh_cluster_build(h_.get(), rows, 0, local_rows ? FCLSH_ROWS_LOCAL : FCLSH_ROWS_GLOBAL, n, dims,
+                                  radius, plan.handle(), rng_seed, &o));
+    }
+    fclsh_cluster_info info() const {
+        fclsh_cluster_info i{};
+        check(fclsh_cluster_info_get(h_.get(), &i));
+        return i;
+    }
+    // collective; the merged result on rank 0 (empty elsewhere)
+    RnnBatch query_r_nn(const uint64_t* q_rows, uint64_t nq, uint32_t radius) {
+        fclsh_result* r = nullptr;
+        check(fclsh_cluster_query(h_.get(), q_rows, nq, radius, &r));
+        return Index::to_batch(r, nq);
+    }
+
+private:
+    std::shared_ptr<fclsh_cluster> h_;
+};
 
 } // namespace fclsh::gpu

@@ -721,3 +721,123 @@ int orc_scan_truth(const uint64_t* rows, uint64_t n, const uint64_t* qrows, uint
     free(th);
     return 0;
 }
+
+/* ------------------------------------------------- BASELINE workload inputs
+ * Not reference code: the seeded synthetic inputs of the BASELINE configs
+ * (DESIGN.md "Inputs"), restated here so that the CPU baseline and the
+ * reference arm of bench.py build the identical bytes without loading the
+ * product library. Counter-based: word k of a stream with key K is
+ * splitmix64(K + k * gamma) (the k-th SplitMix64 output seeded with K);
+ * stream keys come from the reference's labelled Rng::stream seeds.
+ * tests/test_oracle_pin.py pins these bytes to the product's generators. */
+
+static const uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+static inline uint64_t word_at(uint64_t key, uint64_t k) { return orc_splitmix64(key + k * kGamma); }
+static inline uint64_t scale_below(uint64_t r, uint64_t bound) { /* floor(r * bound / 2^64) */
+    return (uint64_t)(((unsigned __int128)r * bound) >> 64);
+}
+
+typedef struct {
+    int kind; /* 0 bernoulli, 1 clustered */
+    uint64_t key, kc, kf, thresh, row0, dims, words, centres, b, e;
+    const uint64_t* cen;
+    uint64_t* rows;
+} gen_job;
+
+static void* gen_worker(void* arg) {
+    gen_job* j = (gen_job*)arg;
+    const uint64_t W = j->words;
+    const uint64_t tail = j->dims % 64 ? (1ull << (j->dims % 64)) - 1 : ~0ull;
+    for (uint64_t i = j->b; i < j->e; ++i) {
+        const uint64_t g = j->row0 + i;
+        if (j->kind == 0) {
+            for (uint64_t w = 0; w < W; ++w) j->rows[i * W + w] = word_at(j->key, g * W + w);
+            j->rows[i * W + W - 1] &= tail;
+        } else {
+            const uint64_t c = scale_below(word_at(j->kc, g), j->centres);
+            for (uint64_t w = 0; w < W; ++w) {
+                uint64_t flips = 0;
+                const uint64_t bits = j->dims - w * 64 < 64 ? j->dims - w * 64 : 64;
+                for (uint64_t k = 0; k < bits; ++k)
+                    if (word_at(j->kf, g * j->dims + w * 64 + k) < j->thresh) flips |= 1ull << k;
+                j->rows[i * W + w] = j->cen[c * W + w] ^ flips;
+            }
+        }
+    }
+    return NULL;
+}
+
+static void gen_run(gen_job proto, uint64_t n, int threads) {
+    if (threads < 1) threads = 1;
+    if (n < 1024) threads = 1;
+    gen_job* jobs = (gen_job*)calloc((size_t)threads, sizeof(gen_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = proto;
+        jobs[t].b = n * (uint64_t)t / (uint64_t)threads;
+        jobs[t].e = n * (uint64_t)(t + 1) / (uint64_t)threads;
+        if (threads == 1) gen_worker(&jobs[t]);
+        else pthread_create(&th[t], NULL, gen_worker, &jobs[t]);
+    }
+    if (threads > 1)
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+}
+
+void orc_gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
+    gen_job j;
+    memset(&j, 0, sizeof j);
+    j.kind = 0;
+    j.key = orc_rng_stream(seed, "data");
+    j.row0 = row0;
+    j.dims = dims;
+    j.words = (dims + 63) / 64;
+    j.rows = rows;
+    gen_run(j, n, threads);
+}
+
+void orc_gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
+                       uint64_t* rows, int threads) {
+    const uint64_t W = (dims + 63) / 64;
+    uint64_t* cen = (uint64_t*)malloc((centres ? centres : 1) * W * 8);
+    orc_gen_bernoulli(orc_rng_stream(seed, "centres"), 0, centres, dims, cen, threads);
+    gen_job j;
+    memset(&j, 0, sizeof j);
+    j.kind = 1;
+    j.kc = orc_rng_stream(seed, "assign");
+    j.kf = orc_rng_stream(seed, "flips");
+    j.thresh = flip_p >= 1.0 ? ~0ull : (uint64_t)(flip_p * 18446744073709551616.0);
+    j.row0 = row0;
+    j.dims = dims;
+    j.words = W;
+    j.centres = centres;
+    j.cen = cen;
+    j.rows = rows;
+    gen_run(j, n, threads);
+    free(cen);
+}
+
+void orc_gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
+                     uint64_t* qrows, uint32_t* src_out) {
+    const uint64_t W = (dims + 63) / 64;
+    const uint64_t kq = orc_rng_stream(seed, "queries");
+    const uint64_t kp = orc_rng_stream(seed, "positions");
+    uint32_t* pos = (uint32_t*)malloc((dims ? dims : 1) * 4);
+    for (uint64_t j = 0; j < nq; ++j) {
+        const uint64_t src = scale_below(word_at(kq, 2 * j), n);
+        const uint64_t k = scale_below(word_at(kq, 2 * j + 1), (uint64_t)kmax + 1);
+        memcpy(qrows + j * W, data + src * W, W * 8);
+        for (uint64_t i = 0; i < dims; ++i) pos[i] = (uint32_t)i;
+        /* k distinct positions: prefix of a Fisher-Yates shuffle */
+        for (uint64_t s = 0; s < k && s < dims; ++s) {
+            const uint64_t r = s + scale_below(word_at(kp, j * dims + s), dims - s);
+            const uint32_t tmp = pos[s];
+            pos[s] = pos[r];
+            pos[r] = tmp;
+            qrows[j * W + pos[s] / 64] ^= 1ull << (pos[s] % 64);
+        }
+        if (src_out) src_out[j] = (uint32_t)src;
+    }
+    free(pos);
+}

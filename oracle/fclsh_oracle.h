@@ -98,6 +98,14 @@ int orc_scan_truth(const uint64_t* rows, uint64_t n, const uint64_t* qrows, uint
                    uint64_t dims, uint32_t radius, int threads, uint32_t** triples_out,
                    uint64_t* count);
 
+/* BASELINE workload inputs (not reference code; identical bytes to the
+ * product's fclsh_gen_*, so CPU legs never load the product library). */
+void orc_gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
+void orc_gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
+                       uint64_t* rows, int threads);
+void orc_gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
+                     uint64_t* qrows, uint32_t* src_out);
+
 #ifdef __cplusplus
 }
 #endif

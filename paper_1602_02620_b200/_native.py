@@ -122,11 +122,15 @@ SIGNATURES = {
     "fclsh_cluster_info_get": (C.c_int, [vp, C.POINTER(ClusterInfo)]),
     "fclsh_cluster_query": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.POINTER(C.POINTER(Result))]),
     "fclsh_cluster_query_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, C.POINTER(DeviceResult)]),
+    "fclsh_cluster_stage_timing": (C.c_int, [vp, C.c_int]),
+    "fclsh_cluster_stage_ms": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_double), C.c_int]),
+    "fclsh_cluster_path_counts": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "fclsh_cluster_destroy": (None, [vp]),
     "fclsh_launch_count": (C.c_uint64, []),
     "fclsh_launch_count_reset": (None, []),
-    "fclsh_gen_bernoulli": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]),
-    "fclsh_gen_clustered": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, u64p, C.c_int]),
+    "fclsh_gen_bernoulli": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_int]),
+    "fclsh_gen_clustered": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, u64p,
+                                      C.c_int]),
     "fclsh_gen_planted": (C.c_int, [C.c_uint64, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, u64p, u32p]),
 }
 

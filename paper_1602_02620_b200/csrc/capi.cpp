@@ -22,9 +22,9 @@
 #include "cluster.hpp"
 
 namespace fclsh_b200 {
-void gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
-void gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p, uint64_t* rows,
-                   int threads);
+void gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads);
+void gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
+                   uint64_t* rows, int threads);
 void gen_planted(uint64_t seed, const uint64_t* data, uint64_t n, uint64_t dims, uint64_t nq, uint32_t kmax,
                  uint64_t* qrows, uint32_t* src_out);
 
@@ -912,27 +912,75 @@ int fclsh_cluster_query_device(fclsh_cluster* ch, const uint64_t* d_q_rows, uint
     });
 }
 
+int fclsh_cluster_stage_timing(fclsh_cluster* ch, int enable) {
+    return guarded([&] {
+        need(ch, "cluster");
+        std::lock_guard<std::mutex> lk(ch->cl->mu);
+        for (auto& m : ch->cl->members)
+            for (auto& sh : m->shards) sh.ix->stage_timing = enable != 0;
+    });
+}
+
+namespace {
+DeviceIndex& local_shard(const fclsh_cluster* ch, uint32_t k) {
+    for (auto& m : ch->cl->members) {
+        if (k < m->shards.size()) return *m->shards[k].ix;
+        k -= uint32_t(m->shards.size());
+    }
+    throw UsageError("cluster: shard out of range");
+}
+} // namespace
+
+int fclsh_cluster_stage_ms(const fclsh_cluster* ch, uint32_t shard, double* ms, int n) {
+    if (!ch || (!ms && n > 0)) {
+        g_err = "fclsh_cluster_stage_ms: NULL argument";
+        return -FCLSH_ERR_USAGE;
+    }
+    std::lock_guard<std::mutex> lk(ch->cl->mu);
+    int k = 0;
+    const int rc = guarded([&] {
+        DeviceIndex& ix = local_shard(ch, shard);
+        ix.collect_stages();
+        k = std::min(n, DeviceIndex::kStages);
+        for (int i = 0; i < k; ++i) ms[i] = ix.stage_ms[i];
+    });
+    return rc == FCLSH_OK ? k : -rc;
+}
+
+int fclsh_cluster_path_counts(const fclsh_cluster* ch, uint32_t shard, uint64_t* dense, uint64_t* general) {
+    if (!ch) {
+        g_err = "fclsh_cluster_path_counts: NULL cluster";
+        return -FCLSH_ERR_USAGE;
+    }
+    std::lock_guard<std::mutex> lk(ch->cl->mu);
+    return -guarded([&] {
+        DeviceIndex& ix = local_shard(ch, shard);
+        if (dense) *dense = ix.last_dense;
+        if (general) *general = ix.last_overflow;
+    });
+}
+
 void fclsh_cluster_destroy(fclsh_cluster* c) { delete c; }
 
 uint64_t fclsh_launch_count(void) { return launch_counter(); }
 void fclsh_launch_count_reset(void) { launch_counter() = 0; }
 
-int fclsh_gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
+int fclsh_gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
     return guarded([&] {
         if (dims == 0) throw UsageError("gen: dims must be positive");
         if (n) need(rows, "rows");
-        gen_bernoulli(seed, n, dims, rows, threads);
+        gen_bernoulli(seed, row0, n, dims, rows, threads);
     });
 }
 
-int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p, uint64_t* rows,
-                        int threads) {
+int fclsh_gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
+                        uint64_t* rows, int threads) {
     return guarded([&] {
         if (dims == 0) throw UsageError("gen: dims must be positive");
         if (centres == 0) throw UsageError("gen: need at least one centre");
         if (!(flip_p >= 0.0 && flip_p <= 1.0)) throw UsageError("gen: flip probability out of [0, 1]");
         if (n) need(rows, "rows");
-        gen_clustered(seed, centres, n, dims, flip_p, rows, threads);
+        gen_clustered(seed, centres, row0, n, dims, flip_p, rows, threads);
     });
 }
 

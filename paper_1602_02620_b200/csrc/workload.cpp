@@ -44,35 +44,38 @@ void parallel_rows(uint64_t n, int threads, F&& f) {
 
 } // namespace
 
-void gen_bernoulli(uint64_t seed, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
+// rows [row0, row0 + n) of the stream (any slice of one global dataset)
+void gen_bernoulli(uint64_t seed, uint64_t row0, uint64_t n, uint64_t dims, uint64_t* rows, int threads) {
     const uint64_t key = Rng(seed).stream("data").seed();
     const uint64_t W = (dims + 63) / 64;
     const uint64_t tail = dims % 64 ? (uint64_t(1) << (dims % 64)) - 1 : ~0ull;
     parallel_rows(n, threads, [&](uint64_t b, uint64_t e) {
         for (uint64_t i = b; i < e; ++i) {
-            for (uint64_t w = 0; w < W; ++w) rows[i * W + w] = word_at(key, i * W + w);
+            const uint64_t g = row0 + i;
+            for (uint64_t w = 0; w < W; ++w) rows[i * W + w] = word_at(key, g * W + w);
             rows[i * W + W - 1] &= tail;
         }
     });
 }
 
-void gen_clustered(uint64_t seed, uint64_t centres, uint64_t n, uint64_t dims, double flip_p, uint64_t* rows,
-                   int threads) {
+void gen_clustered(uint64_t seed, uint64_t centres, uint64_t row0, uint64_t n, uint64_t dims, double flip_p,
+                   uint64_t* rows, int threads) {
     const uint64_t W = (dims + 63) / 64;
     std::vector<uint64_t> cen(centres * W);
-    gen_bernoulli(Rng(seed).stream("centres").seed(), centres, dims, cen.data(), threads);
+    gen_bernoulli(Rng(seed).stream("centres").seed(), 0, centres, dims, cen.data(), threads);
     const uint64_t kc = Rng(seed).stream("assign").seed();
     const uint64_t kf = Rng(seed).stream("flips").seed();
     const double scaled = flip_p * 18446744073709551616.0; // 2^64
     const uint64_t thresh = flip_p >= 1.0 ? ~0ull : uint64_t(scaled);
     parallel_rows(n, threads, [&](uint64_t b, uint64_t e) {
         for (uint64_t i = b; i < e; ++i) {
-            const uint64_t c = scale(word_at(kc, i), centres);
+            const uint64_t g = row0 + i;
+            const uint64_t c = scale(word_at(kc, g), centres);
             for (uint64_t w = 0; w < W; ++w) {
                 uint64_t flips = 0;
                 const uint64_t bits = std::min<uint64_t>(64, dims - w * 64);
                 for (uint64_t k = 0; k < bits; ++k)
-                    if (word_at(kf, i * dims + w * 64 + k) < thresh) flips |= uint64_t(1) << k;
+                    if (word_at(kf, g * dims + w * 64 + k) < thresh) flips |= uint64_t(1) << k;
                 rows[i * W + w] = cen[c * W + w] ^ flips;
             }
         }

@@ -596,6 +596,25 @@ class Cluster:
             return None
         return _results_from(rp, nq)
 
+    def stage_timing(self, enable: bool = True) -> None:
+        """Per-stage CUDA events in every local shard (off by default)."""
+        _check(N.lib().fclsh_cluster_stage_timing(self._h, int(bool(enable))))
+
+    def stage_ms(self, shard: int = 0) -> dict:
+        """Stage times (ms) of the last batch on local shard `shard`."""
+        buf = (C.c_double * 8)()
+        k = N.lib().fclsh_cluster_stage_ms(self._h, shard, buf, 8)
+        if k < 0:
+            _check(-k)
+        return {name: float(buf[i]) for i, name in enumerate(IndexSet.STAGES[:k])}
+
+    def path_counts(self, shard: int = 0) -> dict:
+        dense, general = C.c_uint64(0), C.c_uint64(0)
+        rc = N.lib().fclsh_cluster_path_counts(self._h, shard, C.byref(dense), C.byref(general))
+        if rc < 0:
+            _check(-rc)
+        return {"dense": int(dense.value), "general": int(general.value)}
+
     def query_device(self, q_rows, radius: int, stream=None, nq: int | None = None):
         """Device rows in (CUDA tensor on rank 0's GPU), device results on rank 0
         (DeviceQueryResults; nq == 0 and null pointers on other ranks)."""
@@ -610,15 +629,18 @@ class Cluster:
 
 # ------------------------------------------------------------------ workloads
 
-def gen_bernoulli(seed: int, n: int, dims: int, threads: int = 8) -> np.ndarray:
+def gen_bernoulli(seed: int, n: int, dims: int, threads: int = 8, row0: int = 0) -> np.ndarray:
+    """Rows [row0, row0 + n) of the seeded Bernoulli(0.5) stream."""
     out = np.zeros((n, words_for(dims)), np.uint64)
-    _check(N.lib().fclsh_gen_bernoulli(seed, n, dims, _ptr(out, N.u64p), threads))
+    _check(N.lib().fclsh_gen_bernoulli(seed, row0, n, dims, _ptr(out, N.u64p), threads))
     return out
 
 
-def gen_clustered(seed: int, centres: int, n: int, dims: int, flip_p: float, threads: int = 8) -> np.ndarray:
+def gen_clustered(seed: int, centres: int, n: int, dims: int, flip_p: float, threads: int = 8,
+                  row0: int = 0) -> np.ndarray:
+    """Rows [row0, row0 + n) of the seeded clustered stream."""
     out = np.zeros((n, words_for(dims)), np.uint64)
-    _check(N.lib().fclsh_gen_clustered(seed, centres, n, dims, float(flip_p), _ptr(out, N.u64p), threads))
+    _check(N.lib().fclsh_gen_clustered(seed, centres, row0, n, dims, float(flip_p), _ptr(out, N.u64p), threads))
     return out
 
 

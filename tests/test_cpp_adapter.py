@@ -4,6 +4,7 @@ CPU, the full build + query on the GPU."""
 import os
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -29,8 +30,43 @@ def test_cpp_adapter_host_only(binary, oracle):
     assert f"mapping0={m[0]} seed0={s[0]}" in lines[0]
 
 
+def _read_dump(path, nq):
+    with open(path) as f:
+        lines = f.read().split("\n")
+    out, k = [], 0
+    for _ in range(2):
+        total = int(lines[k])
+        k += 1
+        per = np.array([[int(x) for x in lines[k + i].split()] for i in range(nq)], np.uint64)
+        k += nq
+        pairs = np.array([[int(x) for x in lines[k + i].split()] for i in range(total)], np.uint64).reshape(-1, 2)
+        k += total
+        out.append((per, pairs))
+    return out
+
+
 @pytest.mark.gpu
-def test_cpp_adapter_on_gpu(binary):
-    r = subprocess.run([binary], capture_output=True, text=True)
+def test_cpp_adapter_on_gpu(binary, tmp_path, oracle):
+    """The C++ caller's index and 4-shard cluster results equal the
+    reference's query_r_nn (ids, counters) and scan_truth (distances)."""
+    from oracle.workloads import OracleBackend
+    path = str(tmp_path / "dump.txt")
+    r = subprocess.run([binary, "--dump", path], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "index tables=31" in r.stdout
+    n, d, nq, radius = 20000, 128, 200, 4
+    rows = OracleBackend().gen_bernoulli(42, n, d, 4)
+    q = rows[np.arange(nq) * 100].copy()
+    for i in range(nq):
+        for b in range(i % 6):
+            q[i, b // 64] ^= np.uint64(1 << (b % 64))
+    run = oracle.stream(42, "run", 0)
+    oi = oracle.index_build(rows, d, radius, oracle.stream(run, "plan"), oracle.stream(run, "index"),
+                            override=(0, 1), prime=(1 << 31) - 1, threads=4)
+    counters, offsets, ids = oi.query(q, radius, threads=4)
+    truth = oracle.scan_truth(rows, q, d, radius, threads=4)
+    for per, pairs in _read_dump(path, nq):
+        assert (per[:, 0] == offsets[1:]).all()
+        assert (per[:, 1:] == counters).all()
+        assert (pairs[:, 0] == ids).all()
+        assert (pairs[:, 1] == truth[:, 2]).all()

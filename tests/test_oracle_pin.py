@@ -275,3 +275,28 @@ def test_golden_fixtures(orc):
         counters, offsets, ids = h.query(q, ix["radius"])
         assert counters.tolist() == ix["counters"]
         assert offsets.tolist() == ix["offsets"] and ids.tolist() == ix["ids"]
+
+
+def test_workload_generators_oracle_equals_product():
+    """oracle/workloads.py (liboracle.so's orc_gen_*) produces the product's
+    BASELINE inputs byte for byte, seed chain included, so the reference arm
+    and the CPU baselines of bench.py never load libfclsh_b200.so; slices
+    [row0, row0 + n) continue one global stream (the ranks of a cluster)."""
+    from oracle.workloads import OracleBackend, load_configs
+    from paper_1602_02620_b200 import configs as P
+    S = load_configs()
+    ob = OracleBackend()
+    for cid in (1, 2, 3, 4):
+        cfg = P.CONFIGS[cid].scaled(3000 if cid != 4 else 5000, queries=50)
+        scfg = S.CONFIGS[cid].scaled(3000 if cid != 4 else 5000, queries=50)
+        assert cfg.plan_seed() == scfg.plan_seed(ob) and cfg.index_seed() == scfg.index_seed(ob)
+        a = P.make_data(cfg, 3)
+        b = S.make_data(scfg, 5, backend=ob)
+        assert (a == b).all()
+        assert (P.make_queries(cfg, a, 2) == S.make_queries(scfg, b, 7, backend=ob)).all()
+        tail = S.make_data(scfg, 4, backend=ob, row0=1000, n=1500)
+        assert (tail == a[1000:2500]).all()
+        assert (P.make_data(cfg, 1, row0=1000, n=1500) == tail).all()
+    u = P.CONFIGS[2].scaled(2000)  # with the uniform queries
+    d = P.make_data(u)
+    assert (P.make_queries(u, d) == S.make_queries(S.CONFIGS[2].scaled(2000), d, backend=ob)).all()
