@@ -138,15 +138,16 @@ def make_data(cfg: Config, threads: int = 8, backend=None, row0: int = 0, n: int
     return b.gen_bernoulli(cfg.root(), count, cfg.dims, threads, row0=row0)
 
 
-def make_queries(cfg: Config, data: np.ndarray, threads: int = 8, backend=None) -> np.ndarray:
+def make_queries(cfg: Config, data: np.ndarray | None, threads: int = 8, backend=None,
+                 n_data: int | None = None) -> np.ndarray:
     """Planted queries (a row of `data` -- the whole dataset -- with k in [0, kmax]
     flipped bits), then uniform ones; for clustered configs, fresh draws from the
-    same cluster process (rows [len(data), len(data) + planted) of its stream:
-    independent of the data rows)."""
+    same cluster process (rows [n_data, n_data + planted) of its stream, n_data =
+    len(data) by default: independent of the data rows; `data` is not read)."""
     b = backend or _PRODUCT
     if cfg.data == "clustered":
         return b.gen_clustered(cfg.root(), cfg.centres, cfg.planted, cfg.dims, cfg.flip_p, threads,
-                               row0=data.shape[0])
+                               row0=data.shape[0] if n_data is None else n_data)
     parts = []
     if cfg.planted:
         q, _ = b.gen_planted(cfg.root(), data, cfg.dims, cfg.planted, cfg.kmax)

@@ -584,14 +584,21 @@ class Cluster:
         self._keep = data_rows  # (the library copied the rows; kept only for symmetry with IndexSet)
         return self
 
-    def query_r_nn(self, q_rows, radius: int):
-        """query_r_nn over every shard (host rows in on rank 0; None on other ranks)."""
-        q = _u64(q_rows) if q_rows is not None else np.zeros((0, 1), np.uint64)
-        if q.ndim == 1:
-            q = q.reshape(1, -1)
-        nq = q.shape[0]
+    def query_r_nn(self, q_rows, radius: int, nq: int | None = None):
+        """query_r_nn over every shard (host rows in on rank 0, where the merged
+        result comes back; other ranks pass None and the batch size `nq` and
+        get None)."""
+        if q_rows is None:
+            nq = nq or 0
+            ptr = N.u64p()
+        else:
+            q = _u64(q_rows)
+            if q.ndim == 1:
+                q = q.reshape(1, -1)
+            nq = q.shape[0]
+            ptr = _ptr(q, N.u64p)
         rp = C.POINTER(N.Result)()
-        _check(N.lib().fclsh_cluster_query(self._h, _ptr(q, N.u64p), nq, radius, C.byref(rp)))
+        _check(N.lib().fclsh_cluster_query(self._h, ptr, nq, radius, C.byref(rp)))
         if not rp:
             return None
         return _results_from(rp, nq)
