@@ -633,6 +633,10 @@ def main():
     flush = Flush(ctx.devices)
     clocks = ClockSampler(ctx.devices[0])
     spr4 = max(1, CONFIGS[4].shards // ctx.G)
+    # a small build + batch first, so the kernels' lazy module loading is not timed
+    warm = CONFIGS[2].scaled(20000, queries=100)
+    run_config(ctx, warm, "weak", 1, argparse.Namespace(**{**vars(args), "steps": 1, "no_cpu": True}), flush, stream,
+               ClockSampler(ctx.devices[0]), hbm, peak_src, threads)
 
     head, extra = run_config(ctx, CONFIGS[HEADLINE], "weak", 1, args, flush, stream, clocks, hbm, peak_src, threads,
                              headline=True)

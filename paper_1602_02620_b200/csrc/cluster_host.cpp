@@ -205,6 +205,11 @@ void cluster_build(Cluster& cl, const uint64_t* rows, bool rows_on_device, bool 
                 IndexBuildOptions o = opt;
                 o.device = m.device;
                 o.id_offset = opt.id_offset + b;
+                // the GPU's free memory shared by its shards still to build: each
+                // one picks its table layout (buckets, else CSR) within its share
+                size_t free_b = 0, total_b = 0;
+                FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+                o.mem_budget = free_b / (cl.shards_per_rank - j);
                 ClusterShard sh;
                 sh.begin = b;
                 sh.end = e;

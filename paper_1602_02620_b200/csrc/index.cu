@@ -140,6 +140,30 @@ __device__ __forceinline__ void load_bucket(const ulonglong2* bp, ulonglong2 (&x
         : "l"(bp + 2));
 }
 
+// Hamming distance (bitvec.cpp:73-79) of a stored row and a query row with
+// vector loads: vec = 4 -> 256-bit loads (W % 4 == 0, 32-B aligned rows: a
+// d = 256 row is one load, one 32-B sector), 2 -> 128-bit, 1 -> 64-bit.
+__device__ __forceinline__ uint32_t row_distance(const uint64_t* r, const uint64_t* q, uint32_t words, int vec) {
+    uint32_t d = 0;
+    if (vec == 4) {
+        for (uint32_t w = 0; w < words; w += 4) {
+            unsigned long long a0, a1, a2, a3, b0, b1, b2, b3;
+            asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(r + w));
+            asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(b0), "=l"(b1), "=l"(b2), "=l"(b3) : "l"(q + w));
+            d += __popcll(a0 ^ b0) + __popcll(a1 ^ b1) + __popcll(a2 ^ b2) + __popcll(a3 ^ b3);
+        }
+    } else if (vec == 2) {
+        for (uint32_t w = 0; w < words; w += 2) {
+            const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(r + w));
+            const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(q + w));
+            d += __popcll(a.x ^ b.x) + __popcll(a.y ^ b.y);
+        }
+    } else {
+        for (uint32_t w = 0; w < words; ++w) d += __popcll(__ldg(r + w) ^ __ldg(q + w));
+    }
+    return d;
+}
+
 // Read-only view of one shard's tables, passed by value to the kernels.
 template <typename T>
 struct Tables {
@@ -814,6 +838,179 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
             const uint64_t* qr = qrows + q * words;
             for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __ldg(qr + w));
         }
+        const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
+        const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
+        if (over || nfound > slot_cap) {
+            if (lane == 0) {
+                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                found_q[q] = 0; // written by the CTA kernel later
+                src_pos[q] = 0;
+            }
+            continue;
+        }
+        // ascending ids: bitonic sort across the warp (non-passes = +inf)
+        unsigned long long mine = pass ? (static_cast<unsigned long long>(list) << 32) | dist : ~0ull;
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(kAll, mine, j);
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
+                mine = (lower == up) ? lo : hi;
+            }
+        }
+        if (uint32_t(lane) < nfound) {
+            tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
+            tmp_dist[q * slot_cap + lane] = uint32_t(mine);
+        }
+        if (lane == 0) {
+            coll_q[q] = m;
+            cand_q[q] = nd;
+            found_q[q] = nfound;
+            if (hc) {
+                hc[(nq + 1) + q] = m;
+                hc[2 * (nq + 1) + q] = nd;
+                hc[3 * (nq + 1) + q] = nfound;
+            }
+            src_pos[q] = q * slot_cap;
+            if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
+        }
+    }
+}
+
+// Warp per query with the probe rounds software-pipelined (buckets layout;
+// the default for indexes of <= 640 tables). k_query_warp walks the tables in
+// rounds of 32 x U, and every round is a chain of three dependent memory
+// trips: the round's keys, their L2 filter words, then the random bucket
+// reads. Here the three stages of consecutive rounds overlap: while round c's
+// bucket reads are in flight the warp has already issued round c+1's filter
+// words (keys loaded a round earlier) and round c+2's keys, so a round waits
+// on its bucket reads only (reference loop replaced: index.cpp:169-177).
+// Dedup, counters, verify and outputs are k_query_warp's.
+#ifndef FCLSH_WARP_PF_MINB
+#define FCLSH_WARP_PF_MINB 5
+#endif
+template <typename T, int U>
+__global__ void __launch_bounds__(256, FCLSH_WARP_PF_MINB) k_query_warp_pf(
+    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
+    const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
+    uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
+    unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
+    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
+    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum,
+    const unsigned long long* __restrict__ desc, int vec_rows) {
+    using E = typename T::E;
+    using K = typename T::K;
+    constexpr unsigned kAll = 0xffffffffu;
+    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+    constexpr uint32_t kStep = 32 * U; // tables per round
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
+    const int lane = threadIdx.x & 31;
+    const uint64_t fpol = l2_evict_last_policy();
+    const uint64_t bpol = l2_evict_first_policy();
+    pdl_trigger();
+    pdl_wait(); // the batch's keys (hash kernel) are complete from here on
+    auto fetch = [&]() -> uint64_t {
+        unsigned int v = 0;
+        if (lane == 0) v = atomicAdd(qnext, 1u);
+        return __shfl_sync(kAll, v, 0);
+    };
+    for (uint64_t q = fetch(); q < nq; q = fetch()) {
+        const K* qk = qkeys + q * tables;
+        uint32_t list = kEmpty; // this lane's distinct id (lane < nd)
+        uint32_t nd = 0;        // distinct ids so far (warp-uniform)
+        bool over = false;      // more than 32 distinct ids (warp-uniform)
+        uint32_t coll = 0;      // this lane's postings
+        auto offer = [&](bool has, uint32_t id) {
+            coll += has;
+            if (!__any_sync(kAll, has) || over) return;
+            bool seen = false;
+            for (uint32_t k = 0; k < nd; ++k) seen |= __shfl_sync(kAll, list, k) == id;
+            const bool fresh = has && !seen;
+            const uint32_t grp = __match_any_sync(kAll, fresh ? id : kEmpty);
+            const uint32_t lead = __ballot_sync(kAll, fresh && __ffs(grp) - 1 == lane);
+            if (!lead) return;
+            if (nd + __popc(lead) > 32) {
+                over = true;
+                return;
+            }
+            for (uint32_t b = lead; b; b &= b - 1) {
+                const uint32_t v = __shfl_sync(kAll, id, __ffs(b) - 1);
+                if (uint32_t(lane) == nd) list = v;
+                ++nd;
+            }
+        };
+        // the pipeline: keys of rounds c, c+1, c+2 and the filter result of c+1
+        K k0[U], k1[U], k2[U];
+        bool p1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t0 = u * 32 + lane, t1 = kStep + t0;
+            k0[u] = t0 < tables ? qk[t0] : K(0);
+            k1[u] = t1 < tables ? qk[t1] : K(0);
+        }
+        bool p0[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t t = u * 32 + lane;
+            p0[u] = t < tables && (!tb.filter || filter_pass(tb, t, uint64_t(k0[u]), fpol));
+        }
+        for (uint32_t base_t = 0; base_t < tables && !over; base_t += kStep) {
+            E sl[U][kSlots];
+#pragma unroll
+            for (int u = 0; u < U; ++u) { // round c: U home buckets in flight
+                const uint32_t t = base_t + u * 32 + lane;
+                if (p0[u]) {
+                    load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + home_of(uint64_t(k0[u]), tb)) * kSlots,
+                                      sl[u], bpol);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) { // round c+1: filter words; round c+2: keys
+                const uint32_t t1 = base_t + kStep + u * 32 + lane, t2 = t1 + kStep;
+                p1[u] = t1 < tables && (!tb.filter || filter_pass(tb, t1, uint64_t(k1[u]), fpol));
+                k2[u] = t2 < tables ? qk[t2] : K(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t kk = uint64_t(k0[u]);
+                const bool live = p0[u];
+#pragma unroll
+                for (int j = 0; j < kSlots; ++j)
+                    offer(live && !T::empty(sl[u][j]) && T::key(sl[u][j]) == kk, T::id(sl[u][j]));
+                // the run continues into the next bucket (~3 %)
+                bool cont = live && !T::empty(sl[u][kSlots - 1]);
+                uint64_t b = home_of(kk, tb) + 1;
+                const E* base = tb.data + uint64_t(base_t + u * 32 + lane) * tb.nbuckets * kSlots;
+                while (__any_sync(kAll, cont)) {
+                    E x[kSlots];
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j) x[j] = T::make(~0ull, ~0u);
+                    b &= tb.nbuckets - 1;
+                    if (cont) load_bucket(base + b * kSlots, x);
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j) offer(cont && !T::empty(x[j]) && T::key(x[j]) == kk, T::id(x[j]));
+                    cont = cont && !T::empty(x[kSlots - 1]);
+                    ++b;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                k0[u] = k1[u];
+                p0[u] = p1[u];
+                k1[u] = k2[u];
+            }
+        }
+        const uint64_t m = __reduce_add_sync(kAll, coll);
+        // verify the listed ids, one per lane
+        uint32_t dist = 0;
+        if (!over && uint32_t(lane) < nd)
+            dist = row_distance(rows + uint64_t(list) * words, qrows + q * words, words, vec_rows);
         const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
         const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
         if (over || nfound > slot_cap) {
@@ -1536,6 +1733,15 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
 
 uint32_t bit_length(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
 
+// vector width of the verify's row loads (row_distance): every stored row is
+// W words at a cudaMalloc'd base; the query rows' base must be aligned too
+int vec_for(uint32_t words, const void* q) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(q);
+    if (words % 4 == 0 && a % 32 == 0) return 4;
+    if (words % 2 == 0 && a % 16 == 0) return 2;
+    return 1;
+}
+
 unsigned grid_for(uint64_t work, int device, unsigned threads = 256, unsigned per_sm = 8) {
     const uint64_t want = (work + threads - 1) / threads;
     return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sm_count(device)) * per_sm)));
@@ -1649,6 +1855,27 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     // default: the id list in registers (no shared memory, all of L1 for the
     // probes in flight); FCLSH_FUSED_SHARED=1 selects the shared-set kernel
     static const bool shared_set = getenv("FCLSH_FUSED_SHARED") != nullptr;
+    static const bool v1 = getenv("FCLSH_WARP_V1") != nullptr; // A/B: the unpipelined warp kernel
+    if (!shared_set && !v1 && LAYOUT == kLayoutBuckets) {
+        const int vec = vec_for(ix.row_words, d_q);
+        auto go = [&](auto kern) {
+            static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
+            const uint64_t bit = uint64_t(1) << (ix.device & 63);
+            if (!(carved.load(std::memory_order_acquire) & bit)) {
+                FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+                carved.fetch_or(bit, std::memory_order_acq_rel);
+            }
+            const int per_sm = resident_ctas(kern, 256, 0, ix.device);
+            const uint64_t grid = std::max<uint64_t>(
+                1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
+            launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
+                       ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
+                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec);
+            FCLSH_LAUNCHED();
+        };
+        go(k_query_warp_pf<T, kFusedU>);
+        return;
+    }
     if (!shared_set) {
         auto kern = k_query_warp<T, LAYOUT, kFusedU>;
         static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
@@ -2150,6 +2377,7 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     {
         size_t free_b = 0, total_b = 0;
         FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (opt.mem_budget) free_b = std::min<size_t>(free_b, opt.mem_budget); // (several shards on one GPU)
         const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * (ix->wide ? 8 : 4) + (uint64_t(2) << 30);
         if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) ++bb;
         if (layout == kLayoutAuto)

@@ -120,6 +120,7 @@ struct IndexBuildOptions {
     uint64_t id_offset = 0;
     int directory_bits = 0;
     int layout = kLayoutAuto;
+    uint64_t mem_budget = 0; // device bytes this build may take (0: the free memory); picks the layout
 };
 
 // build_index(data, covering_batch, radius, plan, Rng(rng_seed), opt).
