@@ -112,6 +112,20 @@ int fclsh_hash_batch(const fclsh_family* f, const uint64_t* d_rows, uint64_t n,
 int fclsh_hash_batch_host(const fclsh_family* f, const uint64_t* rows, uint64_t n,
                           uint32_t row_words, void* keys, uint32_t key_bytes, int device);
 
+/* ------------------------------------------------------ classic family ---
+ * Bit-sampling LSH, the paper's classic baseline (classic.hpp:15-50). */
+/* choose_k(dims, radius, tables, delta) (classic.cpp:10-23). */
+int fclsh_choose_k(uint64_t dims, uint32_t radius, uint64_t tables, double delta, uint32_t* out);
+/* build_bit_sample_family(dims, k, tables, Rng(rng_seed), prime)
+ * (classic.cpp:25-46): positions / seeds [tables * k]. */
+int fclsh_bitsample_family_build(uint64_t dims, uint32_t k, uint64_t tables, uint64_t rng_seed, uint64_t prime,
+                                 uint32_t* positions, uint64_t* seeds);
+/* hash_tables_into (classic.cpp:48-63) for n host rows on the device:
+ * keys [n][tables] (u64), synchronous. */
+int fclsh_hash_tables_batch(uint64_t dims, uint32_t k, uint64_t tables, const uint32_t* positions,
+                            const uint64_t* seeds, uint64_t prime, const uint64_t* rows, uint64_t n, uint64_t* keys,
+                            int device);
+
 /* ------------------------------------------------------------------ plan ---
  * PreprocessPlan (transform.hpp:26-44) */
 typedef struct fclsh_plan fclsh_plan;
@@ -153,7 +167,17 @@ typedef struct {
     uint64_t id_offset;          /* added to every reported id (shards) */
     int32_t directory_bits;      /* CSR layout: 0 = automatic */
     int32_t layout;              /* FCLSH_TABLES_* */
+    int32_t method;              /* FCLSH_METHOD_* (Method, index.hpp:22) */
+    double delta;                /* IndexOptions::delta (classic; default 0.1) */
+    uint32_t k_override;         /* IndexOptions::k_override (classic; 0 = unset) */
+    uint64_t tables_override;    /* IndexOptions::tables_override (classic; 0 = unset) */
 } fclsh_index_options;
+
+/* Method (index.hpp:22). COVERING = covering_batch; covering_reference
+ * (bcLSH) builds identical buckets (index.hpp:17-22), so it is COVERING too.
+ * CLASSIC = bit-sampling LSH (classic.hpp) over the identity plan. */
+#define FCLSH_METHOD_COVERING 0
+#define FCLSH_METHOD_CLASSIC 2
 
 /* Device table layouts (same query results):
  * BUCKETS  open-addressed buckets of four postings, one random 32-byte read
@@ -183,10 +207,15 @@ typedef struct {
     double build_ms; /* device time of the last build, CUDA events */
     int32_t layout;  /* FCLSH_TABLES_CSR or FCLSH_TABLES_BUCKETS */
     uint64_t buckets_per_table;
+    int32_t method;     /* FCLSH_METHOD_* */
+    uint32_t classic_k; /* bits sampled per table (classic) */
 } fclsh_index_info;
 int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out);
-/* Part p's family (a new handle the caller destroys). */
+/* Part p's family (a new handle the caller destroys; covering indexes). */
 int fclsh_index_family(const fclsh_index* ix, uint32_t part, fclsh_family** out);
+/* A classic index's bit-sampling family: positions / seeds [tables * k]
+ * (either may be NULL). */
+int fclsh_index_bitsample_family(const fclsh_index* ix, uint32_t* positions, uint64_t* seeds);
 void fclsh_index_destroy(fclsh_index* ix);
 
 /* ----------------------------------------------------------------- query ---

@@ -116,6 +116,18 @@ class Oracle:
                                       C.c_char_p, C.c_uint32, C.c_double, C.c_int, C.c_uint32, C.c_uint64,
                                       C.c_uint32, C.c_int, C.c_uint64, C.POINTER(C.c_double),
                                       C.POINTER(C.c_char_p)]
+            self._choose_k = f("choose_k")
+            self._choose_k.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, u32p]
+            self._bsf = f("bitsample_family")
+            self._bsf.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, u32p, u64p]
+            self._hash_tables = f("hash_tables")
+            self._hash_tables.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, u32p, u64p, C.c_uint64, u64p,
+                                          C.c_uint64, u64p, C.c_int]
+            self._build_classic = f("index_build_classic")
+            self._build_classic.restype = C.c_void_p
+            self._build_classic.argtypes = [u64p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, C.c_double,
+                                            C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_uint32,
+                                            C.c_uint64, C.POINTER(C.c_int)]
             self._hist = f("distance_histogram")
             self._hist.argtypes = [u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p]
         else:
@@ -226,6 +238,35 @@ class Oracle:
             h = self._index_build(_p(rows, u64p), n, dims, radius, plan_seed,
                                   int(override is not None), ok, ot, c, index_seed, prime,
                                   int(include_zero), budget, threads, C.byref(code))
+        self._check(code.value)
+        return OracleIndex(self, h, dims)
+
+    # ----------------------------------------- classic (compiled reference only)
+    def choose_k(self, dims, radius, tables, delta):
+        out = C.c_uint32(0)
+        self._check(self._choose_k(dims, radius, tables, float(delta), C.byref(out)))
+        return int(out.value)
+
+    def bitsample_family(self, dims, k, tables, seed, prime=(1 << 61) - 1):
+        pos = np.zeros(tables * k, np.uint32)
+        seeds = np.zeros(tables * k, np.uint64)
+        self._check(self._bsf(dims, k, tables, seed, prime, _p(pos, u32p), _p(seeds, u64p)))
+        return pos, seeds
+
+    def hash_tables(self, dims, k, tables, positions, seeds, prime, rows, threads=1):
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        out = np.zeros((rows.shape[0], tables), np.uint64)
+        self._check(self._hash_tables(dims, k, tables, _p(np.ascontiguousarray(positions, np.uint32), u32p),
+                                      _p(np.ascontiguousarray(seeds, np.uint64), u64p), prime, _p(rows, u64p),
+                                      rows.shape[0], _p(out, u64p), threads))
+        return out
+
+    def index_build_classic(self, rows, dims, radius, plan_seed, index_seed, prime=(1 << 61) - 1, c=1.0,
+                            budget=1 << 21, delta=0.1, k_override=0, tables_override=0):
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        code = C.c_int(0)
+        h = self._build_classic(_p(rows, u64p), rows.shape[0], dims, radius, plan_seed, c, index_seed, prime, budget,
+                                delta, k_override, tables_override, C.byref(code))
         self._check(code.value)
         return OracleIndex(self, h, dims)
 

@@ -19,6 +19,8 @@
 //   ref_dataset_save / ref_dataset_load -> fclsh::save_dataset[_text] /
 //                         fclsh::load_dataset             (dataset.cpp:82-111)
 //   ref_fht_mod / ref_batch_hash_kernel -> hadamard.cpp:51-72
+//   ref_choose_k / ref_bitsample_family / ref_hash_tables -> classic.cpp:10-63
+//   ref_index_build_classic -> fclsh::build_index(Method::classic) (index.cpp:65-76)
 //
 // Rows cross the boundary as row-major uint64 words, bit i of a row in word
 // i/64 at offset i%64 (the BitVector layout, bitvec.hpp:13-19).
@@ -32,6 +34,7 @@
 
 #include "fclsh/bench.hpp"
 #include "fclsh/bitvec.hpp"
+#include "fclsh/classic.hpp"
 #include "fclsh/covering.hpp"
 #include "fclsh/dataset.hpp"
 #include "fclsh/errors.hpp"
@@ -518,6 +521,65 @@ int ref_run_experiment(const uint64_t* rows, uint64_t n, const uint64_t* qrows, 
         // from oracle/_ref/ref_write_metrics instead)
         (void)csv_out;
     });
+}
+
+// ---------------------------------------------------------- classic.cpp
+int ref_choose_k(uint64_t dims, uint32_t radius, uint64_t tables, double delta, uint32_t* out) {
+    return guarded([&] { *out = choose_k(dims, radius, tables, delta); });
+}
+
+// build_bit_sample_family(dims, k, tables, Rng(seed), prime): positions / seeds [tables * k]
+int ref_bitsample_family(uint64_t dims, uint32_t k, uint64_t tables, uint64_t seed, uint64_t prime,
+                         uint32_t* positions, uint64_t* seeds) {
+    return guarded([&] {
+        Rng rng(seed);
+        BitSampleFamily f = build_bit_sample_family(dims, k, tables, rng, prime);
+        std::copy(f.positions.begin(), f.positions.end(), positions);
+        std::copy(f.seeds.begin(), f.seeds.end(), seeds);
+    });
+}
+
+// hash_tables_into for every row: out [n][tables]
+int ref_hash_tables(uint64_t dims, uint32_t k, uint64_t tables, const uint32_t* positions, const uint64_t* seeds,
+                    uint64_t prime, const uint64_t* rows, uint64_t n, uint64_t* out, int threads) {
+    return guarded([&] {
+        BitSampleFamily f;
+        f.dims = dims;
+        f.k = k;
+        f.tables = tables;
+        f.prime = prime;
+        f.positions.assign(positions, positions + tables * k);
+        f.seeds.assign(seeds, seeds + tables * k);
+        Dataset ds = rows_to_dataset(rows, n, dims, threads);
+        parallel_for(n, threads, [&](uint64_t i, int) {
+            hash_tables_into(f, ds[i], std::span<uint64_t>(out + i * tables, tables));
+        });
+    });
+}
+
+// make_plan(dims, radius, c, n, Rng(plan_seed), identity) + build_index(data,
+// Method::classic, radius, plan, Rng(index_seed), {prime, budget, delta,
+// k_override, tables_override}) -- single-threaded, the reference's own.
+void* ref_index_build_classic(const uint64_t* rows, uint64_t n, uint64_t dims, uint32_t radius, uint64_t plan_seed,
+                              double c, uint64_t index_seed, uint64_t prime, uint64_t budget, double delta,
+                              uint32_t k_override, uint64_t tables_override, int* code) {
+    RefIndex* h = nullptr;
+    *code = guarded([&] {
+        auto idx = std::make_unique<RefIndex>();
+        idx->data = rows_to_dataset(rows, n, dims, 8);
+        Rng plan_rng(plan_seed);
+        idx->plan = make_plan(dims, radius, c, n, plan_rng, PlanOverride{PlanKind::identity, 1}, budget);
+        IndexOptions opt;
+        opt.prime = prime;
+        opt.table_budget = budget;
+        opt.delta = delta;
+        if (k_override) opt.k_override = k_override;
+        if (tables_override) opt.tables_override = tables_override;
+        Rng rng(index_seed);
+        idx->index = build_index(idx->data, Method::classic, radius, idx->plan, rng, opt);
+        h = idx.release();
+    });
+    return h;
 }
 
 } // extern "C"

@@ -37,13 +37,15 @@ class PlanInfo(C.Structure):
 class IndexOptions(C.Structure):
     _fields_ = [("prime", C.c_uint64), ("include_zero_column", C.c_int32), ("table_budget", C.c_uint64),
                 ("device", C.c_int32), ("id_offset", C.c_uint64), ("directory_bits", C.c_int32),
-                ("layout", C.c_int32)]
+                ("layout", C.c_int32), ("method", C.c_int32), ("delta", C.c_double), ("k_override", C.c_uint32),
+                ("tables_override", C.c_uint64)]
 
 
 class IndexInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("dims", C.c_uint64), ("radius", C.c_uint32), ("table_count", C.c_uint64),
                 ("entry_count", C.c_uint64), ("directory_bits", C.c_uint32), ("device_bytes", C.c_uint64),
-                ("build_ms", C.c_double), ("layout", C.c_int32), ("buckets_per_table", C.c_uint64)]
+                ("build_ms", C.c_double), ("layout", C.c_int32), ("buckets_per_table", C.c_uint64),
+                ("method", C.c_int32), ("classic_k", C.c_uint32)]
 
 
 class Result(C.Structure):
@@ -92,6 +94,12 @@ SIGNATURES = {
     "fclsh_index_info_get": (C.c_int, [vp, C.POINTER(IndexInfo)]),
     "fclsh_index_family": (C.c_int, [vp, C.c_uint32, C.POINTER(vp)]),
     "fclsh_index_destroy": (None, [vp]),
+    "fclsh_index_bitsample_family": (C.c_int, [vp, u32p, u64p]),
+    "fclsh_choose_k": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, u32p]),
+    "fclsh_bitsample_family_build": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, u32p,
+                                               u64p]),
+    "fclsh_hash_tables_batch": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, u32p, u64p, C.c_uint64, u64p,
+                                          C.c_uint64, u64p, C.c_int]),
     "fclsh_query": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.POINTER(C.POINTER(Result))]),
     "fclsh_result_free": (None, [C.POINTER(Result)]),
     "fclsh_query_c_r_nn": (C.c_int, [vp, u64p, C.c_uint64, C.c_uint32, C.c_int64, u64p, u32p]),

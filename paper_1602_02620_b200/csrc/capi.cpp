@@ -460,6 +460,10 @@ void fclsh_index_options_default(fclsh_index_options* o) {
     o->id_offset = 0;
     o->directory_bits = 0;
     o->layout = FCLSH_TABLES_AUTO;
+    o->method = FCLSH_METHOD_COVERING;
+    o->delta = 0.1;
+    o->k_override = 0;
+    o->tables_override = 0;
 }
 
 int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint64_t dims, uint32_t radius,
@@ -479,6 +483,10 @@ int fclsh_index_build(const uint64_t* rows, int rows_on_device, uint64_t n, uint
         bo.id_offset = o.id_offset;
         bo.directory_bits = o.directory_bits;
         bo.layout = o.layout;
+        bo.method = o.method;
+        bo.delta = o.delta;
+        bo.k_override = o.k_override;
+        bo.tables_override = o.tables_override;
         auto h = std::make_unique<fclsh_index>();
         h->ix = build_index(rows, rows_on_device != 0, n, dims, radius, plan->p, rng_seed, bo);
         *out = h.release();
@@ -500,6 +508,8 @@ int fclsh_index_info_get(const fclsh_index* ix, fclsh_index_info* out) {
         out->build_ms = d.build_ms;
         out->layout = d.layout;
         out->buckets_per_table = d.nbuckets;
+        out->method = d.method;
+        out->classic_k = d.fs->classic ? d.fs->cls_k : 0;
     });
 }
 
@@ -507,6 +517,7 @@ int fclsh_index_family(const fclsh_index* ix, uint32_t part, fclsh_family** out)
     return guarded([&] {
         need(ix, "index");
         need(out, "out");
+        if (ix->ix->fs->classic) throw UsageError("index: a classic index holds a bit-sampling family");
         if (part >= ix->ix->fs->parts) throw UsageError("index: part out of range");
         auto h = std::make_unique<fclsh_family>();
         h->f = ix->ix->fs->families[part];
@@ -514,7 +525,67 @@ int fclsh_index_family(const fclsh_index* ix, uint32_t part, fclsh_family** out)
     });
 }
 
+int fclsh_index_bitsample_family(const fclsh_index* ix, uint32_t* positions, uint64_t* seeds) {
+    return guarded([&] {
+        need(ix, "index");
+        if (!ix->ix->fs->classic) throw UsageError("index: not a classic index");
+        const BitSampleFamily& f = ix->ix->fs->classic_family;
+        if (positions) std::memcpy(positions, f.positions.data(), f.positions.size() * 4);
+        if (seeds) std::memcpy(seeds, f.seeds.data(), f.seeds.size() * 8);
+    });
+}
+
 void fclsh_index_destroy(fclsh_index* ix) { delete ix; }
+
+int fclsh_choose_k(uint64_t dims, uint32_t radius, uint64_t tables, double delta, uint32_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = choose_k(dims, radius, tables, delta);
+    });
+}
+
+int fclsh_bitsample_family_build(uint64_t dims, uint32_t k, uint64_t tables, uint64_t rng_seed, uint64_t prime,
+                                 uint32_t* positions, uint64_t* seeds) {
+    return guarded([&] {
+        const BitSampleFamily f = build_bit_sample_family(dims, k, tables, rng_seed, prime);
+        if (positions) std::memcpy(positions, f.positions.data(), f.positions.size() * 4);
+        if (seeds) std::memcpy(seeds, f.seeds.data(), f.seeds.size() * 8);
+    });
+}
+
+int fclsh_hash_tables_batch(uint64_t dims, uint32_t k, uint64_t tables, const uint32_t* positions,
+                            const uint64_t* seeds, uint64_t prime, const uint64_t* rows, uint64_t n, uint64_t* keys,
+                            int device) {
+    return guarded([&] {
+        if (dims == 0) throw UsageError("bit sample family: dims must be positive");
+        if (k == 0) throw UsageError("bit sample family: k must be >= 1");
+        if (tables == 0) throw UsageError("bit sample family: need at least one table");
+        if (prime < 3 || prime % 2 == 0) throw UsageError("bit sample family: prime must be odd and > 2");
+        need(positions, "positions");
+        need(seeds, "seeds");
+        BitSampleFamily f;
+        f.dims = dims;
+        f.k = k;
+        f.tables = tables;
+        f.prime = prime;
+        f.positions.assign(positions, positions + tables * uint64_t(k));
+        f.seeds.assign(seeds, seeds + tables * uint64_t(k));
+        for (uint32_t p : f.positions)
+            if (p >= dims) throw UsageError("bit sample family: position out of range");
+        if (n == 0) return;
+        need(rows, "rows");
+        need(keys, "keys");
+        FCLSH_CUDA(cudaSetDevice(device));
+        auto fs = make_device_classic_set(f, device);
+        const uint64_t W = (dims + 63) / 64;
+        DevBuf dr, dk;
+        dr.ensure(n * W * 8);
+        dk.ensure(n * tables * 8);
+        FCLSH_CUDA(cudaMemcpy(dr.p, rows, n * W * 8, cudaMemcpyHostToDevice));
+        hash_rows(*fs, dr.as<uint64_t>(), n, dk.p, 8, tables, kLayoutPointMajor, nullptr);
+        FCLSH_CUDA(cudaMemcpy(keys, dk.p, n * tables * 8, cudaMemcpyDeviceToHost));
+    });
+}
 
 int fclsh_query(fclsh_index* ixh, const uint64_t* q_rows, uint64_t nq, uint32_t radius, fclsh_result** out) {
     return guarded([&] {
@@ -812,6 +883,10 @@ int fclsh_cluster_build(fclsh_cluster* ch, const uint64_t* rows, int rows_on_dev
         bo.id_offset = o.id_offset;
         bo.directory_bits = o.directory_bits;
         bo.layout = o.layout;
+        bo.method = o.method;
+        bo.delta = o.delta;
+        bo.k_override = o.k_override;
+        bo.tables_override = o.tables_override;
         cluster_build(*ch->cl, rows, rows_on_device != 0, rows_scope == FCLSH_ROWS_GLOBAL, n, dims, radius, plan->p,
                       rng_seed, bo);
     });

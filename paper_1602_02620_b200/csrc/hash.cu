@@ -1198,6 +1198,61 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
     return fs;
 }
 
+namespace {
+// hash_tables_into (classic.cpp:48-63) for n rows: thread per (row, table),
+// consecutive threads on consecutive tables of a row (point-major keys
+// coalesce); key = sum of the seeds at the set sampled positions mod prime,
+// reduced term by term (every partial sum < prime < 2^63: the same residue
+// as the reference's 128-bit sum % prime).
+__global__ void __launch_bounds__(256) k_hash_classic(const uint64_t* __restrict__ rows, uint64_t n, uint32_t words,
+                                                      uint64_t tables, uint32_t k, const uint32_t* __restrict__ pos,
+                                                      const uint64_t* __restrict__ seeds, uint64_t prime,
+                                                      void* __restrict__ keys, uint64_t key_stride, int layout,
+                                                      int key_bytes) {
+    const uint64_t total = n * tables;
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < total;
+         x += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = x / tables, t = x % tables;
+        const uint64_t* r = rows + i * words;
+        const uint32_t* p = pos + t * k;
+        const uint64_t* sd = seeds + t * k;
+        uint64_t acc = 0;
+        for (uint32_t j = 0; j < k; ++j) {
+            const uint32_t b = __ldg(p + j);
+            const uint64_t bit = (__ldg(r + (b >> 6)) >> (b & 63)) & 1;
+            acc += __ldg(sd + j) & (0ull - bit);
+            acc = acc >= prime ? acc - prime : acc;
+        }
+        const uint64_t dst = layout == kLayoutPointMajor ? i * key_stride + t : t * key_stride + i;
+        if (key_bytes == 4)
+            static_cast<uint32_t*>(keys)[dst] = uint32_t(acc);
+        else
+            static_cast<uint64_t*>(keys)[dst] = acc;
+    }
+}
+} // namespace
+
+std::unique_ptr<DeviceFamilySet> make_device_classic_set(const BitSampleFamily& f, int device) {
+    if (f.prime >= (uint64_t(1) << 63)) throw UsageError("hash: primes >= 2^63 are not supported");
+    auto fs = std::make_unique<DeviceFamilySet>();
+    fs->device = device;
+    fs->parts = 1;
+    fs->classic = true;
+    fs->cls_k = f.k;
+    fs->tables = f.tables;
+    fs->prime = f.prime;
+    fs->dims = f.dims;
+    fs->row_words = uint32_t((f.dims + 63) / 64);
+    fs->max_part_dims = f.dims;
+    FCLSH_CUDA(cudaSetDevice(device));
+    fs->cls_pos.ensure(f.positions.size() * 4);
+    fs->cls_seed.ensure(f.seeds.size() * 8);
+    FCLSH_CUDA(cudaMemcpy(fs->cls_pos.p, f.positions.data(), f.positions.size() * 4, cudaMemcpyHostToDevice));
+    FCLSH_CUDA(cudaMemcpy(fs->cls_seed.p, f.seeds.data(), f.seeds.size() * 8, cudaMemcpyHostToDevice));
+    fs->classic_family = f;
+    return fs;
+}
+
 std::unique_ptr<DeviceFamilySet> make_device_family_set(const Family& f, int device) {
     Plan plan;
     plan.kind = PlanKind::identity;
@@ -1222,6 +1277,20 @@ void hash_rows(DeviceFamilySet& fs, const uint64_t* d_rows, uint64_t n, void* d_
         throw UsageError("hash: key_stride below the table count");
     if (n == 0) return;
     FCLSH_CUDA(cudaSetDevice(fs.device));
+    if (fs.classic) {
+        if (rows_copy) {
+            FCLSH_CUDA(cudaMemcpyAsync(rows_copy, d_rows, n * fs.row_words * 8, cudaMemcpyDefault, stream));
+            d_rows = rows_copy;
+        }
+        const uint64_t work = n * fs.tables;
+        const unsigned grid = unsigned(std::max<uint64_t>(
+            1, std::min<uint64_t>((work + 255) / 256, uint64_t(sm_count(fs.device)) * 8)));
+        k_hash_classic<<<grid, 256, 0, stream>>>(d_rows, n, fs.row_words, fs.tables, fs.cls_k,
+                                                fs.cls_pos.as<uint32_t>(), fs.cls_seed.as<uint64_t>(), fs.prime,
+                                                d_keys, key_stride, layout, int(key_bytes));
+        FCLSH_LAUNCHED();
+        return;
+    }
     if (rows_copy && !fs.fast) {
         // only k_hash_f64_pt copies as it goes: copy first, hash the copy
         FCLSH_CUDA(cudaMemcpyAsync(rows_copy, d_rows, n * fs.row_words * 8, cudaMemcpyDefault, stream));

@@ -46,6 +46,15 @@ struct DeviceFamilySet {
     uint64_t max_part_dims = 0;
     DevBuf scratch;  // generic path workspace
 
+    // Classic bit sampling (Method::classic, classic.hpp): one part of
+    // `tables` tables, k sampled positions each; hash_rows runs
+    // k_hash_classic (hash_tables_into, classic.cpp:48-63).
+    bool classic = false;
+    uint32_t cls_k = 0;
+    DevBuf cls_pos;  // uint32 [tables][k]
+    DevBuf cls_seed; // uint64 [tables][k]
+    BitSampleFamily classic_family; // host copy
+
     uint64_t total_tables() const { return uint64_t(parts) * tables; }
 };
 
@@ -53,6 +62,8 @@ struct DeviceFamilySet {
 // (families[p].dims == plan.part_dims(p)).
 std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan,
                                                         std::vector<Family> families, int device);
+// The classic bit-sampling family over rows of f.dims bits (identity plan).
+std::unique_ptr<DeviceFamilySet> make_device_classic_set(const BitSampleFamily& f, int device);
 // A single family over rows of exactly f.dims bits (identity plan).
 std::unique_ptr<DeviceFamilySet> make_device_family_set(const Family& f, int device);
 

@@ -206,4 +206,42 @@ Plan make_plan(uint64_t dims, uint32_t radius, double c, uint64_t n, uint64_t rn
     return plan;
 }
 
+uint32_t choose_k(uint64_t dims, uint32_t radius, uint64_t tables, double delta) {
+    if (dims == 0) throw UsageError("choose_k: dims must be positive");
+    if (radius == 0 || radius >= dims) throw UsageError("choose_k: radius must be in [1, dims)");
+    if (tables == 0) throw UsageError("choose_k: need at least one table");
+    if (!(delta > 0.0 && delta < 1.0)) throw UsageError("choose_k: delta must be in (0, 1)");
+    // k = ceil(log(1 - delta^(1/L)) / log(1 - r/d)), clamped into [1, 4d]
+    const double per_table = 1.0 - std::exp(std::log(delta) / static_cast<double>(tables));
+    const double raw = std::log(per_table) / std::log1p(-static_cast<double>(radius) / static_cast<double>(dims));
+    const double k = std::ceil(raw);
+    const double cap = static_cast<double>(kMaxSamplesPerDim) * static_cast<double>(dims);
+    if (!(k >= 1.0)) return 1;
+    if (k > cap) return static_cast<uint32_t>(cap);
+    return static_cast<uint32_t>(k);
+}
+
+BitSampleFamily build_bit_sample_family(uint64_t dims, uint32_t k, uint64_t tables, uint64_t rng_seed,
+                                        uint64_t prime) {
+    if (dims == 0) throw UsageError("bit sample family: dims must be positive");
+    if (k == 0) throw UsageError("bit sample family: k must be >= 1");
+    if (tables == 0) throw UsageError("bit sample family: need at least one table");
+    if (prime < 3 || prime % 2 == 0) throw UsageError("bit sample family: prime must be odd and > 2");
+    BitSampleFamily f;
+    f.dims = dims;
+    f.k = k;
+    f.tables = tables;
+    f.prime = prime;
+    f.positions.resize(tables * uint64_t(k));
+    f.seeds.resize(tables * uint64_t(k));
+    const Rng rng(rng_seed);
+    Rng pos_rng = rng.stream("positions");
+    Rng seed_rng = rng.stream("seeds");
+    for (uint64_t j = 0; j < f.positions.size(); ++j) { // positions and seeds from their own streams
+        f.positions[j] = static_cast<uint32_t>(pos_rng.below(dims));
+        f.seeds[j] = seed_rng.below(prime);
+    }
+    return f;
+}
+
 } // namespace fclsh_b200

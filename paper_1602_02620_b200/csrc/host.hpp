@@ -84,6 +84,24 @@ Family build_family(uint64_t dims, uint32_t radius, int kind, uint64_t rng_seed,
 Family make_family(uint64_t dims, uint32_t radius, Kind kind, std::vector<uint32_t> mapping,
                    std::vector<uint64_t> seeds, uint64_t prime);
 
+// BitSampleFamily (classic.hpp:15-27): the classic bit-sampling baseline.
+// Table t's key is the sum, mod prime, of the seeds of its k sampled
+// positions (with replacement) that are set in the row.
+struct BitSampleFamily {
+    uint64_t dims = 0;
+    uint32_t k = 0;
+    uint64_t tables = 0;
+    uint64_t prime = kMersenne61;
+    std::vector<uint32_t> positions; // tables * k
+    std::vector<uint64_t> seeds;     // tables * k, each < prime
+};
+constexpr uint32_t kMaxSamplesPerDim = 4; // classic.hpp:30
+// choose_k (classic.cpp:10-23)
+uint32_t choose_k(uint64_t dims, uint32_t radius, uint64_t tables, double delta);
+// build_bit_sample_family (classic.cpp:25-46)
+BitSampleFamily build_bit_sample_family(uint64_t dims, uint32_t k, uint64_t tables, uint64_t rng_seed,
+                                        uint64_t prime);
+
 enum class PlanKind : int32_t { identity = 0, replicate = 1, partition = 2 };
 
 // PreprocessPlan (transform.hpp:26-44)

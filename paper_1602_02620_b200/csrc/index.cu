@@ -2324,11 +2324,17 @@ DeviceIndex::~DeviceIndex() {
 std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_device, uint64_t n, uint64_t dims,
                                          uint32_t radius, const Plan& plan, uint64_t rng_seed,
                                          const IndexBuildOptions& opt) {
-    // index.cpp:51-53, 78-79
+    // index.cpp:51-53, 65-79
     if (n == 0) throw UsageError("index: empty dataset");
     if (dims != plan.dims) throw UsageError("index: dataset width does not match the plan");
     if (radius != plan.radius) throw UsageError("index: radius does not match the plan");
-    if (plan.table_count() > opt.table_budget) throw ResourceError("index: table count exceeds the budget");
+    if (opt.method != kMethodCovering && opt.method != kMethodClassic) throw UsageError("index: unknown method");
+    const bool classic = opt.method == kMethodClassic;
+    if (classic && plan.kind != PlanKind::identity)
+        throw UsageError("index: the classic baseline expects the identity plan");
+    const uint64_t classic_tables = opt.tables_override ? opt.tables_override : (uint64_t(1) << (radius + 1)) - 1;
+    if ((classic ? classic_tables : plan.table_count()) > opt.table_budget)
+        throw ResourceError("index: table count exceeds the budget");
     if (n + opt.id_offset > (uint64_t(1) << 32)) throw UsageError("index: ids must fit 32 bits");
     if (opt.layout < 0 || opt.layout > 2) throw UsageError("index: unknown table layout");
 
@@ -2343,16 +2349,22 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     ix->wide = opt.prime > 0xFFFFFFFFull;
     ix->id_offset = opt.id_offset;
 
-    // families per part from rng.stream("family", p) (index.cpp:83-88)
-    std::vector<Family> fams;
+    ix->method = opt.method;
     Rng rng(rng_seed);
-    for (uint32_t p = 0; p < plan.part_count(); ++p)
-        fams.push_back(build_family(plan.part_dims(p), plan.per_part_radius, -1, rng.stream("family", p).seed(),
-                                    opt.prime, opt.include_zero_column));
+    std::vector<Family> fams;
+    BitSampleFamily bsf;
+    if (classic) { // index.cpp:65-76: k from choose_k unless overridden, family stream ("family", 0)
+        const uint32_t k = opt.k_override ? opt.k_override : choose_k(dims, radius, classic_tables, opt.delta);
+        bsf = build_bit_sample_family(dims, k, classic_tables, rng.stream("family", 0).seed(), opt.prime);
+    } else { // families per part from rng.stream("family", p) (index.cpp:83-88)
+        for (uint32_t p = 0; p < plan.part_count(); ++p)
+            fams.push_back(build_family(plan.part_dims(p), plan.per_part_radius, -1, rng.stream("family", p).seed(),
+                                        opt.prime, opt.include_zero_column));
+    }
 
     FCLSH_CUDA(cudaSetDevice(opt.device));
     FCLSH_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
-    ix->fs = make_device_family_set(plan, std::move(fams), opt.device);
+    ix->fs = classic ? make_device_classic_set(bsf, opt.device) : make_device_family_set(plan, std::move(fams), opt.device);
     ix->tables = ix->fs->total_tables();
 
     const uint32_t kbits = bit_length(opt.prime - 1);

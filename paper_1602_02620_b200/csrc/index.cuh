@@ -15,6 +15,8 @@ namespace fclsh_b200 {
 constexpr int kLayoutAuto = 0;
 constexpr int kLayoutCsr = 1;
 constexpr int kLayoutBuckets = 2;
+constexpr int kMethodCovering = 0;
+constexpr int kMethodClassic = 2; // Method::classic (index.hpp:22)
 
 // Device layout of one shard's index. An entry is
 // u64 (key << 32 | id) when prime < 2^32, else {u64 key, u64 id}.
@@ -44,6 +46,7 @@ struct DeviceIndex {
     uint64_t key_scale = 0;   // floor(2^64 / prime)
     uint64_t id_offset = 0;
     double build_ms = 0;
+    int method = kMethodCovering;
     std::unique_ptr<DeviceFamilySet> fs;
     DevBuf rows, entries, dir;
     // per-table key filter (buckets layout, index.cu): filter_words 32-bit
@@ -121,6 +124,13 @@ struct IndexBuildOptions {
     int directory_bits = 0;
     int layout = kLayoutAuto;
     uint64_t mem_budget = 0; // device bytes this build may take (0: the free memory); picks the layout
+    // Method (index.hpp:22): covering_batch (= covering_reference: identical
+    // buckets) or classic bit sampling with IndexOptions::delta / k_override /
+    // tables_override (index.hpp:29-32; 0 = unset)
+    int method = kMethodCovering;
+    double delta = 0.1;
+    uint32_t k_override = 0;
+    uint64_t tables_override = 0;
 };
 
 // build_index(data, covering_batch, radius, plan, Rng(rng_seed), opt).

@@ -4,8 +4,10 @@ per-query metrics (bench.hpp:17-67, bench.cpp:64-158) and its CSV writer
 
 Methods: "fclsh" and "bclsh" build the covering index on the GPU ("bclsh"
 hashes per mask in the reference; its buckets, and so every counter, are the
-same by construction, index.hpp:17-22), "linear" is the GPU scan. "classic"
-and "mih" are other libraries' baselines, not on this engine's path.
+same by construction, index.hpp:17-22), "classic" builds the bit-sampling
+index on the GPU (identity plan, k from choose_k, the covering plan's table
+count unless overridden, bench.cpp:118-136), "linear" is the GPU scan.
+"mih" (multi-index hashing, mih.cpp) is not on this engine's path.
 
 Counters, true_near, precision and recall equal the reference's exactly
 (same seeds: Rng(seed).stream("run", run).stream("plan" | "index")). Stage
@@ -27,7 +29,10 @@ class ExperimentConfig:  # bench.hpp:17-38
     method: str = "fclsh"
     radius: int = 0
     c: float = 1.0
+    delta: float = 0.1
     plan_override: Optional[F.PlanOverride] = None
+    k_override: Optional[int] = None
+    tables_override: Optional[int] = None
     seed: int = 0
     repeats: int = 5
     fresh_seeds: bool = True
@@ -92,8 +97,8 @@ def run_experiment(data_rows, query_rows, dims: int, truth: GroundTruth, cfg: Ex
     if truth.radius < cfg.radius:
         raise F.DataError(f"experiment: ground truth radius {truth.radius} is below the query radius "
                           f"{cfg.radius}")
-    if cfg.method not in ("fclsh", "bclsh", "linear"):
-        if cfg.method in ("classic", "mih"):
+    if cfg.method not in ("fclsh", "bclsh", "classic", "linear"):
+        if cfg.method == "mih":
             raise F.UsageError(f"experiment: method '{cfg.method}' is not part of the GPU engine")
         raise F.UsageError(f"unknown method '{cfg.method}'")
     true_pairs = _true_ids(truth, nq, cfg.radius)
@@ -115,11 +120,22 @@ def run_experiment(data_rows, query_rows, dims: int, truth: GroundTruth, cfg: Ex
             s1 = s2 = np.zeros(nq)
             s3 = np.zeros(nq)  # the scan's device time is not split per query
         else:
-            plan = F.make_plan(dims, cfg.radius, cfg.c, n, F.rng_stream(run_seed, "plan"), cfg.plan_override,
-                               cfg.table_budget)
+            extra = {}
+            if cfg.method == "classic":  # bench.cpp:121-136
+                plan = F.make_plan(dims, cfg.radius, cfg.c, n, F.rng_stream(run_seed, "plan"),
+                                   F.PlanOverride(F.PlanKind.identity, 1), cfg.table_budget)
+                tables = cfg.tables_override
+                if not tables:  # the covering family's table count under the same plan flags
+                    tables = F.make_plan(dims, cfg.radius, cfg.c, n, F.rng_stream(run_seed, "plan-probe"),
+                                         cfg.plan_override, cfg.table_budget).table_count()
+                extra = {"method": "classic", "delta": cfg.delta, "k_override": cfg.k_override,
+                         "tables_override": tables}
+            else:
+                plan = F.make_plan(dims, cfg.radius, cfg.c, n, F.rng_stream(run_seed, "plan"), cfg.plan_override,
+                                   cfg.table_budget)
             ix = F.build_index(data, cfg.radius, plan, F.rng_stream(run_seed, "index"), prime=cfg.prime,
                                include_zero_column=cfg.include_zero_column, table_budget=cfg.table_budget,
-                               device=device, dims=dims)
+                               device=device, dims=dims, **extra)
             ix.stage_timing(True)
             res = ix.query_r_nn(queries, cfg.radius)
             fq, fid = res.query, res.id

@@ -239,6 +239,54 @@ def hash_batch_device(family: CoveringFamily, rows, keys, *, layout: int = 0, ke
                                     C.c_void_p(keys.data_ptr()), kb, stride, layout, dev or 0, _stream_ptr(stream)))
 
 
+# ----------------------------------------------------------- classic family
+
+@dataclass
+class BitSampleFamily:  # classic.hpp:15-27
+    dims: int
+    k: int
+    tables: int
+    prime: int
+    positions: np.ndarray  # uint32 [tables * k]
+    seeds: np.ndarray      # uint64 [tables * k]
+
+    def table_count(self) -> int:
+        return self.tables
+
+
+def choose_k(dims: int, radius: int, tables: int, delta: float) -> int:
+    """choose_k (classic.cpp:10-23)."""
+    out = C.c_uint32(0)
+    _check(N.lib().fclsh_choose_k(dims, radius, tables, float(delta), C.byref(out)))
+    return int(out.value)
+
+
+def build_bit_sample_family(dims: int, k: int, tables: int, rng_seed: int, prime: int = M61) -> BitSampleFamily:
+    """build_bit_sample_family (classic.cpp:25-46)."""
+    pos = np.zeros(max(1, tables * k), np.uint32)
+    seeds = np.zeros(max(1, tables * k), np.uint64)
+    _check(N.lib().fclsh_bitsample_family_build(dims, k, tables, rng_seed, prime, _ptr(pos, N.u32p),
+                                                _ptr(seeds, N.u64p)))
+    return BitSampleFamily(dims, k, tables, prime, pos[:tables * k], seeds[:tables * k])
+
+
+def hash_tables(family: BitSampleFamily, rows, device: int = 0) -> np.ndarray:
+    """hash_tables_into (classic.cpp:48-63) for every row, on the device -> uint64 [n, tables]."""
+    r = _u64(rows)
+    if r.ndim == 1:
+        r = r.reshape(1, -1)
+    n = r.shape[0]
+    if n and r.shape[1] != words_for(family.dims):
+        raise UsageError("hash: vector width does not match the family")
+    out = np.zeros((n, family.tables), np.uint64)
+    pos = np.ascontiguousarray(family.positions, np.uint32)
+    sd = np.ascontiguousarray(family.seeds, np.uint64)
+    _check(N.lib().fclsh_hash_tables_batch(family.dims, family.k, family.tables, _ptr(pos, N.u32p),
+                                           _ptr(sd, N.u64p), family.prime, _ptr(r, N.u64p), n, _ptr(out, N.u64p),
+                                           device))
+    return out
+
+
 class PreprocessPlan:
     """PreprocessPlan (transform.hpp:26-44)."""
 
@@ -385,6 +433,16 @@ class IndexSet:
         self.build_ms = float(info.build_ms)
         self.layout = {1: "csr", 2: "buckets"}.get(int(info.layout), "?")
         self.buckets_per_table = int(info.buckets_per_table)
+        self.method = {0: "covering", 2: "classic"}.get(int(info.method), "?")
+        self.classic_k = int(info.classic_k)
+
+    def bit_sample_family(self) -> BitSampleFamily:
+        """A classic index's family (positions / seeds [tables * k])."""
+        k, T = self.classic_k, self._tables
+        pos = np.zeros(max(1, T * k), np.uint32)
+        seeds = np.zeros(max(1, T * k), np.uint64)
+        _check(N.lib().fclsh_index_bitsample_family(self._h, _ptr(pos, N.u32p), _ptr(seeds, N.u64p)))
+        return BitSampleFamily(self.dims, k, T, self._prime, pos[:T * k], seeds[:T * k])
 
     def __del__(self, _free=_release):  # bound at definition: module globals may be gone at exit
         _free(self, "fclsh_index_destroy")
@@ -467,15 +525,28 @@ class IndexSet:
                                   out.d_candidates or 0, out.d_found or 0, out)
 
 
+METHODS = {"covering": 0, "covering_batch": 0, "covering_reference": 0, "classic": 2}
+
+
 def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, prime: int = M61,
                 include_zero_column: bool = False, table_budget: int = DEFAULT_TABLE_BUDGET, device: int = 0,
                 id_offset: int = 0, directory_bits: int = 0, dims: int | None = None,
-                layout: str = "auto") -> IndexSet:
-    """build_index(data, Method::covering_batch, radius, plan, Rng(rng_seed), IndexOptions{...})
+                layout: str = "auto", method: str = "covering", delta: float = 0.1,
+                k_override: int | None = None, tables_override: int | None = None) -> IndexSet:
+    """build_index(data, method, radius, plan, Rng(rng_seed), IndexOptions{...})
     (index.cpp:49-119). data_rows: numpy uint64 [n, W] or a CUDA tensor.
-    layout: "auto" | "csr" | "buckets" (device table layout; same results)."""
+    layout: "auto" | "csr" | "buckets" (device table layout; same results).
+    method: "covering" (covering_batch; covering_reference builds the same
+    buckets) or "classic" (bit sampling, identity plan; delta / k_override /
+    tables_override as IndexOptions, index.hpp:29-32)."""
+    if method not in METHODS:
+        raise UsageError(f"unknown method '{method}'")
     opt = N.IndexOptions()
     N.lib().fclsh_index_options_default(C.byref(opt))
+    opt.method = METHODS[method]
+    opt.delta = float(delta)
+    opt.k_override = k_override or 0
+    opt.tables_override = tables_override or 0
     opt.prime = prime
     opt.include_zero_column = int(include_zero_column)
     opt.table_budget = table_budget
@@ -499,7 +570,9 @@ def build_index(data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, 
             raise UsageError("index: dataset width does not match the plan")
         _check(N.lib().fclsh_index_build(r.ctypes.data_as(C.c_void_p), 0, n, d, radius, plan._h, rng_seed,
                                          C.byref(opt), C.byref(h)))
-    return IndexSet(h, plan)
+    ix = IndexSet(h, plan)
+    ix._prime = prime
+    return ix
 
 
 def launch_count() -> int:
@@ -558,7 +631,8 @@ class Cluster:
     def build(self, data_rows, radius: int, plan: PreprocessPlan, rng_seed: int, *, n: int | None = None,
               local_rows: bool = False, prime: int = M61, include_zero_column: bool = False,
               table_budget: int = DEFAULT_TABLE_BUDGET, id_offset: int = 0, directory_bits: int = 0,
-              layout: str = "auto") -> "Cluster":
+              layout: str = "auto", method: str = "covering", delta: float = 0.1, k_override: int | None = None,
+              tables_override: int | None = None) -> "Cluster":
         """build_index over the sharded points. data_rows: all n points (numpy
         or a CUDA tensor), or with local_rows=True only this process's range
         (n = the global count)."""
@@ -570,6 +644,12 @@ class Cluster:
         opt.id_offset = id_offset
         opt.directory_bits = directory_bits
         opt.layout = {"auto": 0, "csr": 1, "buckets": 2}[layout]
+        if method not in METHODS:
+            raise UsageError(f"unknown method '{method}'")
+        opt.method = METHODS[method]
+        opt.delta = float(delta)
+        opt.k_override = k_override or 0
+        opt.tables_override = tables_override or 0
         if hasattr(data_rows, "data_ptr"):
             ptr, on_dev, rows_n = C.c_void_p(data_rows.data_ptr()), int(data_rows.is_cuda), data_rows.shape[0]
         else:

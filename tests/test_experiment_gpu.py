@@ -24,6 +24,8 @@ CASES = [
     ("bclsh", 96, 4, (0, 1), F.M31, 1, True),
     ("fclsh", 100, 5, None, F.M61, 3, True),
     ("linear", 128, 5, None, F.M31, 1, True),
+    ("classic", 64, 3, (0, 1), F.M31, 2, True),
+    ("classic", 128, 6, (2, 2), F.M61, 1, False),
 ]
 
 
