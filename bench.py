@@ -21,7 +21,7 @@ index build times.
 
 Scaling: cfg1-3 and cfg5 are weak (every GPU holds the config's n points of
 one global dataset of N x n points; queries broadcast), cfg4 is strong (the
-10M points in 8 shards over N GPUs, 8 / N per GPU).
+10M points in one shard per GPU: at N = 8 the BASELINE's 8-way sharding).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
@@ -632,7 +632,7 @@ def main():
     torch.cuda.set_stream(stream)
     flush = Flush(ctx.devices)
     clocks = ClockSampler(ctx.devices[0])
-    spr4 = max(1, CONFIGS[4].shards // ctx.G)
+    spr4 = 1  # cfg4: one shard per GPU (at 8 GPUs exactly the BASELINE's 8-way sharding)
     # a small build + batch first, so the kernels' lazy module loading is not timed
     warm = CONFIGS[2].scaled(20000, queries=100)
     run_config(ctx, warm, "weak", 1, argparse.Namespace(**{**vars(args), "steps": 1, "no_cpu": True}), flush, stream,

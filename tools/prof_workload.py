@@ -15,8 +15,8 @@ from paper_1602_02620_b200 import fclsh as F  # noqa: E402
 from paper_1602_02620_b200.configs import CONFIGS, make_data, make_queries  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "all"
-if what in ("all", "query"):
-    cfg = CONFIGS[2]
+if what in ("all", "query", "cfg2", "cfg3", "cfg1"):
+    cfg = CONFIGS[{"cfg3": 3, "cfg1": 1}.get(what, 2)]
     data = make_data(cfg)
     q = make_queries(cfg, data)
     plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg.plan_seed(), cfg.override())
