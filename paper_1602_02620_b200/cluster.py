@@ -75,17 +75,25 @@ def exchange(triples: torch.Tensor, total: int, offsets: torch.Tensor, counters:
     return Exchanged(totals, all_off, all_trip, summed)
 
 
+def exchange_cluster_id(group=None) -> bytes:
+    """Rank 0's NCCL unique id (ncclGetUniqueId, fclsh_cluster_unique_id) on
+    every rank, carried by torch.distributed (any backend; gloo is enough).
+    A world of one needs no id (the library skips NCCL there)."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world == 1:
+        return bytes(F.CLUSTER_ID_BYTES)
+    box = [F.cluster_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return box[0]
+
+
 def rank_cluster(shards_per_rank: int = 1, device: int | None = None, group=None) -> F.Cluster:
     """One rank of a multi-process fclsh_cluster (one process per GPU, e.g.
-    under torchrun): rank 0 draws the NCCL id and torch.distributed (any
-    backend; gloo is enough) carries it to the other ranks, then every rank
-    joins with ncclCommInitRank inside the library."""
+    under torchrun): rank 0 draws the NCCL id, torch.distributed carries it to
+    the other ranks, then every rank joins with ncclCommInitRank inside the
+    library."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     if device is None:
         device = torch.cuda.current_device()
-    uid = bytes(F.CLUSTER_ID_BYTES)
-    if world > 1:
-        box = [F.cluster_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(box, src=0, group=group)
-        uid = box[0]
+    uid = exchange_cluster_id(group)
     return F.Cluster(rank=rank, world=world, device=device, uid=uid, shards_per_rank=shards_per_rank)

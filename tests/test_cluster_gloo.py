@@ -1,8 +1,14 @@
-"""Multi-process (world_size 2, gloo on CPU) test of the sharded query path's
-host logic: shard ranges, id offsets, the torch.distributed exchange
-(cluster.exchange), counter additivity and the rank-ordered merge -- with
-each rank's shard answered by the CPU oracle (no GPU here). The device merge
-kernel is covered by tests/test_cluster_gpu.py."""
+"""Multi-process (world_size 2, gloo on CPU) tests of the sharded query
+path's host logic (no GPU here):
+
+* the NCCL id exchange of a one-process-per-GPU fclsh_cluster
+  (cluster.exchange_cluster_id: rank 0's ncclGetUniqueId reaches every rank);
+* the invariants the library's merge (k_merge_sources) relies on -- shard
+  ranges, id offsets, shard-additive counters, rank order = id order --
+  checked by answering each rank's shard with the CPU oracle and exchanging
+  through torch.distributed (cluster.exchange).
+The device path itself (fclsh_cluster, 1-8 shards, NCCL forced on at one
+rank) is tests/test_cluster_gpu.py."""
 import os
 import socket
 
@@ -58,6 +64,26 @@ def _worker(rank, world, port, outdir):
                  triples=ex.triples.numpy(), counters=ex.counters.numpy())
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _id_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    from paper_1602_02620_b200 import cluster
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    uid = cluster.exchange_cluster_id()
+    with open(os.path.join(outdir, f"id{rank}.bin"), "wb") as f:
+        f.write(uid)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_cluster_id_exchange(tmp_path):
+    world = 2
+    mp.start_processes(_id_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    ids = [open(os.path.join(tmp_path, f"id{r}.bin"), "rb").read() for r in range(world)]
+    assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])
 
 
 def test_shard_range_partitions():
