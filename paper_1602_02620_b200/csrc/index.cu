@@ -104,7 +104,11 @@ constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 constexpr int kDenseU = FCLSH_DENSE_U;     // home buckets per thread in flight in the CTA kernel
 constexpr int kDenseRun = FCLSH_DENSE_RUN; // buckets read at a time along a spilled run (CTA kernel)
 constexpr int kFusedU = FCLSH_FUSED_U; // tables per lane in flight in the warp kernel
-constexpr int kFusedCap = FCLSH_FUSED_CAP; // warp-kernel id-set slots (3/4 of it: distinct ids; more: the CTA kernel)
+constexpr int kFusedCap = FCLSH_FUSED_CAP;
+#ifndef FCLSH_WARP_U_DEFAULT
+#define FCLSH_WARP_U_DEFAULT 2
+#endif
+constexpr int kWarpU = FCLSH_WARP_U_DEFAULT; // probes per lane in flight in k_query_warp_pf // warp-kernel id-set slots (3/4 of it: distinct ids; more: the CTA kernel)
 
 // One bucket (4 slots) with 256-bit loads: a random probe is one L1 request
 // for the narrow layout (two for wide) instead of four 64-bit ones; the
@@ -889,11 +893,8 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
 // words (keys loaded a round earlier) and round c+2's keys, so a round waits
 // on its bucket reads only (reference loop replaced: index.cpp:169-177).
 // Dedup, counters, verify and outputs are k_query_warp's.
-#ifndef FCLSH_WARP_PF_MINB
-#define FCLSH_WARP_PF_MINB 5
-#endif
-template <typename T, int U>
-__global__ void __launch_bounds__(256, FCLSH_WARP_PF_MINB) k_query_warp_pf(
+template <typename T, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
@@ -1873,7 +1874,14 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                        tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec);
             FCLSH_LAUNCHED();
         };
-        go(k_query_warp_pf<T, kFusedU>);
+        // probes per lane in flight per round (A/B: FCLSH_WARP_U = 2 | 4)
+        static const int wu = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : kWarpU;
+        if (wu == 4)
+            go(k_query_warp_pf<T, 4, 3>);
+        else if (wu == 3)
+            go(k_query_warp_pf<T, 3, 4>);
+        else
+            go(k_query_warp_pf<T, 2, 5>);
         return;
     }
     if (!shared_set) {
