@@ -924,15 +924,18 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         uint32_t nd = 0;        // distinct ids so far (warp-uniform)
         bool over = false;      // more than 32 distinct ids (warp-uniform)
         uint32_t coll = 0;      // this lane's postings
-        auto offer = [&](bool has, uint32_t id) {
-            coll += has;
-            if (!__any_sync(kAll, has) || over) return;
+        // one warp-uniform step: each lane offers at most one colliding id
+        // (counted by the caller); ids already listed -- the usual case, the
+        // query's near point seen again in table after table -- cost one
+        // vote, only new ones the match-any dedup and the append
+        auto offer_id = [&](bool has, uint32_t id) {
+            if (over) return;
             bool seen = false;
             for (uint32_t k = 0; k < nd; ++k) seen |= __shfl_sync(kAll, list, k) == id;
             const bool fresh = has && !seen;
+            if (!__any_sync(kAll, fresh)) return;
             const uint32_t grp = __match_any_sync(kAll, fresh ? id : kEmpty);
             const uint32_t lead = __ballot_sync(kAll, fresh && __ffs(grp) - 1 == lane);
-            if (!lead) return;
             if (nd + __popc(lead) > 32) {
                 over = true;
                 return;
@@ -941,6 +944,20 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                 const uint32_t v = __shfl_sync(kAll, id, __ffs(b) - 1);
                 if (uint32_t(lane) == nd) list = v;
                 ++nd;
+            }
+        };
+        // the postings of one bucket with this lane's key: a vote when no lane
+        // has one (most probes), else one offer step per posting
+        auto offer_bucket = [&](const E (&bk)[kSlots], bool live, uint64_t kk) {
+            uint32_t mm = 0;
+#pragma unroll
+            for (int i = 0; i < kSlots; ++i) mm |= uint32_t(live && !T::empty(bk[i]) && T::key(bk[i]) == kk) << i;
+            coll += __popc(mm);
+            while (__any_sync(kAll, mm != 0)) {
+                const int i = __ffs(mm) - 1;
+                const uint32_t id = i <= 0 ? T::id(bk[0]) : i == 1 ? T::id(bk[1]) : i == 2 ? T::id(bk[2]) : T::id(bk[3]);
+                offer_id(mm != 0, id);
+                mm &= mm - 1;
             }
         };
         // the pipeline: keys of rounds c, c+1, c+2 and the filter result of c+1
@@ -981,9 +998,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             for (int u = 0; u < U; ++u) {
                 const uint64_t kk = uint64_t(k0[u]);
                 const bool live = p0[u];
-#pragma unroll
-                for (int j = 0; j < kSlots; ++j)
-                    offer(live && !T::empty(sl[u][j]) && T::key(sl[u][j]) == kk, T::id(sl[u][j]));
+                offer_bucket(sl[u], live, kk);
                 // the run continues into the next bucket (~3 %)
                 bool cont = live && !T::empty(sl[u][kSlots - 1]);
                 uint64_t b = home_of(kk, tb) + 1;
@@ -994,8 +1009,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                     for (int j = 0; j < kSlots; ++j) x[j] = T::make(~0ull, ~0u);
                     b &= tb.nbuckets - 1;
                     if (cont) load_bucket(base + b * kSlots, x);
-#pragma unroll
-                    for (int j = 0; j < kSlots; ++j) offer(cont && !T::empty(x[j]) && T::key(x[j]) == kk, T::id(x[j]));
+                    offer_bucket(x, cont, kk);
                     cont = cont && !T::empty(x[kSlots - 1]);
                     ++b;
                 }
@@ -1023,168 +1037,6 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             continue;
         }
         // ascending ids: bitonic sort across the warp (non-passes = +inf)
-        unsigned long long mine = pass ? (static_cast<unsigned long long>(list) << 32) | dist : ~0ull;
-#pragma unroll
-        for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(kAll, mine, j);
-                const bool up = (lane & k) == 0;
-                const bool lower = (lane & j) == 0;
-                const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
-                mine = (lower == up) ? lo : hi;
-            }
-        }
-        if (uint32_t(lane) < nfound) {
-            tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
-            tmp_dist[q * slot_cap + lane] = uint32_t(mine);
-        }
-        if (lane == 0) {
-            coll_q[q] = m;
-            cand_q[q] = nd;
-            found_q[q] = nfound;
-            if (hc) {
-                hc[(nq + 1) + q] = m;
-                hc[2 * (nq + 1) + q] = nd;
-                hc[3 * (nq + 1) + q] = nfound;
-            }
-            src_pos[q] = q * slot_cap;
-            if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
-        }
-    }
-}
-
-// Warp per query, every home bucket of the query in flight at once (buckets
-// layout, narrow entries): a lane loads its KPL = ceil(T/32) keys, their
-// filter words, then issues one asynchronous 32-byte copy per passing probe
-// (cp.async.cg: L2 -> shared memory, no registers held while in flight), so
-// a query costs three memory round trips (keys, filter words, buckets) instead
-// of KPL/U bucket rounds, and the registers no longer cap the reads in flight.
-// Each lane reads back only its own slots. Dedup, counters, verify and
-// outputs are k_query_warp's. Shared memory: 32 x KPL x 32 B per warp.
-__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-template <typename T, int KPL, int WPB>
-__global__ void __launch_bounds__(32 * WPB) k_query_warp_ga(
-    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
-    const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
-    uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
-    unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
-    uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
-    unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum,
-    const unsigned long long* __restrict__ desc, int vec_rows) {
-    using E = typename T::E;
-    using K = typename T::K;
-    static_assert(sizeof(E) == 8, "narrow entries: a bucket is 32 bytes");
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr unsigned kAll = 0xffffffffu;
-    constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
-    const int lane = threadIdx.x & 31;
-    // this warp's landing slots: [KPL][32 lanes][4 entries]
-    E* const land = reinterpret_cast<E*>(smem) + size_t(threadIdx.x >> 5) * KPL * 32 * kSlots;
-    const uint64_t fpol = l2_evict_last_policy();
-    pdl_trigger();
-    pdl_wait(); // the batch's keys (hash kernel) are complete from here on
-    auto fetch = [&]() -> uint64_t {
-        unsigned int v = 0;
-        if (lane == 0) v = atomicAdd(qnext, 1u);
-        return __shfl_sync(kAll, v, 0);
-    };
-    for (uint64_t q = fetch(); q < nq; q = fetch()) {
-        const K* qk = qkeys + q * tables;
-        K key[KPL];
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const uint32_t t = uint32_t(j) * 32 + lane;
-            key[j] = t < tables ? qk[t] : K(0);
-        }
-        uint32_t pmask = 0;
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const uint32_t t = uint32_t(j) * 32 + lane;
-            const bool p = t < tables && (!tb.filter || filter_pass(tb, t, uint64_t(key[j]), fpol));
-            pmask |= uint32_t(p) << j;
-        }
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            if (pmask >> j & 1) {
-                const uint32_t t = uint32_t(j) * 32 + lane;
-                const E* src = tb.data + (uint64_t(t) * tb.nbuckets + home_of(uint64_t(key[j]), tb)) * kSlots;
-                E* dst = land + (size_t(j) * 32 + lane) * kSlots;
-                cp_async16_cg(dst, src);
-                cp_async16_cg(dst + 2, src + 2);
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        uint32_t list = kEmpty; // this lane's distinct id (lane < nd)
-        uint32_t nd = 0;        // distinct ids so far (warp-uniform)
-        bool over = false;      // more than 32 distinct ids (warp-uniform)
-        uint32_t coll = 0;      // this lane's postings
-        auto offer = [&](bool has, uint32_t id) {
-            coll += has;
-            if (!__any_sync(kAll, has) || over) return;
-            bool seen = false;
-            for (uint32_t k = 0; k < nd; ++k) seen |= __shfl_sync(kAll, list, k) == id;
-            const bool fresh = has && !seen;
-            const uint32_t grp = __match_any_sync(kAll, fresh ? id : kEmpty);
-            const uint32_t lead = __ballot_sync(kAll, fresh && __ffs(grp) - 1 == lane);
-            if (!lead) return;
-            if (nd + __popc(lead) > 32) {
-                over = true;
-                return;
-            }
-            for (uint32_t b = lead; b; b &= b - 1) {
-                const uint32_t v = __shfl_sync(kAll, id, __ffs(b) - 1);
-                if (uint32_t(lane) == nd) list = v;
-                ++nd;
-            }
-        };
-        asm volatile("cp.async.wait_group 0;" ::: "memory"); // this lane's copies have landed
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            if (uint32_t(j) * 32 >= tables || over) break;
-            const bool live = pmask >> j & 1;
-            const uint64_t kk = uint64_t(key[j]);
-            E sl[kSlots];
-            const E* mine = land + (size_t(j) * 32 + lane) * kSlots;
-#pragma unroll
-            for (int i = 0; i < kSlots; ++i) sl[i] = live ? mine[i] : T::make(~0ull, ~0u);
-#pragma unroll
-            for (int i = 0; i < kSlots; ++i) offer(live && !T::empty(sl[i]) && T::key(sl[i]) == kk, T::id(sl[i]));
-            // the run continues into the next bucket (~3 %)
-            bool cont = live && !T::empty(sl[kSlots - 1]);
-            uint64_t b = home_of(kk, tb) + 1;
-            const E* base = tb.data + uint64_t(uint32_t(j) * 32 + lane) * tb.nbuckets * kSlots;
-            while (__any_sync(kAll, cont)) {
-                E x[kSlots];
-#pragma unroll
-                for (int i = 0; i < kSlots; ++i) x[i] = T::make(~0ull, ~0u);
-                b &= tb.nbuckets - 1;
-                if (cont) load_bucket(base + b * kSlots, x);
-#pragma unroll
-                for (int i = 0; i < kSlots; ++i) offer(cont && !T::empty(x[i]) && T::key(x[i]) == kk, T::id(x[i]));
-                cont = cont && !T::empty(x[kSlots - 1]);
-                ++b;
-            }
-        }
-        __syncwarp(); // every lane is done with its slots before the next query's copies
-        const uint64_t m = __reduce_add_sync(kAll, coll);
-        uint32_t dist = 0;
-        if (!over && uint32_t(lane) < nd)
-            dist = row_distance(rows + uint64_t(list) * words, qrows + q * words, words, vec_rows);
-        const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
-        const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
-        if (over || nfound > slot_cap) {
-            if (lane == 0) {
-                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
-                found_q[q] = 0; // written by the CTA kernel later
-                src_pos[q] = 0;
-            }
-            continue;
-        }
         unsigned long long mine = pass ? (static_cast<unsigned long long>(list) << 32) | dist : ~0ull;
 #pragma unroll
         for (int k = 2; k <= 32; k <<= 1) {
@@ -2036,35 +1888,6 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                        tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec);
             FCLSH_LAUNCHED();
         };
-        // every home bucket of a query in flight at once (cp.async into shared
-        // memory): FCLSH_WARP_GA=1 (A/B), narrow entries
-        static const bool ga = getenv("FCLSH_WARP_GA") && getenv("FCLSH_WARP_GA")[0] == '1';
-        if constexpr (sizeof(typename T::E) == 8) {
-        if (ga && ix.tables <= 16 * 32) {
-            const uint32_t kpl = uint32_t((ix.tables + 31) / 32);
-            auto go_ga = [&](auto kern, int kplc, int wpb) {
-                const size_t smem = size_t(wpb) * kplc * 32 * kSlots * sizeof(typename T::E);
-                const int per_sm = resident_ctas(kern, 32 * wpb, smem, ix.device);
-                const uint64_t grid = std::max<uint64_t>(
-                    1, std::min<uint64_t>((nq + wpb - 1) / wpb, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
-                launch_pdl(kern, unsigned(grid), 32 * wpb, smem, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
-                           ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q,
-                           src_pos, tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec);
-                FCLSH_LAUNCHED();
-            };
-            if (kpl <= 1)
-                go_ga(k_query_warp_ga<T, 1, 4>, 1, 4);
-            else if (kpl <= 2)
-                go_ga(k_query_warp_ga<T, 2, 4>, 2, 4);
-            else if (kpl <= 4)
-                go_ga(k_query_warp_ga<T, 4, 4>, 4, 4);
-            else if (kpl <= 8)
-                go_ga(k_query_warp_ga<T, 8, 4>, 8, 4);
-            else
-                go_ga(k_query_warp_ga<T, 16, 2>, 16, 2);
-            return;
-        }
-        }
         // probes per lane in flight per round (A/B: FCLSH_WARP_U = 2 | 4)
         static const int wu = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : kWarpU;
         if (wu == 4)
