@@ -893,15 +893,113 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
 // words (keys loaded a round earlier) and round c+2's keys, so a round waits
 // on its bucket reads only (reference loop replaced: index.cpp:169-177).
 // Dedup, counters, verify and outputs are k_query_warp's.
-template <typename T, int U, int MINB>
+// The covering hash of one query row inside the query kernel (fused: no
+// separate hash launch, no grid-wide wait for the batch's keys). Narrow keys
+// (prime < 2^32), parts of N = 32 x FE columns. Per part: the sketch
+// t[c] = sum of the seeds of the set positions mapped to column c (the
+// family's column lists, positions already in source-row bits), an exact
+// int64 Walsh-Hadamard transform F over the warp (index bits 5.. in
+// registers, bits 0..4 across lanes), and key[v] = (F[0] - F[v]) / 2 mod P
+// = sum of the seeds at set positions i with popcount(v & m(i)) odd: the
+// reference's h[v] (covering.cpp:150-182, hadamard.cpp:51-72). Keys go to
+// the batch's key array (read back by this warp and, for handed-over
+// queries, by the other query kernels); the row stays in registers, and
+// rows read from mapped host memory are also copied to the device rows.
+struct FusedHash {
+    uint32_t parts = 0, N = 0, L = 0;
+    uint64_t max_dims = 0;
+    const uint32_t* col_ptr = nullptr; // [parts][N+1]
+    const uint32_t* ent_pos = nullptr; // [parts][max_dims] source-row bit
+    const uint64_t* ent_seed = nullptr;
+    uint64_t prime = 0;
+    const uint64_t* hash_src = nullptr; // mapped pinned host rows (null: the device rows)
+};
+
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_cg(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+template <int FE, typename K>
+__device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint32_t words, const uint64_t* qrows,
+                                           K* keys, int lane, uint64_t& rw) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const uint64_t* src = (fh.hash_src ? fh.hash_src : qrows) + q * words;
+    if (uint32_t(lane) < words) {
+        rw = src[lane];
+        if (fh.hash_src) const_cast<uint64_t*>(qrows)[q * words + lane] = rw;
+    }
+    const uint64_t P = fh.prime;
+    for (uint32_t p = 0; p < fh.parts; ++p) {
+        const uint32_t* cp = fh.col_ptr + uint64_t(p) * (fh.N + 1);
+        const uint32_t* ep = fh.ent_pos + uint64_t(p) * fh.max_dims;
+        const uint64_t* es = fh.ent_seed + uint64_t(p) * fh.max_dims;
+        long long t[FE];
+#pragma unroll
+        for (int i = 0; i < FE; ++i) {
+            const uint32_t c = uint32_t(lane) + 32u * i;
+            const uint32_t b0 = __ldg(cp + c), cnt = __ldg(cp + c + 1) - b0;
+            const uint32_t m = __reduce_max_sync(kAll, cnt); // warp-uniform trip count (the shuffle needs every lane)
+            long long acc = 0;
+            for (uint32_t k = 0; k < m; ++k) {
+                const bool has = k < cnt;
+                const uint32_t pos = has ? __ldg(ep + b0 + k) : 0u;
+                const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
+                if (has && ((w >> (pos & 63)) & 1)) acc += (long long)__ldg(es + b0 + k);
+            }
+            t[i] = acc;
+        }
+#pragma unroll
+        for (int h = 1; h < FE; h <<= 1) { // index bits 5.. : within the lane
+#pragma unroll
+            for (int i = 0; i < FE; ++i)
+                if (!(i & h)) {
+                    const long long x = t[i], y = t[i | h];
+                    t[i] = x + y;
+                    t[i | h] = x - y;
+                }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { // index bits 0..4: across lanes
+#pragma unroll
+            for (int i = 0; i < FE; ++i) {
+                const long long other = __shfl_xor_sync(kAll, t[i], o);
+                t[i] = (lane & o) ? other - t[i] : t[i] + other;
+            }
+        }
+        const long long l1 = __shfl_sync(kAll, t[0], 0); // F[0] = sum of the sketch
+        K* kp = keys + uint64_t(p) * fh.L;
+#pragma unroll
+        for (int i = 0; i < FE; ++i) {
+            const uint32_t v = uint32_t(lane) + 32u * i;
+            uint64_t x = uint64_t(l1 - t[i]) >> 1;
+            if (P == 0x7FFFFFFFull) {
+                x = (x & P) + (x >> 31);
+                x = (x & P) + (x >> 31);
+                x = x >= P ? x - P : x;
+            } else {
+                x %= P;
+            }
+            if (v) kp[v - 1] = K(x);
+        }
+    }
+}
+
+template <typename T, int U, int MINB, int FE>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
-    const typename T::K* __restrict__ qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
+    typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
     uint32_t slot_cap, unsigned long long* __restrict__ coll_q, unsigned long long* __restrict__ cand_q,
     unsigned long long* __restrict__ found_q, unsigned long long* __restrict__ src_pos, uint32_t* __restrict__ tmp_id,
     uint32_t* __restrict__ tmp_dist, uint32_t* __restrict__ overflow, unsigned int* __restrict__ overflow_count,
     unsigned int* __restrict__ qnext, unsigned long long* __restrict__ tile_sum,
-    const unsigned long long* __restrict__ desc, int vec_rows) {
+    const unsigned long long* __restrict__ desc, int vec_rows, const FusedHash fh) {
     using E = typename T::E;
     using K = typename T::K;
     constexpr unsigned kAll = 0xffffffffu;
@@ -912,7 +1010,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
-    pdl_wait(); // the batch's keys (hash kernel) are complete from here on
+    pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
     auto fetch = [&]() -> uint64_t {
         unsigned int v = 0;
         if (lane == 0) v = atomicAdd(qnext, 1u);
@@ -920,6 +1018,17 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     };
     for (uint64_t q = fetch(); q < nq; q = fetch()) {
         const K* qk = qkeys + q * tables;
+        uint64_t rw = 0; // FE > 0: word `lane` of the query row
+        if constexpr (FE > 0) {
+            fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw);
+            __syncwarp(); // the keys (written across lanes) are visible to the loads below
+        }
+        // FE > 0: the keys were written by this warp a moment ago: coherent
+        // L2 loads, not the read-only path
+        auto ldk = [&](uint32_t t) -> K {
+            if constexpr (FE > 0) return ld_cg(qk + t);
+            else return __ldg(qk + t);
+        };
         uint32_t list = kEmpty; // this lane's distinct id (lane < nd)
         uint32_t nd = 0;        // distinct ids so far (warp-uniform)
         bool over = false;      // more than 32 distinct ids (warp-uniform)
@@ -966,8 +1075,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t t0 = u * 32 + lane, t1 = kStep + t0;
-            k0[u] = t0 < tables ? qk[t0] : K(0);
-            k1[u] = t1 < tables ? qk[t1] : K(0);
+            k0[u] = t0 < tables ? ldk(t0) : K(0);
+            k1[u] = t1 < tables ? ldk(t1) : K(0);
         }
         bool p0[U];
 #pragma unroll
@@ -992,7 +1101,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             for (int u = 0; u < U; ++u) { // round c+1: filter words; round c+2: keys
                 const uint32_t t1 = base_t + kStep + u * 32 + lane, t2 = t1 + kStep;
                 p1[u] = t1 < tables && (!tb.filter || filter_pass(tb, t1, uint64_t(k1[u]), fpol));
-                k2[u] = t2 < tables ? qk[t2] : K(0);
+                k2[u] = t2 < tables ? ldk(t2) : K(0);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1024,8 +1133,13 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         const uint64_t m = __reduce_add_sync(kAll, coll);
         // verify the listed ids, one per lane
         uint32_t dist = 0;
-        if (!over && uint32_t(lane) < nd)
+        if constexpr (FE > 0) { // the query row is in registers (word w on lane w)
+            const uint64_t* r = rows + uint64_t(over || uint32_t(lane) >= nd ? 0 : list) * words;
+            for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __shfl_sync(kAll, rw, w));
+            if (over || uint32_t(lane) >= nd) dist = 0;
+        } else if (!over && uint32_t(lane) < nd) {
             dist = row_distance(rows + uint64_t(list) * words, qrows + q * words, words, vec_rows);
+        }
         const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
         const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
         if (over || nfound > slot_cap) {
@@ -1861,12 +1975,42 @@ void build_all(DeviceIndex& ix) {
     FCLSH_CUDA(cudaStreamSynchronize(s));
 }
 
+// The query kernel hashes its own queries (k_query_warp_pf<.., FE>) when the
+// keys are narrow (prime < 2^32), the family is a covering family with
+// N = 32 x FE columns per part, FE in {1, 2, 4, 8, 16} (per-part radius 4..8),
+// and rows fit a warp (d <= 2048): returns FE, else 0 (the separate hash
+// kernel runs first). FCLSH_NO_FUSED_HASH=1: never (A/B).
+int fused_fe(const DeviceIndex& ix) {
+    static const bool off = getenv("FCLSH_NO_FUSED_HASH") != nullptr || getenv("FCLSH_WARP_V1") != nullptr ||
+                            getenv("FCLSH_FUSED_SHARED") != nullptr;
+    const DeviceFamilySet& fs = *ix.fs;
+    if (off || ix.layout != kLayoutBuckets || ix.wide || fs.classic || ix.prime > 0xFFFFFFFFull) return 0;
+    if (ix.tables > 600 || ix.row_words > 32 || fs.order < 32 || fs.order > 512) return 0;
+    return int(fs.order / 32);
+}
+
+FusedHash fused_params(const DeviceIndex& ix, const uint64_t* hash_src) {
+    FusedHash f;
+    const DeviceFamilySet& fs = *ix.fs;
+    if (!fused_fe(ix)) return f;
+    f.parts = fs.parts;
+    f.N = uint32_t(fs.order);
+    f.L = uint32_t(fs.tables);
+    f.max_dims = fs.max_part_dims;
+    f.col_ptr = fs.col_ptr.as<uint32_t>();
+    f.ent_pos = fs.ent_pos.as<uint32_t>();
+    f.ent_seed = fs.ent_seed.as<uint64_t>();
+    f.prime = fs.prime;
+    f.hash_src = hash_src;
+    return f;
+}
+
 template <typename T, int LAYOUT, int CAP>
-void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
+void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, unsigned long long* tile_sum,
-                  const unsigned long long* desc, cudaStream_t s) {
+                  const unsigned long long* desc, cudaStream_t s, const uint64_t* hash_src) {
     // default: the id list in registers (no shared memory, all of L1 for the
     // probes in flight); FCLSH_FUSED_SHARED=1 selects the shared-set kernel
     static const bool shared_set = getenv("FCLSH_FUSED_SHARED") != nullptr;
@@ -1885,17 +2029,30 @@ void launch_fused(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
             launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
                        ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec);
+                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec, fused_params(ix, hash_src));
             FCLSH_LAUNCHED();
         };
-        // probes per lane in flight per round (A/B: FCLSH_WARP_U = 2 | 4)
-        static const int wu = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : kWarpU;
-        if (wu == 4)
-            go(k_query_warp_pf<T, 4, 3>);
+        // probes per lane in flight per round: 3 for indexes of <= 400
+        // tables, else 2 (measured; A/B: FCLSH_WARP_U = 2 | 3 | 4)
+        static const int wu_env = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : 0;
+        const int wu = wu_env ? wu_env : (ix.tables <= 400 ? 3 : 2);
+        const int fe = fused_fe(ix);
+        if (fe == 1)
+            go(k_query_warp_pf<T, 3, 4, 1>);
+        else if (fe == 2)
+            go(k_query_warp_pf<T, 3, 4, 2>);
+        else if (fe == 4)
+            go(k_query_warp_pf<T, 3, 4, 4>);
+        else if (fe == 8)
+            go(k_query_warp_pf<T, 2, 4, 8>);
+        else if (fe == 16)
+            go(k_query_warp_pf<T, 2, 4, 16>);
+        else if (wu == 4)
+            go(k_query_warp_pf<T, 4, 3, 0>);
         else if (wu == 3)
-            go(k_query_warp_pf<T, 3, 4>);
+            go(k_query_warp_pf<T, 3, 4, 0>);
         else
-            go(k_query_warp_pf<T, 2, 5>);
+            go(k_query_warp_pf<T, 2, 5, 0>);
         return;
     }
     if (!shared_set) {
@@ -2085,15 +2242,18 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
                                    ix.side));
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
-        // hash_src (mapped pinned host rows): hashed from there, copied to d_q on the way
-        hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
-                  hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
+        // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
+        // the way; with the hash fused into the query kernel it does both
+        const bool fused_hash = !dense_all && fused_fe(ix) > 0;
+        if (!fused_hash)
+            hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
+                      hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
         rec(1);
         FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
                                                b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
-                                               b.tile_sum, d_desc, s);
+                                               b.tile_sum, d_desc, s, fused_hash ? hash_src : nullptr);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : b.ovf, b.ovf_cnt, nq, b.coll_q,
                                 b.cand_q, b.found_q, b.src_pos, nq * slot_cap, b.cta_id, b.cta_dist, b.cta_cap,
