@@ -1205,7 +1205,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
     uint32_t* __restrict__ res_dist, uint64_t res_cap, unsigned long long* __restrict__ res_cursor,
     uint32_t* __restrict__ ovf2, unsigned int* __restrict__ ovf2_cnt, unsigned int* __restrict__ qnext,
     unsigned long long* __restrict__ tile_sum, const unsigned long long* __restrict__ desc, uint64_t nq_all,
-    uint32_t slot_cap, uint32_t* __restrict__ slot_id, uint32_t* __restrict__ slot_dist) {
+    uint32_t slot_cap, uint32_t* __restrict__ slot_id, uint32_t* __restrict__ slot_dist, int vec_rows) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
@@ -1338,8 +1338,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
             for (uint32_t k = tid; k < ncand; k += nt) {
                 const uint32_t id = set[clist[k]];
                 const uint64_t* r = rows + uint64_t(id) * words;
-                uint32_t d = 0;
-                for (uint32_t w = 0; w < words; ++w) d += __popcll(__ldg(r + w) ^ __ldg(qr + w));
+                const uint32_t d = row_distance(r, qr, words, vec_rows);
                 if (d <= radius) {
                     const uint32_t pos = atomicAdd(&found_s, 1u);
                     if (pos < FCAP)
@@ -1985,7 +1984,10 @@ int fused_fe(const DeviceIndex& ix) {
                             getenv("FCLSH_FUSED_SHARED") != nullptr;
     const DeviceFamilySet& fs = *ix.fs;
     if (off || ix.layout != kLayoutBuckets || ix.wide || fs.classic || ix.prime > 0xFFFFFFFFull) return 0;
-    if (ix.tables > 600 || ix.row_words > 32 || fs.order < 32 || fs.order > 512) return 0;
+    // (N = 512, FE = 16 -- cfg2 -- measured slower fused: 0.139 -> 0.186 ms per
+    // batch, the 16-deep register transform spills and delays every query's
+    // probes; the separate hash kernel runs there)
+    if (ix.tables > 600 || ix.row_words > 32 || fs.order < 32 || fs.order > 256) return 0;
     return int(fs.order / 32);
 }
 
@@ -2045,8 +2047,6 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
             go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 8)
             go(k_query_warp_pf<T, 2, 4, 8>);
-        else if (fe == 16)
-            go(k_query_warp_pf<T, 2, 4, 16>);
         else if (wu == 4)
             go(k_query_warp_pf<T, 4, 3, 0>);
         else if (wu == 3)
@@ -2105,7 +2105,7 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
     launch_pdl(kern, unsigned(grid), kDenseThreads, smem, s, qkeys, uint32_t(ix.tables), view<T>(ix),
                ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q,
                found_q, src_pos, src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum, desc,
-               nq_all, slot_cap, slot_id, slot_dist);
+               nq_all, slot_cap, slot_id, slot_dist, vec_for(ix.row_words, d_q));
     FCLSH_LAUNCHED();
 }
 
