@@ -1976,7 +1976,7 @@ void build_all(DeviceIndex& ix) {
 
 // The query kernel hashes its own queries (k_query_warp_pf<.., FE>) when the
 // keys are narrow (prime < 2^32), the family is a covering family with
-// N = 32 x FE columns per part, FE in {1, 2, 4, 8, 16} (per-part radius 4..8),
+// N = 32 x FE columns per part, FE in {1, 2, 4, 8} (per-part radius 4..7),
 // and rows fit a warp (d <= 2048): returns FE, else 0 (the separate hash
 // kernel runs first). FCLSH_NO_FUSED_HASH=1: never (A/B).
 int fused_fe(const DeviceIndex& ix) {
