@@ -437,12 +437,17 @@ def run_config(ctx, cfg, scaling, spr, args, flush, stream, clocks, hbm, peak_sr
     kern_stage = "dense" if T_ > 600 else "fused"
     kern_name = "k_query_dense" if kern_stage == "dense" else "k_query_warp"
     algo = (nq * T_ * (4 + probe) + cand.sum() * R + found.sum() * 8) / S + nq * cfg.dims / 8
+    # the query kernel hashes its own queries (index.cu fused_fe: narrow keys,
+    # per-part radius 4..7, <= 600 tables): the hash pass's bytes are its too
+    fused_hash = 4 <= cfg.per_part_radius <= 7 and T_ <= 600 and kern_stage == "fused"
+    if fused_hash:
+        algo += nq * T_ * 4
     dur = stage_avg[kern_stage]
     ach = algo / (dur / 1e3) / 1e9
     traffic, tsrc = measured_traffic(kern_name, cfg.name)
     out["roofline"] = {"bound": "hbm", "kernel": kern_name, "achieved": ach, "peak": hbm, "unit": "GB/s",
                        "frac": ach / hbm, "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
-                       "algorithmic_bytes_per_launch": algo, "duration_ms": dur,
+                       "algorithmic_bytes_per_launch": algo, "duration_ms": dur, "hash_fused": fused_hash,
                        "bytes_note": "per (query, table) the key + one random 32-B bucket sector (also for the "
                                      "probes the L2 key filter skips), per distinct candidate max(32, d/8) B, per "
                                      "result 8 B, query rows once; traffic = measured DRAM bytes per launch (ncu)"}
@@ -502,6 +507,8 @@ def replay_batch(ctx, cl, q, q_dev, cfg, args, flush, stream, clocks):
         kern = "fused" if T_ <= 600 else "dense"
         dur = st[kern] + (st["hash"] if st.get("hash", 0) > 0 and kern == "fused" else 0)
         algo = nq * T_ * (4 + 32) + cand * R_ + found * 8 + nq * cfg.dims / 8
+        if 4 <= cfg.per_part_radius <= 7 and T_ <= 600:  # hash fused into the kernel: its key writes too
+            algo += nq * T_ * 4
         verify = cand * (4 + R_) + found * 12 + nq * cfg.dims / 8
         out.update({"kernel_ms": dur, "kernel_us_per_query": 1e3 * dur / nq,
                     "roofline_frac": algo / (dur / 1e3) / 1e9 / hbm_peak()[0], "algorithmic_bytes": algo,
