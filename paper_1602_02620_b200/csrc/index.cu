@@ -2026,7 +2026,9 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
                 FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
                 carved.fetch_or(bit, std::memory_order_acq_rel);
             }
-            const int per_sm = resident_ctas(kern, 256, 0, ix.device);
+            int per_sm = resident_ctas(kern, 256, 0, ix.device);
+            static const int cap = getenv("FCLSH_WARP_CTAS") ? atoi(getenv("FCLSH_WARP_CTAS")) : 0; // A/B
+            if (cap > 0) per_sm = std::min(per_sm, cap);
             const uint64_t grid = std::max<uint64_t>(
                 1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
             launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
@@ -2043,6 +2045,8 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
             go(k_query_warp_pf<T, 3, 4, 1>);
         else if (fe == 2)
             go(k_query_warp_pf<T, 3, 4, 2>);
+        else if (fe == 4 && wu == 2)
+            go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 4)
             go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 8)
