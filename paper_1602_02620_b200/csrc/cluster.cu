@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256) k_merge_sources(const MergeSrcs srcs, uin
                 const unsigned long long st = __shfl_sync(kAll, start, k);
                 const unsigned long long b = __shfl_sync(kAll, beg[h], k);
                 const MergeSrc& m = srcs.s[s];
+                FCLSH_DCHECK(s < S);
                 for (unsigned long long j = lane; j < c; j += 32) {
                     dst.q[st + j] = uint32_t(q);
                     dst.id[st + j] = m.id[b + j];

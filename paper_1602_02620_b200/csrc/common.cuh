@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <utility>
@@ -18,6 +19,25 @@ namespace fclsh_b200 {
         if (_e != cudaSuccess)                                                               \
             throw ::fclsh_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e)); \
     } while (0)
+
+// Device-side bounds checks (a build with -DFCLSH_DEBUG_BOUNDS: make
+// EXTRA=-DFCLSH_DEBUG_BOUNDS BUILD=build_dbg OUT=lib/libfclsh_b200_dbg.so; the
+// test suite runs against it with FCLSH_LIB, tools/bounds_check.sh). A failed
+// check prints the site and traps, which fails the batch with a CUDA error.
+#ifdef FCLSH_DEBUG_BOUNDS
+#define FCLSH_DCHECK(cond)                                                                        \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("FCLSH_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   int(blockIdx.x), int(threadIdx.x));                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define FCLSH_DCHECK(cond) \
+    do {                   \
+    } while (0)
+#endif
 
 // Per-thread count of kernels launched by this library (bench accounting).
 uint64_t& launch_counter();

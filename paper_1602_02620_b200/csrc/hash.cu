@@ -1219,6 +1219,7 @@ __global__ void __launch_bounds__(256) k_hash_classic(const uint64_t* __restrict
         uint64_t acc = 0;
         for (uint32_t j = 0; j < k; ++j) {
             const uint32_t b = __ldg(p + j);
+            FCLSH_DCHECK((b >> 6) < words);
             const uint64_t bit = (__ldg(r + (b >> 6)) >> (b & 63)) & 1;
             acc += __ldg(sd + j) & (0ull - bit);
             acc = acc >= prime ? acc - prime : acc;

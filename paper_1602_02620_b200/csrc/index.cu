@@ -326,6 +326,7 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
             atomicOr(filter + uint64_t(t) * filter_words + (r >> 5), 1u << (r & 31));
         }
         uint64_t b = home_of(key, kscale, shift);
+        FCLSH_DCHECK(b < nbuckets && t < t0 + tg);
         for (;;) {
             typename T::E* bp = bt + b * kSlots;
             bool done = false;
@@ -654,7 +655,9 @@ __global__ void __launch_bounds__(256) k_query_fused(
         }
         if (nd >= kMaxD || nfound > slot_cap || nfound > 32) {
             if (lane == 0) {
-                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                const unsigned int at = atomicAdd(overflow_count, 1u);
+                FCLSH_DCHECK(at < nq);
+                overflow[at] = uint32_t(q);
                 found_q[q] = 0; // written by the CTA kernel later
                 src_pos[q] = 0;
             }
@@ -673,6 +676,7 @@ __global__ void __launch_bounds__(256) k_query_fused(
             }
         }
         if (uint32_t(lane) < nfound) {
+            FCLSH_DCHECK(q < nq && uint32_t(lane) < slot_cap);
             tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
             tmp_dist[q * slot_cap + lane] = uint32_t(mine);
         }
@@ -846,7 +850,9 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
         const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
         if (over || nfound > slot_cap) {
             if (lane == 0) {
-                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                const unsigned int at = atomicAdd(overflow_count, 1u);
+                FCLSH_DCHECK(at < nq);
+                overflow[at] = uint32_t(q);
                 found_q[q] = 0; // written by the CTA kernel later
                 src_pos[q] = 0;
             }
@@ -866,6 +872,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
             }
         }
         if (uint32_t(lane) < nfound) {
+            FCLSH_DCHECK(q < nq && uint32_t(lane) < slot_cap);
             tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
             tmp_dist[q * slot_cap + lane] = uint32_t(mine);
         }
@@ -950,6 +957,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
             for (uint32_t k = 0; k < m; ++k) {
                 const bool has = k < cnt;
                 const uint32_t pos = has ? __ldg(ep + b0 + k) : 0u;
+                FCLSH_DCHECK((pos >> 6) < words && b0 + cnt <= fh.max_dims);
                 const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
                 if (has && ((w >> (pos & 63)) & 1)) acc += (long long)__ldg(es + b0 + k);
             }
@@ -1090,6 +1098,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             for (int u = 0; u < U; ++u) { // round c: U home buckets in flight
                 const uint32_t t = base_t + u * 32 + lane;
                 if (p0[u]) {
+                    FCLSH_DCHECK(t < tables && home_of(uint64_t(k0[u]), tb) < tb.nbuckets);
                     load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + home_of(uint64_t(k0[u]), tb)) * kSlots,
                                       sl[u], bpol);
                 } else {
@@ -1144,7 +1153,9 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
         if (over || nfound > slot_cap) {
             if (lane == 0) {
-                overflow[atomicAdd(overflow_count, 1u)] = uint32_t(q);
+                const unsigned int at = atomicAdd(overflow_count, 1u);
+                FCLSH_DCHECK(at < nq);
+                overflow[at] = uint32_t(q);
                 found_q[q] = 0; // written by the CTA kernel later
                 src_pos[q] = 0;
             }
@@ -1164,6 +1175,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             }
         }
         if (uint32_t(lane) < nfound) {
+            FCLSH_DCHECK(q < nq && uint32_t(lane) < slot_cap);
             tmp_id[q * slot_cap + lane] = uint32_t(mine >> 32);
             tmp_dist[q * slot_cap + lane] = uint32_t(mine);
         }
@@ -1391,6 +1403,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
             __syncthreads();
             bitonic_sort<NarrowEntry>(fl, P, P);
             const bool slots = nf <= slot_cap;
+            FCLSH_DCHECK(slots ? q < nq_all : base_s + nf <= res_cap);
             uint32_t* const oid = slots ? slot_id + q * slot_cap : res_id + base_s;
             uint32_t* const odist = slots ? slot_dist + q * slot_cap : res_dist + base_s;
             for (uint32_t k = tid; k < nf; k += nt) {
@@ -1507,6 +1520,7 @@ __global__ void __launch_bounds__(512) k_query_c(const typename T::K* __restrict
                 h = (h + 1) & (HS - 1);
             }
             const uint32_t k = atomicAdd(&cand_s, 1u);
+            FCLSH_DCHECK(!slots || k < HS / 2);
             if (slots) slots[k] = h;
         };
         for (uint32_t t = tid; t < tables; t += nt) {
