@@ -44,6 +44,10 @@ int main(int argc, char** argv) {
         }
         auto ix = G::build_index(rows.data(), n, d, r, plan, index_seed, G::kMersenne31);
         auto res = ix.query_r_nn(q.data(), nq, r);
+        auto cix = G::build_classic_index(rows.data(), n, d, r, plan, index_seed, G::kMersenne31);
+        auto clres = cix.query_r_nn(q.data(), nq, r);
+        std::printf("classic tables=%llu found0=%llu\n", (unsigned long long)cix.table_count(),
+                    (unsigned long long)clres.found[0]);
         G::Cluster cl({0}, 4);
         cl.build(rows.data(), n, d, r, plan, index_seed, G::kMersenne31);
         auto cres = cl.query_r_nn(q.data(), nq, r);

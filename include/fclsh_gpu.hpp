@@ -153,15 +153,36 @@ private:
     fclsh_index_info info_{};
 };
 
+// build_index(data, Method, radius, plan, rng, IndexOptions) with every option
+// (fclsh_index_options_default, then set prime / method / delta / ...)
+inline Index build_index(const uint64_t* rows, uint64_t n, uint64_t dims, uint32_t radius, const PreprocessPlan& plan,
+                         uint64_t rng_seed, const fclsh_index_options& o) {
+    fclsh_index* h = nullptr;
+    check(fclsh_index_build(rows, 0, n, dims, radius, plan.handle(), rng_seed, &o, &h));
+    return Index(h);
+}
+
 inline Index build_index(const uint64_t* rows, uint64_t n, uint64_t dims, uint32_t radius, const PreprocessPlan& plan,
                          uint64_t rng_seed, uint64_t prime = kMersenne61, int device = 0) {
     fclsh_index_options o;
     fclsh_index_options_default(&o);
     o.prime = prime;
     o.device = device;
-    fclsh_index* h = nullptr;
-    check(fclsh_index_build(rows, 0, n, dims, radius, plan.handle(), rng_seed, &o, &h));
-    return Index(h);
+    return build_index(rows, n, dims, radius, plan, rng_seed, o);
+}
+
+// Method::classic (index.cpp:65-76): bit sampling over the identity plan
+inline Index build_classic_index(const uint64_t* rows, uint64_t n, uint64_t dims, uint32_t radius,
+                                 const PreprocessPlan& plan, uint64_t rng_seed, uint64_t prime = kMersenne61,
+                                 double delta = 0.1, uint32_t k_override = 0, uint64_t tables_override = 0) {
+    fclsh_index_options o;
+    fclsh_index_options_default(&o);
+    o.prime = prime;
+    o.method = FCLSH_METHOD_CLASSIC;
+    o.delta = delta;
+    o.k_override = k_override;
+    o.tables_override = tables_override;
+    return build_index(rows, n, dims, radius, plan, rng_seed, o);
 }
 
 // A point-sharded index over several GPUs (or several shards on one GPU):
