@@ -151,6 +151,8 @@ class Ctx:
             dist.init_process_group("gloo")
             self.dist = dist
         self.devices = [self.local] if self.torchrun else list(range(self.G))
+        if self.G > 1:  # NCCL's own log names every rank it connects (the library's communicator)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
         self.root = self.rank == 0
 
     def check_gpus(self, args):
