@@ -920,11 +920,6 @@ struct FusedHash {
     const uint64_t* ent_seed = nullptr;
     uint64_t prime = 0;
     const uint64_t* hash_src = nullptr; // mapped pinned host rows (null: the device rows)
-    // SPLIT = 2 (k_query_warp_pf): the two halves of a query meet here
-    unsigned int* half_flag = nullptr;  // [nq], zeroed per batch
-    uint32_t* half_list = nullptr;      // [nq][2][32] distinct ids of each half
-    uint32_t* half_info = nullptr;      // [nq][2][4] {nd, collisions, over, -}
-    uint32_t split_at = 0;              // first table of the second half
 };
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
@@ -940,7 +935,7 @@ __device__ __forceinline__ uint64_t ld_cg(const uint64_t* p) {
 
 template <int FE, typename K>
 __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint32_t words, const uint64_t* qrows,
-                                           K* keys, int lane, uint64_t& rw, uint32_t part_begin, uint32_t part_end) {
+                                           K* keys, int lane, uint64_t& rw) {
     constexpr unsigned kAll = 0xffffffffu;
     const uint64_t* src = (fh.hash_src ? fh.hash_src : qrows) + q * words;
     if (uint32_t(lane) < words) {
@@ -948,7 +943,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
         if (fh.hash_src) const_cast<uint64_t*>(qrows)[q * words + lane] = rw;
     }
     const uint64_t P = fh.prime;
-    for (uint32_t p = part_begin; p < part_end; ++p) {
+    for (uint32_t p = 0; p < fh.parts; ++p) {
         const uint32_t* cp = fh.col_ptr + uint64_t(p) * (fh.N + 1);
         const uint32_t* ep = fh.ent_pos + uint64_t(p) * fh.max_dims;
         const uint64_t* es = fh.ent_seed + uint64_t(p) * fh.max_dims;
@@ -1004,7 +999,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
     }
 }
 
-template <typename T, int U, int MINB, int FE, int SPLIT>
+template <typename T, int U, int MINB, int FE>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -1029,23 +1024,11 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         if (lane == 0) v = atomicAdd(qnext, 1u);
         return __shfl_sync(kAll, v, 0);
     };
-    // SPLIT = 2: a unit of work is half a query (its tables [0, split_at) or
-    // [split_at, T); with the hash fused, one part each): more, shorter units
-    // shorten the batch's tail; the half that finishes second merges the
-    // other's distinct ids and counters (published in fh.half_*) and writes
-    // the query's outputs
-    for (uint64_t u = fetch(); u < nq * SPLIT; u = fetch()) {
-        const uint64_t q = u / SPLIT;
-        const uint32_t h = uint32_t(u % SPLIT);
-        const uint32_t t_lo = SPLIT == 2 && h ? fh.split_at : 0u;
-        const uint32_t t_hi = SPLIT == 2 && !h ? fh.split_at : tables;
+    for (uint64_t q = fetch(); q < nq; q = fetch()) {
         const K* qk = qkeys + q * tables;
         uint64_t rw = 0; // FE > 0: word `lane` of the query row
         if constexpr (FE > 0) {
-            if constexpr (SPLIT == 2)
-                fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw, h, h + 1);
-            else
-                fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw, 0, fh.parts);
+            fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
         // FE > 0: the keys were written by this warp a moment ago: coherent
@@ -1099,23 +1082,23 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         bool p1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t t0 = t_lo + u * 32 + lane, t1 = kStep + t0;
-            k0[u] = t0 < t_hi ? ldk(t0) : K(0);
-            k1[u] = t1 < t_hi ? ldk(t1) : K(0);
+            const uint32_t t0 = u * 32 + lane, t1 = kStep + t0;
+            k0[u] = t0 < tables ? ldk(t0) : K(0);
+            k1[u] = t1 < tables ? ldk(t1) : K(0);
         }
         bool p0[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t t = t_lo + u * 32 + lane;
-            p0[u] = t < t_hi && (!tb.filter || filter_pass(tb, t, uint64_t(k0[u]), fpol));
+            const uint32_t t = u * 32 + lane;
+            p0[u] = t < tables && (!tb.filter || filter_pass(tb, t, uint64_t(k0[u]), fpol));
         }
-        for (uint32_t base_t = t_lo; base_t < t_hi && !over; base_t += kStep) {
+        for (uint32_t base_t = 0; base_t < tables && !over; base_t += kStep) {
             E sl[U][kSlots];
 #pragma unroll
             for (int u = 0; u < U; ++u) { // round c: U home buckets in flight
                 const uint32_t t = base_t + u * 32 + lane;
                 if (p0[u]) {
-                    FCLSH_DCHECK(t < t_hi && home_of(uint64_t(k0[u]), tb) < tb.nbuckets);
+                    FCLSH_DCHECK(t < tables && home_of(uint64_t(k0[u]), tb) < tb.nbuckets);
                     load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + home_of(uint64_t(k0[u]), tb)) * kSlots,
                                       sl[u], bpol);
                 } else {
@@ -1126,8 +1109,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
 #pragma unroll
             for (int u = 0; u < U; ++u) { // round c+1: filter words; round c+2: keys
                 const uint32_t t1 = base_t + kStep + u * 32 + lane, t2 = t1 + kStep;
-                p1[u] = t1 < t_hi && (!tb.filter || filter_pass(tb, t1, uint64_t(k1[u]), fpol));
-                k2[u] = t2 < t_hi ? ldk(t2) : K(0);
+                p1[u] = t1 < tables && (!tb.filter || filter_pass(tb, t1, uint64_t(k1[u]), fpol));
+                k2[u] = t2 < tables ? ldk(t2) : K(0);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1156,32 +1139,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                 k1[u] = k2[u];
             }
         }
-        uint64_t m = __reduce_add_sync(kAll, coll);
-        if constexpr (SPLIT == 2) {
-            // publish this half; the second to arrive merges and finishes the query
-            uint32_t* my_list = fh.half_list + (q * 2 + h) * 32;
-            uint32_t* my_info = fh.half_info + (q * 2 + h) * 4;
-            my_list[lane] = list;
-            if (lane == 0) {
-                my_info[0] = nd;
-                my_info[1] = uint32_t(m);
-                my_info[2] = over;
-            }
-            __threadfence();
-            __syncwarp();
-            unsigned int prev = 0;
-            if (lane == 0) prev = atomicAdd(fh.half_flag + q, 1u);
-            prev = __shfl_sync(kAll, prev, 0);
-            if (prev == 0) continue; // the other half finishes this query
-            __threadfence();
-            const uint32_t* o_list = fh.half_list + (q * 2 + (h ^ 1)) * 32;
-            const uint32_t* o_info = fh.half_info + (q * 2 + (h ^ 1)) * 4;
-            const uint32_t o_nd = ld_cg(o_info), o_coll = ld_cg(o_info + 1), o_over = ld_cg(o_info + 2);
-            const uint32_t o_id = ld_cg(o_list + lane);
-            over = over || o_over;
-            m += o_coll;
-            offer_id(uint32_t(lane) < o_nd, o_id); // the other half's ids, deduplicated into this list
-        }
+        const uint64_t m = __reduce_add_sync(kAll, coll);
         // verify the listed ids, one per lane
         uint32_t dist = 0;
         if constexpr (FE > 0) { // the query row is in registers (word w on lane w)
@@ -2063,26 +2021,12 @@ FusedHash fused_params(const DeviceIndex& ix, const uint64_t* hash_src) {
     return f;
 }
 
-// Two warps per query (k_query_warp_pf<.., SPLIT = 2>): the first table of
-// the second half, or 0 for one warp per query. Halves are the plan's two
-// parts when the hash is fused (each warp hashes its part), else two ranges
-// of whole 32-table columns; indexes of < 128 tables are not split.
-// FCLSH_SPLIT=0 / 1: never / always when possible (A/B).
-uint32_t split_point(const DeviceIndex& ix) {
-    static const int env = getenv("FCLSH_SPLIT") ? atoi(getenv("FCLSH_SPLIT")) : -1;
-    if (env == 0 || ix.layout != kLayoutBuckets || ix.tables > 600) return 0;
-    if (getenv("FCLSH_WARP_V1") || getenv("FCLSH_FUSED_SHARED")) return 0;
-    if (fused_fe(ix) > 0) return ix.fs->parts == 2 ? uint32_t(ix.fs->tables) : 0u;
-    if (ix.tables < 128) return 0;
-    return uint32_t(((ix.tables / 2) + 31) / 32 * 32);
-}
-
 template <typename T, int LAYOUT, int CAP>
 void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, uint64_t nq, uint32_t radius,
                   uint32_t slot_cap, unsigned long long* coll_q, unsigned long long* cand_q,
                   unsigned long long* found_q, unsigned long long* src_pos, uint32_t* tmp_id, uint32_t* tmp_dist,
                   uint32_t* ovf, unsigned int* ovf_cnt, unsigned int* qnext, unsigned long long* tile_sum,
-                  const unsigned long long* desc, cudaStream_t s, const FusedHash& fh) {
+                  const unsigned long long* desc, cudaStream_t s, const uint64_t* hash_src) {
     // default: the id list in registers (no shared memory, all of L1 for the
     // probes in flight); FCLSH_FUSED_SHARED=1 selects the shared-set kernel
     static const bool shared_set = getenv("FCLSH_FUSED_SHARED") != nullptr;
@@ -2103,7 +2047,7 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
                 1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
             launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
                        ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec, fh);
+                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec, fused_params(ix, hash_src));
             FCLSH_LAUNCHED();
         };
         // probes per lane in flight per round: 3 for indexes of <= 400
@@ -2111,21 +2055,22 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
         static const int wu_env = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : 0;
         const int wu = wu_env ? wu_env : (ix.tables <= 400 ? 3 : 2);
         const int fe = fused_fe(ix);
-        const bool split = fh.split_at > 0;
         if (fe == 1)
-            go(k_query_warp_pf<T, 3, 4, 1, 1>);
+            go(k_query_warp_pf<T, 3, 4, 1>);
         else if (fe == 2)
-            go(k_query_warp_pf<T, 3, 4, 2, 1>);
-        else if (fe == 4)
-            split ? go(k_query_warp_pf<T, 2, 5, 4, 2>) : go(k_query_warp_pf<T, 2, 5, 4, 1>);
+            go(k_query_warp_pf<T, 3, 4, 2>);
+        else if (fe == 4 && wu_env == 3)
+            go(k_query_warp_pf<T, 3, 4, 4>);
+        else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
+            go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 8)
-            split ? go(k_query_warp_pf<T, 2, 4, 8, 2>) : go(k_query_warp_pf<T, 2, 4, 8, 1>);
+            go(k_query_warp_pf<T, 2, 4, 8>);
         else if (wu == 4)
-            go(k_query_warp_pf<T, 4, 3, 0, 1>);
+            go(k_query_warp_pf<T, 4, 3, 0>);
         else if (wu == 3)
-            split ? go(k_query_warp_pf<T, 3, 4, 0, 2>) : go(k_query_warp_pf<T, 3, 4, 0, 1>);
+            go(k_query_warp_pf<T, 3, 4, 0>);
         else
-            split ? go(k_query_warp_pf<T, 2, 5, 0, 2>) : go(k_query_warp_pf<T, 2, 5, 0, 1>);
+            go(k_query_warp_pf<T, 2, 5, 0>);
         return;
     }
     if (!shared_set) {
@@ -2207,8 +2152,6 @@ struct QueryBufs {
     unsigned long long *counters, *res_off, *coll_q, *cand_q, *found_q, *src_pos, *res_cursor, *tile_sum;
     uint32_t *tmp_id, *tmp_dist, *ovf, *ovf2, *cta_id, *cta_dist, *oq, *oi, *od;
     unsigned int* ovf_cnt;
-    unsigned int* half_flag; // split warp kernel: [nq] meeting counters, zeroed per batch
-    uint32_t *half_list, *half_info;
     uint64_t ntiles, cta_cap, out_cap;
     size_t scan_bytes;
     void* scan_tmp;
@@ -2233,13 +2176,6 @@ QueryBufs<T> query_bufs(DeviceIndex& ix, uint64_t nq, cudaStream_t s) {
     b.tmp_dist = static_cast<uint32_t*>(ix.res_tmp_dist.ensure(std::max<uint64_t>(1, nq * kSlotCap) * 4));
     b.ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
     b.ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
-    {
-        const uint64_t per = 4 + 2 * 32 + 2 * 4; // flag (padded), two id lists, two info records
-        auto* hb = static_cast<uint32_t*>(ix.half.ensure(std::max<uint64_t>(1, nq) * per * 4));
-        b.half_flag = reinterpret_cast<unsigned int*>(hb);
-        b.half_list = hb + std::max<uint64_t>(1, nq) * 4;
-        b.half_info = b.half_list + std::max<uint64_t>(1, nq) * 64;
-    }
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
     // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
     // query to hand out in the warp / CTA kernel, [8]: k_scan_compact CTAs
@@ -2314,16 +2250,6 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         }
     };
     const unsigned long long* d_desc = d_seq + 1;
-    // the warp kernel's extra inputs: the fused hash's tables and the split
-    // queries' meeting records
-    const bool fused_hash = !dense_all && fused_fe(ix) > 0;
-    FusedHash fh = fused_params(ix, fused_hash ? hash_src : nullptr);
-    const uint32_t split_at = split_point(ix);
-    const bool split = !dense_all && split_at > 0;
-    fh.half_flag = b.half_flag;
-    fh.half_list = b.half_list;
-    fh.half_info = b.half_info;
-    fh.split_at = split_at;
     auto enqueue_common = [&] {
         rec(0);
         // on a side branch beside the hash: clear the batch counters and copy
@@ -2331,12 +2257,12 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
         FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
         FCLSH_CUDA(cudaMemsetAsync(b.ovf_cnt, 0, 64 + b.ntiles * 8, ix.side));
-        if (split) FCLSH_CUDA(cudaMemsetAsync(b.half_flag, 0, nq * 4, ix.side));
         FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
                                    ix.side));
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
         // the way; with the hash fused into the query kernel it does both
+        const bool fused_hash = !dense_all && fused_fe(ix) > 0;
         if (!fused_hash)
             hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
                       hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
@@ -2345,7 +2271,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
                                                b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
-                                               b.tile_sum, d_desc, s, fh);
+                                               b.tile_sum, d_desc, s, fused_hash ? hash_src : nullptr);
         rec(2);
         launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : b.ovf, b.ovf_cnt, nq, b.coll_q,
                                 b.cand_q, b.found_q, b.src_pos, nq * slot_cap, b.cta_id, b.cta_dist, b.cta_cap,

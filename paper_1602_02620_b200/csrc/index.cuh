@@ -59,7 +59,7 @@ struct DeviceIndex {
     // query workspace (grow-only)
     DevBuf q_rows, q_keys, r_start, r_count, counters, coll_off, coll_sel, fill, cand, cand_sorted, src_pos,
         res_tmp_id, res_tmp_dist, res2_id, res2_dist, res_cta_id, res_cta_dist, overflow, overflow2, overflow_cnt,
-        out_q, out_id, out_dist, cub_tmp, half;
+        out_q, out_id, out_dist, cub_tmp;
     // mapped pinned words k_compact publishes {total, hand-over counts, seq} to;
     // the batch sequence number is counted on the device (pub_seq_dev)
     unsigned long long* h_pub = nullptr;
