@@ -84,6 +84,7 @@ struct WideEntry { // 8-byte keys: {key, id}
 };
 
 constexpr int kSlots = 4; // per bucket
+constexpr uint32_t kBuildSlab = 64; // tables per table-major slab of the bucket build
 constexpr int kScanTileLog = 10; // queries per tile of the found scan (k_scan_compact): 1024
 constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 #ifndef FCLSH_FUSED_CAP
@@ -279,36 +280,41 @@ __device__ __forceinline__ uint32_t probe_one(const Tables<T>& tb, uint32_t t, u
 
 // ----------------------------------------------------------------- build
 
-// point-major keys [n][L] -> table-major [L][n] through 32 x 32 shared tiles
-// (both sides 128-byte coalesced), so the inserts of a few tables read their
-// keys contiguously instead of a 4-byte word out of every row's sector
+// point-major keys [n][L] -> table-major [c][n] for the slab of tables
+// [tb, tb + c), through 32 x 32 shared tiles (both sides 128-byte coalesced),
+// so the inserts of a few tables read their keys contiguously instead of a
+// 4-byte word out of every row's sector; slabs keep the table-major copy
+// small (one slab, not all L tables: cfg4 on one GPU fits the 60 %-load
+// bucket tables beside it)
 template <typename K>
 __global__ void __launch_bounds__(256) k_keys_table_major(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
-                                                          uint32_t L) {
+                                                          uint32_t L, uint32_t tb, uint32_t c) {
     __shared__ K tile[32][33];
     const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const uint64_t tiles_t = (L + 31) / 32, tiles = tiles_t * ((n + 31) / 32);
+    const uint64_t tiles_t = (c + 31) / 32, tiles = tiles_t * ((n + 31) / 32);
     for (uint64_t tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
         const uint32_t t0 = uint32_t(tl % tiles_t) * 32;
         const uint64_t i0 = (tl / tiles_t) * 32;
         for (uint32_t r = ty; r < 32; r += 8) {
             const uint64_t i = i0 + r;
             const uint32_t t = t0 + tx;
-            if (i < n && t < L) tile[r][tx] = in[i * L + t];
+            if (i < n && t < c) tile[r][tx] = in[i * L + tb + t];
         }
         __syncthreads();
         for (uint32_t r = ty; r < 32; r += 8) {
             const uint32_t t = t0 + r;
             const uint64_t i = i0 + tx;
-            if (i < n && t < L) out[uint64_t(t) * n + i] = tile[tx][r];
+            if (i < n && t < c) out[uint64_t(t) * n + i] = tile[tx][r];
         }
         __syncthreads();
     }
 }
 
-// keys are table-major for one part: key of (row i, table t) at keys[t*n + i]
+// keys are table-major for a slab of one part's tables starting at table
+// key_t0: key of (row i, table t) at keys[(t - key_t0)*n + i]
 template <typename T>
-__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t n, uint32_t t0, uint32_t tg,
+__global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint32_t key_t0, uint64_t n, uint32_t t0,
+                                uint32_t tg,
                                 uint32_t shift, uint64_t nbuckets, typename T::E* __restrict__ buckets,
                                 uint32_t* __restrict__ filter, uint32_t filter_words, uint64_t kscale) {
     // tables [t0, t0 + tg) only: the buckets of a few tables stay in L2 while
@@ -319,7 +325,7 @@ __global__ void k_bucket_insert(const typename T::K* __restrict__ keys, uint64_t
         const uint32_t t = t0 + uint32_t(x / n);
         const uint64_t i = x % n;
         typename T::E* bt = buckets + uint64_t(t) * nbuckets * kSlots;
-        const uint64_t key = keys[uint64_t(t) * n + i];
+        const uint64_t key = keys[uint64_t(t - key_t0) * n + i];
         const typename T::E e = T::make(key, uint32_t(i));
         if (filter) {
             const uint32_t r = filter_bit(key, filter_words, kscale);
@@ -1962,21 +1968,24 @@ void build_all(DeviceIndex& ix) {
         if (ix.layout == kLayoutBuckets) {
             auto* bk = static_cast<typename T::E*>(ix.entries.p) + uint64_t(p) * L * ix.nbuckets * kSlots;
             uint32_t* fl = ix.filter_words ? ix.filter.as<uint32_t>() + uint64_t(p) * L * ix.filter_words : nullptr;
-            // keys table-major, then table groups of ~64 MB of buckets (half the L2)
-            K* ktm = static_cast<K*>(keys_tm.ensure(L * n * kb));
-            k_keys_table_major<K><<<unsigned(std::min<uint64_t>(((L + 31) / 32) * ((n + 31) / 32),
-                                                                 uint64_t(sm_count(ix.device)) * 8)),
-                                    256, 0, s>>>(static_cast<const K*>(keys.p), ktm, n, uint32_t(L));
-            FCLSH_LAUNCHED();
+            // keys table-major one slab of tables at a time, then table groups
+            // of ~64 MB of buckets (half the L2) inserted from the slab
             const uint64_t tbytes = ix.nbuckets * kSlots * sizeof(typename T::E);
             const uint32_t tg = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(L, (uint64_t(64) << 20) / tbytes)));
-            for (uint32_t t0 = 0; t0 < L; t0 += tg) {
-                const uint32_t c = uint32_t(std::min<uint64_t>(tg, L - t0));
-                k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(ktm, n, t0, c, ix.key_shift,
-                                                                                      ix.nbuckets, bk, fl,
-                                                                                      ix.filter_words,
-                                                                                      ix.key_scale);
+            const uint32_t slab = uint32_t(std::min<uint64_t>(L, std::max<uint64_t>(tg, kBuildSlab)));
+            K* ktm = static_cast<K*>(keys_tm.ensure(uint64_t(slab) * n * kb));
+            for (uint32_t sb = 0; sb < L; sb += slab) {
+                const uint32_t sc = uint32_t(std::min<uint64_t>(slab, L - sb));
+                k_keys_table_major<K><<<unsigned(std::min<uint64_t>(((sc + 31) / 32) * ((n + 31) / 32),
+                                                                     uint64_t(sm_count(ix.device)) * 8)),
+                                        256, 0, s>>>(static_cast<const K*>(keys.p), ktm, n, uint32_t(L), sb, sc);
                 FCLSH_LAUNCHED();
+                for (uint32_t t0 = sb; t0 < sb + sc; t0 += tg) {
+                    const uint32_t c = uint32_t(std::min<uint64_t>(tg, sb + sc - t0));
+                    k_bucket_insert<T><<<grid_for(n * c, ix.device, 256, 8), 256, 0, s>>>(
+                        ktm, sb, n, t0, c, ix.key_shift, ix.nbuckets, bk, fl, ix.filter_words, ix.key_scale);
+                    FCLSH_LAUNCHED();
+                }
             }
         } else {
             for (uint32_t t = 0; t < L; t += chunk) {
@@ -2578,7 +2587,8 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     // The sparser table is taken when it fits in half the free memory.
     uint32_t bb = bit_length(std::max<uint64_t>(2, (n + 1) / 2) - 1);
     if (bb < 1) bb = 1;
-    auto bkt_fits = [&](uint32_t bits) { return bits <= kbits && (uint64_t(kSlots) << bits) > n; };
+    // slot load <= 75 % at most (longer runs past that)
+    auto bkt_fits = [&](uint32_t bits) { return bits <= 40 && (uint64_t(kSlots) << bits) * 3 >= n * 4; };
     auto bkt_size = [&](uint32_t bits) { return ix->tables * (uint64_t(1) << bits) * kSlots * eb; };
     // CSR directory: 2^b cells, about two postings per cell
     uint32_t b = opt.directory_bits > 0 ? uint32_t(opt.directory_bits)
@@ -2590,8 +2600,18 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
         size_t free_b = 0, total_b = 0;
         FCLSH_CUDA(cudaMemGetInfo(&free_b, &total_b));
         if (opt.mem_budget) free_b = std::min<size_t>(free_b, opt.mem_budget); // (several shards on one GPU)
-        const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * (ix->wide ? 8 : 4) + (uint64_t(2) << 30);
-        if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) ++bb;
+        // the build's transient buffers: one part's point-major keys + one
+        // table-major slab of them
+        const uint64_t kbytes = ix->wide ? 8 : 4;
+        const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * kbytes +
+                                    std::min<uint64_t>(ix->fs->tables, std::max<uint64_t>(kBuildSlab, 64)) * n * kbytes +
+                                    (uint64_t(2) << 30);
+        if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) {
+            ++bb; // slot load <= 25 %
+        } else if (layout != kLayoutCsr && !(bkt_fits(bb) && bkt_size(bb) + need_extra <= free_b) &&
+                   bb > 1 && bkt_fits(bb - 1) && bkt_size(bb - 1) + need_extra <= free_b) {
+            --bb; // the densest tier (load 50-75 %: cfg4's 10M points on one GPU, 137 GB)
+        }
         if (layout == kLayoutAuto)
             layout = (bkt_fits(bb) && bkt_size(bb) + need_extra <= free_b) ? kLayoutBuckets : kLayoutCsr;
     }

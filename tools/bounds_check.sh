@@ -10,7 +10,7 @@ set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 DBG=paper_1602_02620_b200/lib/libfclsh_b200_dbg.so
-[ -f "$DBG" ] || make -C paper_1602_02620_b200 -j8 EXTRA=-DFCLSH_DEBUG_BOUNDS BUILD=build_dbg OUT=lib/libfclsh_b200_dbg.so
+make -C paper_1602_02620_b200 -j8 EXTRA=-DFCLSH_DEBUG_BOUNDS BUILD=build_dbg OUT=lib/libfclsh_b200_dbg.so
 FCLSH_LIB=$PWD/$DBG timeout 3000 python -m pytest tests -q -m gpu -k "not every_key and not full_size" \
   > gpurun_out/bounds_check.log 2>&1
 echo "bounds-checked GPU suite rc=$?" | tee gpurun_out/bounds_check_summary.txt
