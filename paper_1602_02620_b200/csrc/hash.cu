@@ -1129,6 +1129,11 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
         FCLSH_CUDA(cudaMemcpy(fs->col_ptr.ensure(cp.size() * 4), cp.data(), cp.size() * 4, cudaMemcpyHostToDevice));
         FCLSH_CUDA(cudaMemcpy(fs->ent_pos.ensure(epos.size() * 4), epos.data(), epos.size() * 4, cudaMemcpyHostToDevice));
         FCLSH_CUDA(cudaMemcpy(fs->ent_seed.ensure(eseed.size() * 8), eseed.data(), eseed.size() * 8, cudaMemcpyHostToDevice));
+        if (fs->prime <= 0xFFFFFFFFull) { // one 8-byte load per entry (seed < P < 2^32)
+            std::vector<uint64_t> pk(eseed.size());
+            for (size_t k = 0; k < pk.size(); ++k) pk[k] = (eseed[k] << 32) | epos[k];
+            FCLSH_CUDA(cudaMemcpy(fs->ent_pk.ensure(pk.size() * 8), pk.data(), pk.size() * 8, cudaMemcpyHostToDevice));
+        }
     }
 
     // ---------------- fast path tables

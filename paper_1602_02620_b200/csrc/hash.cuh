@@ -43,6 +43,7 @@ struct DeviceFamilySet {
     DevBuf col_ptr;  // uint32 [parts][N+1]
     DevBuf ent_pos;  // uint32 [parts][max_dims]
     DevBuf ent_seed; // uint64 [parts][max_dims]
+    DevBuf ent_pk;   // uint64 [parts][max_dims]: seed << 32 | source bit, primes < 2^32 (the fused query hash)
     uint64_t max_part_dims = 0;
     DevBuf scratch;  // generic path workspace
 

@@ -227,6 +227,32 @@ __device__ __forceinline__ bool filter_pass(const Tables<T>& tb, uint32_t t, uin
     return (ld_filter(tb.filter + uint64_t(t) * tb.filter_words + (r >> 5), pol) >> (r & 31)) & 1u;
 }
 
+// Address-translation warm-up: one L2 prefetch per 2 MB page of the tables,
+// spread over the grid, issued as the first query kernel of a batch starts.
+// A probe's random bucket read is also a random page: after the L2 has been
+// flushed (between the bench's steps, or by other work) the page-table
+// entries of a 34 GB table are cold, and the first touches of its 17k pages
+// each wait on a page walk (tools/lat_bench.cu: 3.3 us per dependent read
+// for 1184 warps over 34 GB right after a flush, 0.74 us warm; touching
+// every page first takes ~12 us and is overlapped with the query hash here).
+template <typename T, int LAYOUT>
+__device__ __forceinline__ void warm_pages(const Tables<T>& tb, uint32_t tables) {
+    using E = typename T::E;
+    const uint64_t bytes = LAYOUT == kLayoutCsr ? uint64_t(tables) * tb.n * sizeof(E)
+                                                : uint64_t(tables) * tb.nbuckets * kSlots * sizeof(E);
+    const uint64_t pages = (bytes + (uint64_t(1) << 21) - 1) >> 21;
+    const uint64_t dpages = LAYOUT == kLayoutCsr ? ((uint64_t(tables) * (tb.cells + 1) * 4 + (uint64_t(1) << 21) - 1) >> 21) : 0;
+#ifdef FCLSH_NO_WARM // (A/B builds)
+    if (pages) return;
+#endif
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pages + dpages; i += stride) {
+        const char* a = i < pages ? reinterpret_cast<const char*>(tb.data) + (i << 21)
+                                  : reinterpret_cast<const char*>(tb.dir) + ((i - pages) << 21);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
 // First position in [a, e) of a CSR cell (sorted by (key, id)) whose key is
 // >= key. Clustered data makes some cells long (a run of one popular key),
 // and every other key of that cell would otherwise scan past the run.
@@ -918,12 +944,34 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
 // the batch's key array (read back by this warp and, for handed-over
 // queries, by the other query kernels); the row stays in registers, and
 // rows read from mapped host memory are also copied to the device rows.
+// FCLSH_TRACE builds (tools/trace_query.py; never the shipped library): the
+// warp kernel stamps each query's phases -- globaltimer at start and end,
+// SM clocks at the end of the hash, the probes and the verify -- into
+// g_trace[q * 8 ..], which the host appends to $FCLSH_TRACE_OUT per batch.
+#ifdef FCLSH_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define FCLSH_TRACE_STAMP(q, k, v) \
+    do { \
+        if (g_trace && lane == 0) g_trace[(q) * 8 + (k)] = (v); \
+    } while (0)
+#else
+#define FCLSH_TRACE_STAMP(q, k, v) \
+    do { \
+    } while (0)
+#endif
+
 struct FusedHash {
     uint32_t parts = 0, N = 0, L = 0;
     uint64_t max_dims = 0;
     const uint32_t* col_ptr = nullptr; // [parts][N+1]
     const uint32_t* ent_pos = nullptr; // [parts][max_dims] source-row bit
     const uint64_t* ent_seed = nullptr;
+    const uint64_t* ent_pk = nullptr; // [parts][max_dims] seed << 32 | source bit
     uint64_t prime = 0;
     const uint64_t* hash_src = nullptr; // mapped pinned host rows (null: the device rows)
 };
@@ -951,23 +999,38 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
     const uint64_t P = fh.prime;
     for (uint32_t p = 0; p < fh.parts; ++p) {
         const uint32_t* cp = fh.col_ptr + uint64_t(p) * (fh.N + 1);
-        const uint32_t* ep = fh.ent_pos + uint64_t(p) * fh.max_dims;
-        const uint64_t* es = fh.ent_seed + uint64_t(p) * fh.max_dims;
+        const uint64_t* pk = fh.ent_pk + uint64_t(p) * fh.max_dims;
+        // the sketch of the lane's FE columns: every column's (seed, bit)
+        // entries are loaded kBatch at a time for all FE columns at once (no
+        // load waits on another: two L2 round trips per batch of kBatch * FE
+        // entries instead of one per entry); a missing entry loads as 0 = seed 0
+        constexpr int kBatch = 4;
+        uint32_t b0[FE], cnt[FE], mx = 0;
         long long t[FE];
 #pragma unroll
         for (int i = 0; i < FE; ++i) {
             const uint32_t c = uint32_t(lane) + 32u * i;
-            const uint32_t b0 = __ldg(cp + c), cnt = __ldg(cp + c + 1) - b0;
-            const uint32_t m = __reduce_max_sync(kAll, cnt); // warp-uniform trip count (the shuffle needs every lane)
-            long long acc = 0;
-            for (uint32_t k = 0; k < m; ++k) {
-                const bool has = k < cnt;
-                const uint32_t pos = has ? __ldg(ep + b0 + k) : 0u;
-                FCLSH_DCHECK((pos >> 6) < words && b0 + cnt <= fh.max_dims);
-                const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
-                if (has && ((w >> (pos & 63)) & 1)) acc += (long long)__ldg(es + b0 + k);
-            }
-            t[i] = acc;
+            b0[i] = __ldg(cp + c);
+            cnt[i] = __ldg(cp + c + 1) - b0[i];
+            mx = max(mx, cnt[i]);
+            t[i] = 0;
+        }
+        const uint32_t m = __reduce_max_sync(kAll, mx); // warp-uniform trip count (the shuffles need every lane)
+        for (uint32_t k0 = 0; k0 < m; k0 += kBatch) {
+            uint64_t e[FE][kBatch];
+#pragma unroll
+            for (int i = 0; i < FE; ++i)
+#pragma unroll
+                for (int k = 0; k < kBatch; ++k) e[i][k] = k0 + k < cnt[i] ? __ldg(pk + b0[i] + k0 + k) : 0ull;
+#pragma unroll
+            for (int i = 0; i < FE; ++i)
+#pragma unroll
+                for (int k = 0; k < kBatch; ++k) {
+                    const uint32_t pos = uint32_t(e[i][k]);
+                    FCLSH_DCHECK((pos >> 6) < words && b0[i] + cnt[i] <= fh.max_dims);
+                    const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
+                    if ((w >> (pos & 63)) & 1) t[i] += (long long)(e[i][k] >> 32);
+                }
         }
 #pragma unroll
         for (int h = 1; h < FE; h <<= 1) { // index bits 5.. : within the lane
@@ -1024,19 +1087,42 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
+    warm_pages<T, kLayoutBuckets>(tb, tables);
     pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
+    // the grid's warps take queries 0 .. warps-1 directly (no atomic storm on
+    // one counter as every warp starts), later ones from the counter
+    const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+    bool first = true;
     auto fetch = [&]() -> uint64_t {
+        if (first) {
+            first = false;
+            return gwarp;
+        }
         unsigned int v = 0;
-        if (lane == 0) v = atomicAdd(qnext, 1u);
+        if (lane == 0) v = nwarp + atomicAdd(qnext, 1u);
         return __shfl_sync(kAll, v, 0);
     };
+#ifdef FCLSH_TRACE
+    const unsigned long long t_entry = gtimer();
+#endif
     for (uint64_t q = fetch(); q < nq; q = fetch()) {
         const K* qk = qkeys + q * tables;
         uint64_t rw = 0; // FE > 0: word `lane` of the query row
+#ifdef FCLSH_TRACE
+        const long long c0 = clock64();
+        FCLSH_TRACE_STAMP(q, 0, gtimer());
+        FCLSH_TRACE_STAMP(q, 6, t_entry);
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        FCLSH_TRACE_STAMP(q, 5, smid);
+#endif
         if constexpr (FE > 0) {
             fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
+#ifdef FCLSH_TRACE
+        FCLSH_TRACE_STAMP(q, 2, clock64() - c0);
+#endif
         // FE > 0: the keys were written by this warp a moment ago: coherent
         // L2 loads, not the read-only path
         auto ldk = [&](uint32_t t) -> K {
@@ -1146,6 +1232,9 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             }
         }
         const uint64_t m = __reduce_add_sync(kAll, coll);
+#ifdef FCLSH_TRACE
+        FCLSH_TRACE_STAMP(q, 3, clock64() - c0);
+#endif
         // verify the listed ids, one per lane
         uint32_t dist = 0;
         if constexpr (FE > 0) { // the query row is in registers (word w on lane w)
@@ -1197,8 +1286,45 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             src_pos[q] = q * slot_cap;
             if (nfound) atomicAdd(tile_sum + (q >> kScanTileLog), (unsigned long long)nfound);
         }
+#ifdef FCLSH_TRACE
+        FCLSH_TRACE_STAMP(q, 4, clock64() - c0);
+        FCLSH_TRACE_STAMP(q, 1, gtimer());
+        FCLSH_TRACE_STAMP(q, 7, nd);
+#endif
     }
 }
+
+// Exclusive prefix sum of v over the CTA's threads (blockDim.x a multiple of
+// 32, <= 1024); ws: 32 words of shared scratch; total = the CTA's sum.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* ws, uint32_t& total) {
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= uint32_t(o)) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < nw ? ws[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= uint32_t(o)) w += y;
+        }
+        ws[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t excl = x - v + (wid ? ws[wid - 1] : 0u);
+    total = ws[nw - 1];
+    __syncthreads(); // ws may be reused
+    return excl;
+}
+
+constexpr int kFlatTables = 2048; // CSR tables the CTA kernel's flattened probe phase handles
+constexpr int kFlatU = 4;         // cell entries per thread in flight there
+constexpr size_t kFlatSmem = size_t(kFlatTables + 2) * 4 + size_t(kFlatTables + 2) * 4 + size_t(kFlatTables) * 8 + 16;
 
 // Dense queries (clustered data, cfg4): one CTA per query. Dedup is a
 // shared-memory open-addressing id set instead of a sort of the collision
@@ -1234,6 +1360,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
     __shared__ unsigned int coll_s, cand_s, found_s;
     __shared__ volatile int bad_s;
     __shared__ unsigned long long base_s;
+    __shared__ uint32_t scan_ws[32];
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     pdl_trigger();
@@ -1341,6 +1468,74 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
                     }
                 }
             }
+        } else if (LAYOUT == kLayoutCsr && tables <= uint32_t(kFlatTables)) {
+            // CSR, flattened: the directory read of every table first (its
+            // cell [s, e) and the query's key into shared memory), a block
+            // scan of the cell lengths, then the CTA's threads take the
+            // concatenated cells' entries j = tid, tid + nt, ... (kFlatU in
+            // flight each) and keep the ones with their table's key. A
+            // popular key's long cell is read by many threads at once
+            // (adjacent entries, coalesced) instead of walked by one thread
+            // while the CTA waits for it at the barrier.
+            using E = typename T::E;
+            uint32_t* const f_off = reinterpret_cast<uint32_t*>(clist + kMaxDistinct + (kMaxDistinct & 1)); // [tables + 1]
+            uint32_t* const f_start = f_off + kFlatTables + 1;                                              // [tables]
+            uint64_t* const f_key = reinterpret_cast<uint64_t*>(f_start + kFlatTables + (kFlatTables & 1) + 1); // [tables]
+            constexpr int kPer = (kFlatTables + 511) / 512; // tables per thread (blockDim.x = 512)
+            uint32_t len[kPer], loc = 0;
+            const uint32_t tb0 = tid * kPer;
+            uint64_t key[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) key[k] = tb0 + k < tables ? uint64_t(qk[tb0 + k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const uint32_t t = tb0 + k;
+                len[k] = 0;
+                if (t < tables) {
+                    const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[k], tb);
+                    const uint32_t a = __ldg(d), e = __ldg(d + 1);
+                    f_start[t] = a;
+                    f_key[t] = key[k];
+                    len[k] = e - a;
+                }
+                loc += len[k];
+            }
+            uint32_t total = 0;
+            uint32_t run = block_exclusive_scan(loc, scan_ws, total);
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                if (tb0 + k < tables) f_off[tb0 + k] = run;
+                run += len[k];
+            }
+            if (tid == 0) f_off[tables] = total;
+            __syncthreads();
+            for (uint32_t j0 = tid; j0 < total && !bad_s; j0 += kFlatU * nt) {
+                E e[kFlatU];
+                uint32_t tt[kFlatU];
+#pragma unroll
+                for (int u = 0; u < kFlatU; ++u) {
+                    const uint32_t j = j0 + u * nt;
+                    tt[u] = ~0u;
+                    if (j < total) {
+                        uint32_t lo = 0, hi = tables; // the table t with f_off[t] <= j < f_off[t + 1]
+                        while (hi - lo > 1) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (f_off[mid] <= j)
+                                lo = mid;
+                            else
+                                hi = mid;
+                        }
+                        tt[u] = lo;
+                        e[u] = tb.data[uint64_t(lo) * tb.n + f_start[lo] + (j - f_off[lo])];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kFlatU; ++u)
+                    if (tt[u] != ~0u && T::key(e[u]) == f_key[tt[u]]) {
+                        ++coll;
+                        insert(T::id(e[u]));
+                    }
+            }
         } else {
             for (uint32_t t = tid; t < tables; t += nt) {
                 if (bad_s) break;
@@ -1421,7 +1616,6 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
         __syncthreads();
     }
 }
-
 
 struct NarrowIdOrder {
     __device__ __forceinline__ static bool less(uint32_t a, uint32_t b) { return a < b; }
@@ -2023,6 +2217,7 @@ FusedHash fused_params(const DeviceIndex& ix, const uint64_t* hash_src) {
     f.L = uint32_t(fs.tables);
     f.max_dims = fs.max_part_dims;
     f.col_ptr = fs.col_ptr.as<uint32_t>();
+    f.ent_pk = fs.ent_pk.as<uint64_t>();
     f.ent_pos = fs.ent_pos.as<uint32_t>();
     f.ent_seed = fs.ent_seed.as<uint64_t>();
     f.prime = fs.prime;
@@ -2123,7 +2318,8 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 uint64_t max_grid, unsigned long long* tile_sum, const unsigned long long* desc, uint64_t nq_all,
                 uint32_t slot_cap, uint32_t* slot_id, uint32_t* slot_dist, cudaStream_t s) {
     auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
-    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2;
+    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2 +
+                        (LAYOUT == kLayoutCsr ? kFlatSmem : 0);
     const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
     // persistent grid: the overflow count is only known on the device
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
@@ -2225,8 +2421,10 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
     // full grid still costs ~4 us; a batch handing over more than the last
     // one did still completes (queries are handed out dynamically)
     const uint64_t dense_grid = std::max<uint64_t>(32, 2 * ix.last_dense);
-    // Many tables (cfg4: 1022): CTA per query for every query (measured
-    // faster than the warp kernel there, clustered or sharded).
+    // Many tables (cfg4: 1022): the CTA kernel for every query (a warp per
+    // query with a shared id set measured slower there: one 1.25M-point
+    // shard 0.44 vs 0.38 ms per 10k batch, the shared-memory atomics and run
+    // walks serialise inside a warp; profiles/r02/cfg4_dense.md).
     const bool dense_all = big;
     if (!ix.h_pub) {
         // [0] total, [1] [2] overflow counts, [3] sequence, [4..8] HostDest
@@ -2271,7 +2469,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
         // the way; with the hash fused into the query kernel it does both
-        const bool fused_hash = !dense_all && fused_fe(ix) > 0;
+        const bool fused_hash = !big && fused_fe(ix) > 0;
         if (!fused_hash)
             hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
                       hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
@@ -2310,6 +2508,14 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         h[4] = host_cnt ? dest->cap : 0;
         std::atomic_thread_fence(std::memory_order_release);
     }
+#ifdef FCLSH_TRACE
+    {
+        static DevBuf tbuf; // (trace builds: single-threaded tools only)
+        void* tp = tbuf.ensure(std::max<uint64_t>(1, nq) * 64);
+        FCLSH_CUDA(cudaMemsetAsync(tp, 0, std::max<uint64_t>(1, nq) * 64, s));
+        FCLSH_CUDA(cudaMemcpyToSymbolAsync(g_trace, &tp, sizeof(tp), 0, cudaMemcpyHostToDevice, s));
+    }
+#endif
     DeviceIndex::Pending& p = ix.pending;
     p.nq = nq;
     p.radius = radius;
@@ -2389,6 +2595,20 @@ QueryOutput query_finish_impl(DeviceIndex& ix) {
     } hs{0, {0, 0}};
     if (nq) {
         wait_published(ix.h_pub, p.seq, s);
+#ifdef FCLSH_TRACE
+        if (const char* path = getenv("FCLSH_TRACE_OUT")) {
+            unsigned long long* tp = nullptr;
+            FCLSH_CUDA(cudaMemcpyFromSymbol(&tp, g_trace, sizeof(tp)));
+            std::vector<unsigned long long> h(nq * 8);
+            FCLSH_CUDA(cudaMemcpy(h.data(), tp, nq * 64, cudaMemcpyDeviceToHost));
+            if (FILE* f = fopen(path, "ab")) {
+                const unsigned long long hdr[2] = {nq, 8};
+                fwrite(hdr, 8, 2, f);
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+#endif
         hs.total = ix.h_pub[0];
         hs.cnt[0] = unsigned(ix.h_pub[1]);
         hs.cnt[1] = unsigned(ix.h_pub[2]);
@@ -2587,8 +2807,8 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
     // The sparser table is taken when it fits in half the free memory.
     uint32_t bb = bit_length(std::max<uint64_t>(2, (n + 1) / 2) - 1);
     if (bb < 1) bb = 1;
-    // slot load <= 75 % at most (longer runs past that)
-    auto bkt_fits = [&](uint32_t bits) { return bits <= 40 && (uint64_t(kSlots) << bits) * 3 >= n * 4; };
+    // slot load <= 50 %, and no more buckets than keys
+    auto bkt_fits = [&](uint32_t bits) { return bits <= std::min<uint32_t>(kbits, 40) && (uint64_t(kSlots) << bits) > n; };
     auto bkt_size = [&](uint32_t bits) { return ix->tables * (uint64_t(1) << bits) * kSlots * eb; };
     // CSR directory: 2^b cells, about two postings per cell
     uint32_t b = opt.directory_bits > 0 ? uint32_t(opt.directory_bits)
@@ -2606,12 +2826,11 @@ std::unique_ptr<DeviceIndex> build_index(const uint64_t* rows, bool rows_on_devi
         const uint64_t need_extra = n * W * 8 + ix->fs->tables * n * kbytes +
                                     std::min<uint64_t>(ix->fs->tables, std::max<uint64_t>(kBuildSlab, 64)) * n * kbytes +
                                     (uint64_t(2) << 30);
-        if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) {
-            ++bb; // slot load <= 25 %
-        } else if (layout != kLayoutCsr && !(bkt_fits(bb) && bkt_size(bb) + need_extra <= free_b) &&
-                   bb > 1 && bkt_fits(bb - 1) && bkt_size(bb - 1) + need_extra <= free_b) {
-            --bb; // the densest tier (load 50-75 %: cfg4's 10M points on one GPU, 137 GB)
-        }
+        // (a 50-75 % tier that fits cfg4's 10M points on one GPU in 137 GB
+        // measured slower than CSR there: 2.34 vs 1.14 ms per 10k batch; at
+        // that load a probe reads 2.25 buckets on average, p99 23, and the
+        // runs are dependent reads; profiles/r02/cfg4_dense.md)
+        if (layout != kLayoutCsr && bkt_fits(bb + 1) && bkt_size(bb + 1) + need_extra <= free_b / 2) ++bb; // load <= 25 %
         if (layout == kLayoutAuto)
             layout = (bkt_fits(bb) && bkt_size(bb) + need_extra <= free_b) ? kLayoutBuckets : kLayoutCsr;
     }

@@ -129,6 +129,26 @@ def test_many_tables_cta_per_query(oracle):
     assert ix.path_counts() == {"dense": q.shape[0], "general": 1}
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_many_tables_clustered(oracle, layout):
+    """cfg4's shape in small: > 600 tables over clustered rows, every query
+    in the CTA kernel (CSR: the flattened probe phase). Most queries have tens
+    to hundreds of distinct candidates and more than 32 results (the shared
+    result region); queries near a 1500-point cluster read cells of ~1500
+    entries."""
+    d, radius = 96, 9
+    rows = F.gen_clustered(9, 60, 6000, d, 0.04)
+    tight = F.gen_clustered(10, 1, 1500, d, 0.01)
+    rows[:1500] = tight
+    q = np.concatenate([F.gen_clustered(9, 60, 6300, d, 0.04)[6000:], tight[:5]])
+    res = _check_one(oracle, rows, q, d, radius, (0, 1), M31, 11, 22, None, 0, layout)
+    assert (res.found > 32).sum() >= 20 and res.candidates.max() > 768
+    plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, F.PlanOverride(F.PlanKind.identity, 1))
+    ix = F.build_index(rows, radius, plan, 22, prime=M31, layout=layout)
+    ix.query_r_nn(q, radius)
+    assert ix.path_counts() == {"dense": q.shape[0], "general": 0}
+
+
 def _device_triples(r):
     import torch
     tri = torch.zeros((3, max(r.total, 1)), dtype=torch.int32, device="cuda")

@@ -19,23 +19,28 @@ if what in ("all", "query", "cfg2", "cfg3", "cfg1"):
     cfg = CONFIGS[{"cfg3": 3, "cfg1": 1}.get(what, 2)]
     data = make_data(cfg)
     q = make_queries(cfg, data)
+    if os.environ.get("NQ"):  # a smaller batch (latency studies)
+        q = q[:int(os.environ["NQ"])]
     plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg.plan_seed(), cfg.override())
     ix = F.build_index(data, cfg.radius, plan, cfg.index_seed(), prime=F.M31)
     qd = torch.from_numpy(q.view(np.int64)).cuda()
     for _ in range(2):
         ix.query_device(qd, cfg.radius)
     torch.cuda.synchronize()
-if what in ("cfg4shard", "cfg4"):
-    # cfg4: shard 0 of the 8-shard layout (buckets), or the whole 10M index (CSR)
+if what in ("cfg4shard", "cfg4", "cfg4csr"):
+    # cfg4: shard 0 of the 8-shard layout (buckets), or the whole 10M index
+    # (automatic layout, or CSR forced)
     from paper_1602_02620_b200 import cluster
     cfg = CONFIGS[4]
     data = make_data(cfg, 16)
     q = make_queries(cfg, data, 16)
     b, e = cluster.shard_range(cfg.n, cfg.shards, 0) if what == "cfg4shard" else (0, cfg.n)
     plan = F.make_plan(cfg.dims, cfg.radius, 1.0, cfg.n, cfg.plan_seed(), cfg.override())
-    ix = F.build_index(data[b:e], cfg.radius, plan, cfg.index_seed(), prime=F.M31, id_offset=b)
+    kw = {"layout": "csr"} if what == "cfg4csr" else {}
+    ix = F.build_index(data[b:e], cfg.radius, plan, cfg.index_seed(), prime=F.M31, id_offset=b, **kw)
     qd = torch.from_numpy(q.view(np.int64)).cuda()
-    for _ in range(2):
+    ix.stage_timing(True)
+    for _ in range(3):
         ix.query_device(qd, cfg.radius)
     torch.cuda.synchronize()
     print(what, ix.layout, ix.stage_ms(), ix.path_counts())
