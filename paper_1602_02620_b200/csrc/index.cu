@@ -227,32 +227,6 @@ __device__ __forceinline__ bool filter_pass(const Tables<T>& tb, uint32_t t, uin
     return (ld_filter(tb.filter + uint64_t(t) * tb.filter_words + (r >> 5), pol) >> (r & 31)) & 1u;
 }
 
-// Address-translation warm-up: one L2 prefetch per 2 MB page of the tables,
-// spread over the grid, issued as the first query kernel of a batch starts.
-// A probe's random bucket read is also a random page: after the L2 has been
-// flushed (between the bench's steps, or by other work) the page-table
-// entries of a 34 GB table are cold, and the first touches of its 17k pages
-// each wait on a page walk (tools/lat_bench.cu: 3.3 us per dependent read
-// for 1184 warps over 34 GB right after a flush, 0.74 us warm; touching
-// every page first takes ~12 us and is overlapped with the query hash here).
-template <typename T, int LAYOUT>
-__device__ __forceinline__ void warm_pages(const Tables<T>& tb, uint32_t tables) {
-    using E = typename T::E;
-    const uint64_t bytes = LAYOUT == kLayoutCsr ? uint64_t(tables) * tb.n * sizeof(E)
-                                                : uint64_t(tables) * tb.nbuckets * kSlots * sizeof(E);
-    const uint64_t pages = (bytes + (uint64_t(1) << 21) - 1) >> 21;
-    const uint64_t dpages = LAYOUT == kLayoutCsr ? ((uint64_t(tables) * (tb.cells + 1) * 4 + (uint64_t(1) << 21) - 1) >> 21) : 0;
-#ifdef FCLSH_NO_WARM // (A/B builds)
-    if (pages) return;
-#endif
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pages + dpages; i += stride) {
-        const char* a = i < pages ? reinterpret_cast<const char*>(tb.data) + (i << 21)
-                                  : reinterpret_cast<const char*>(tb.dir) + ((i - pages) << 21);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    }
-}
-
 // First position in [a, e) of a CSR cell (sorted by (key, id)) whose key is
 // >= key. Clustered data makes some cells long (a run of one popular key),
 // and every other key of that cell would otherwise scan past the run.
@@ -1087,7 +1061,6 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
-    warm_pages<T, kLayoutBuckets>(tb, tables);
     pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
     // the grid's warps take queries 0 .. warps-1 directly (no atomic storm on
     // one counter as every warp starts), later ones from the counter
