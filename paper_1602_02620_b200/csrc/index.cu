@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
 // FCLSH_TRACE builds (tools/trace_query.py; never the shipped library): the
 // warp kernel stamps each query's phases -- globaltimer at start and end,
 // SM clocks at the end of the hash, the probes and the verify -- into
-// g_trace[q * 8 ..], which the host appends to $FCLSH_TRACE_OUT per batch.
+// g_trace[q * 16 ..] (8..15: SM clocks at the end of each probe round), which the host appends to $FCLSH_TRACE_OUT per batch.
 #ifdef FCLSH_TRACE
 __device__ unsigned long long* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -931,7 +931,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define FCLSH_TRACE_STAMP(q, k, v) \
     do { \
-        if (g_trace && lane == 0) g_trace[(q) * 8 + (k)] = (v); \
+        if (g_trace && lane == 0) g_trace[(q) * 16 + (k)] = (v); \
     } while (0)
 #else
 #define FCLSH_TRACE_STAMP(q, k, v) \
@@ -1203,6 +1203,9 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                 p0[u] = p1[u];
                 k1[u] = k2[u];
             }
+#ifdef FCLSH_TRACE
+            if (base_t / kStep < 8) FCLSH_TRACE_STAMP(q, 8 + base_t / kStep, clock64() - c0);
+#endif
         }
         const uint64_t m = __reduce_add_sync(kAll, coll);
 #ifdef FCLSH_TRACE
@@ -2484,8 +2487,8 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
 #ifdef FCLSH_TRACE
     {
         static DevBuf tbuf; // (trace builds: single-threaded tools only)
-        void* tp = tbuf.ensure(std::max<uint64_t>(1, nq) * 64);
-        FCLSH_CUDA(cudaMemsetAsync(tp, 0, std::max<uint64_t>(1, nq) * 64, s));
+        void* tp = tbuf.ensure(std::max<uint64_t>(1, nq) * 128);
+        FCLSH_CUDA(cudaMemsetAsync(tp, 0, std::max<uint64_t>(1, nq) * 128, s));
         FCLSH_CUDA(cudaMemcpyToSymbolAsync(g_trace, &tp, sizeof(tp), 0, cudaMemcpyHostToDevice, s));
     }
 #endif
@@ -2572,10 +2575,10 @@ QueryOutput query_finish_impl(DeviceIndex& ix) {
         if (const char* path = getenv("FCLSH_TRACE_OUT")) {
             unsigned long long* tp = nullptr;
             FCLSH_CUDA(cudaMemcpyFromSymbol(&tp, g_trace, sizeof(tp)));
-            std::vector<unsigned long long> h(nq * 8);
-            FCLSH_CUDA(cudaMemcpy(h.data(), tp, nq * 64, cudaMemcpyDeviceToHost));
+            std::vector<unsigned long long> h(nq * 16);
+            FCLSH_CUDA(cudaMemcpy(h.data(), tp, nq * 128, cudaMemcpyDeviceToHost));
             if (FILE* f = fopen(path, "ab")) {
-                const unsigned long long hdr[2] = {nq, 8};
+                const unsigned long long hdr[2] = {nq, 16};
                 fwrite(hdr, 8, 2, f);
                 fwrite(h.data(), 8, h.size(), f);
                 fclose(f);

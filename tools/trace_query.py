@@ -58,6 +58,13 @@ print("duration       ", pct(en - st))
 print("  hash         ", pct(hs))
 print("  probes       ", pct(pr))
 print("  verify+out   ", pct(vf))
+prev = t[:, 2]
+for r in range(8):
+    c = t[:, 8 + r]
+    if not (c > 0).any():
+        break
+    print(f"  round {r}      ", pct((c - prev) / ghz / 1e3))
+    prev = c
 order = np.argsort(st)
 for lo in range(0, int(en.max()) + 10, 10):
     live = ((st <= lo + 10) & (en >= lo)).sum()
