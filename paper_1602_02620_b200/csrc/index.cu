@@ -99,9 +99,6 @@ constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 #ifndef FCLSH_DENSE_RUN
 #define FCLSH_DENSE_RUN 2
 #endif
-#ifndef FCLSH_DENSE_MINB
-#define FCLSH_DENSE_MINB 2
-#endif
 constexpr int kDenseU = FCLSH_DENSE_U;     // home buckets per thread in flight in the CTA kernel
 constexpr int kDenseRun = FCLSH_DENSE_RUN; // buckets read at a time along a spilled run (CTA kernel)
 constexpr int kFusedU = FCLSH_FUSED_U; // tables per lane in flight in the warp kernel
@@ -1315,8 +1312,8 @@ constexpr size_t kFlatSmem = size_t(kFlatTables + 2) * 4 + size_t(kFlatTables + 
 // 3/4 * HS or more distinct candidates or more than FCAP results, or whose
 // results do not fit the region, goes to the general path (ovf2), which
 // recomputes all its outputs.
-template <typename T, int LAYOUT, int HS, int FCAP>
-__global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
+template <typename T, int LAYOUT, int HS, int FCAP, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_query_dense(
     const typename T::K* __restrict__ qkeys, uint32_t tables, const Tables<T> tb, const uint64_t* __restrict__ rows,
     const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius, const uint32_t* __restrict__ ovf,
     const unsigned int* __restrict__ ovf_cnt, uint32_t direct_n, unsigned long long* __restrict__ coll_q,
@@ -1457,7 +1454,7 @@ __global__ void __launch_bounds__(512, FCLSH_DENSE_MINB) k_query_dense(
             uint32_t* const f_off = reinterpret_cast<uint32_t*>(clist + kMaxDistinct + (kMaxDistinct & 1)); // [tables + 1]
             uint32_t* const f_start = f_off + kFlatTables + 1;                                              // [tables]
             uint64_t* const f_key = reinterpret_cast<uint64_t*>(f_start + kFlatTables + (kFlatTables & 1) + 1); // [tables]
-            constexpr int kPer = (kFlatTables + 511) / 512; // tables per thread (blockDim.x = 512)
+            constexpr int kPer = (kFlatTables + NT - 1) / NT; // tables per thread
             uint32_t len[kPer], loc = 0;
             const uint32_t tb0 = tid * kPer;
             uint64_t key[kPer];
@@ -2281,11 +2278,21 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
     FCLSH_LAUNCHED();
 }
 
-constexpr int kDenseSet = 8192;   // id-set slots per dense query (< 6144 distinct candidates)
-constexpr int kDenseFound = 2048; // results per dense query
-constexpr int kDenseThreads = 512;
+// CTA-kernel shapes (id-set slots: < 3/4 of them distinct candidates; found
+// list; threads; CTAs per SM). Big: the warp kernel's hand-over (its heavy
+// queries) and CSR indexes (the flattened probe phase wants many threads per
+// query). Small: bucket indexes of > 600 tables, every query (cfg4's shards):
+// more queries in flight per SM hide the per-query barriers better -- one
+// 1.25M-point cfg4 shard 0.377 -> 0.298 ms per 10k batch; queries beyond its
+// set or list go on to the general path (profiles/r02/cfg4_dense.md).
+struct DenseBig {
+    static constexpr int HS = 8192, FCAP = 2048, NT = 512, MINB = 2;
+};
+struct DenseSmall {
+    static constexpr int HS = 2048, FCAP = 1024, NT = 128, MINB = 8;
+};
 
-template <typename T, int LAYOUT>
+template <typename T, int LAYOUT, typename S>
 void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d_q, uint32_t radius,
                 const uint32_t* ovf, const unsigned int* ovf_cnt, uint64_t direct_n, unsigned long long* coll_q,
                 unsigned long long* cand_q, unsigned long long* found_q, unsigned long long* src_pos,
@@ -2293,15 +2300,15 @@ void launch_dense(DeviceIndex& ix, const typename T::K* qkeys, const uint64_t* d
                 unsigned long long* res_cursor, uint32_t* ovf2, unsigned int* ovf2_cnt, unsigned int* qnext,
                 uint64_t max_grid, unsigned long long* tile_sum, const unsigned long long* desc, uint64_t nq_all,
                 uint32_t slot_cap, uint32_t* slot_id, uint32_t* slot_dist, cudaStream_t s) {
-    auto kern = k_query_dense<T, LAYOUT, kDenseSet, kDenseFound>;
-    const size_t smem = size_t(kDenseFound) * 8 + size_t(kDenseSet) * 4 + size_t(kDenseSet) / 4 * 3 * 2 +
+    auto kern = k_query_dense<T, LAYOUT, S::HS, S::FCAP, S::NT, S::MINB>;
+    const size_t smem = size_t(S::FCAP) * 8 + size_t(S::HS) * 4 + size_t(S::HS) / 4 * 3 * 2 +
                         (LAYOUT == kLayoutCsr ? kFlatSmem : 0);
-    const int per_sm = resident_ctas(kern, kDenseThreads, smem, ix.device);
+    const int per_sm = resident_ctas(kern, S::NT, smem, ix.device);
     // persistent grid: the overflow count is only known on the device
     uint64_t grid = uint64_t(std::max(per_sm, 1)) * sm_count(ix.device);
     if (!ovf) grid = std::max<uint64_t>(1, std::min(grid, direct_n));
     else grid = std::max<uint64_t>(1, std::min(grid, max_grid)); // sized by the last batch's hand-over
-    launch_pdl(kern, unsigned(grid), kDenseThreads, smem, s, qkeys, uint32_t(ix.tables), view<T>(ix),
+    launch_pdl(kern, unsigned(grid), S::NT, smem, s, qkeys, uint32_t(ix.tables), view<T>(ix),
                ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, ovf, ovf_cnt, uint32_t(direct_n), coll_q, cand_q,
                found_q, src_pos, src_base, res_id, res_dist, res_cap, res_cursor, ovf2, ovf2_cnt, qnext, tile_sum, desc,
                nq_all, slot_cap, slot_id, slot_dist, vec_for(ix.row_words, d_q));
@@ -2456,10 +2463,21 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
                                                b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
                                                b.tile_sum, d_desc, s, fused_hash ? hash_src : nullptr);
         rec(2);
-        launch_dense<T, LAYOUT>(ix, qkeys, d_q, radius, dense_all ? nullptr : b.ovf, b.ovf_cnt, nq, b.coll_q,
-                                b.cand_q, b.found_q, b.src_pos, nq * slot_cap, b.cta_id, b.cta_dist, b.cta_cap,
-                                b.res_cursor, b.ovf2, b.ovf_cnt + 1, b.ovf_cnt + 5, dense_grid, b.tile_sum, d_desc, nq,
-                                slot_cap, b.tmp_id, b.tmp_dist, s);
+        auto dense = [&](auto shape) {
+            launch_dense<T, LAYOUT, decltype(shape)>(ix, qkeys, d_q, radius, dense_all ? nullptr : b.ovf, b.ovf_cnt,
+                                                     nq, b.coll_q, b.cand_q, b.found_q, b.src_pos, nq * slot_cap,
+                                                     b.cta_id, b.cta_dist, b.cta_cap, b.res_cursor, b.ovf2,
+                                                     b.ovf_cnt + 1, b.ovf_cnt + 5, dense_grid, b.tile_sum, d_desc, nq,
+                                                     slot_cap, b.tmp_id, b.tmp_dist, s);
+        };
+        if constexpr (LAYOUT == kLayoutBuckets) {
+            if (dense_all)
+                dense(DenseSmall{});
+            else
+                dense(DenseBig{});
+        } else {
+            dense(DenseBig{});
+        }
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
         launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit), 1024, 0, s, nq,

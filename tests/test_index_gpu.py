@@ -146,7 +146,9 @@ def test_many_tables_clustered(oracle, layout):
     plan = F.make_plan(d, radius, 1.0, rows.shape[0], 11, F.PlanOverride(F.PlanKind.identity, 1))
     ix = F.build_index(rows, radius, plan, 22, prime=M31, layout=layout)
     ix.query_r_nn(q, radius)
-    assert ix.path_counts() == {"dense": q.shape[0], "general": 0}
+    # (buckets: the small CTA shape holds up to 1024 results, so the five
+    # queries with ~1500 go on to the general path)
+    assert ix.path_counts() == {"dense": q.shape[0], "general": 5 if layout == "buckets" else 0}
 
 
 def _device_triples(r):
