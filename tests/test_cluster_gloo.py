@@ -50,7 +50,6 @@ def _worker(rank, world, port, outdir):
     counters, offsets, ids = ix.query(q, 4)
     nq = q.shape[0]
     qcol = np.repeat(np.arange(nq), np.diff(offsets).astype(np.int64))
-    dists = np.array([bin(int(x)).count("1") for x in []], np.int64)  # distances recomputed below
     full = rows[b:e][ids] if ids.size else np.zeros((0, rows.shape[1]), np.uint64)
     qrows = q[qcol] if ids.size else np.zeros((0, rows.shape[1]), np.uint64)
     dists = np.unpackbits((full ^ qrows).view(np.uint8), axis=1).sum(1) if ids.size else np.zeros(0, np.int64)

@@ -149,7 +149,10 @@ def test_cfg4_full_size_cluster_8_shards(oracle):
     reference indexes of the same shards (the reference's full index needs
     ~163 GB of host RAM): per query the shards' counters summed and their ids
     (plus the shard offsets) concatenated in shard order equal the cluster's
-    (SURVEY.md §8c), and the triples equal the exhaustive scan of all 10M."""
+    (SURVEY.md §8c), and the triples equal the exhaustive scan of all 10M.
+    The same batch through one index of all 10M points on this GPU (the
+    bench's N = 1 layout: CSR, the CTA kernel's flattened probe phase) must
+    give the same outputs."""
     cfg = CONFIGS[4]
     data = make_data(cfg, 16)
     q = make_queries(cfg, data, 16)
@@ -158,6 +161,11 @@ def test_cfg4_full_size_cluster_8_shards(oracle):
     cl = F.Cluster([0], cfg.shards).build(data, cfg.radius, plan, cfg.index_seed(), prime=M31)
     res = cl.query_r_nn(q, cfg.radius)
     del cl
+    torch.cuda.empty_cache()
+    ix = F.build_index(data, cfg.radius, plan, cfg.index_seed(), prime=M31)
+    one = ix.query_r_nn(q, cfg.radius)
+    layout = ix.layout
+    del ix
     torch.cuda.empty_cache()
     counters = np.zeros((nq, 3), np.uint64)
     per_query = [[] for _ in range(nq)]
@@ -174,4 +182,5 @@ def test_cfg4_full_size_cluster_8_shards(oracle):
     offsets = np.concatenate([[0], np.cumsum(counters[:, 2])]).astype(np.uint64)
     truth = _gpu_scan_triples(data, q, cfg.dims, cfg.radius)
     _assert_equal(res, counters, offsets, ids, truth, "cfg4 x8")
+    _assert_equal(one, counters, offsets, ids, truth, f"cfg4 one index ({layout})")
     assert res.found.sum() > 100_000  # dense neighbourhoods
