@@ -2330,6 +2330,27 @@ void wait_published(const unsigned long long* h_pub, unsigned long long seq, cud
     std::atomic_thread_fence(std::memory_order_acquire);
 }
 
+// A batch's host destination (HostDest: counters, query, id, distance
+// pointers and the block's capacity; zeros = device outputs only), passed by
+// value to the prologue kernel.
+struct DescVals {
+    unsigned long long v[5];
+};
+
+// Batch prologue, one small CTA on the side branch beside the hash: clears
+// the batch's counters (overflow counts, result cursor, hand-out counters,
+// per-tile result sums) and writes the host destination to device memory for
+// the query and compaction kernels. The destination arrives as a kernel
+// argument that query_enqueue_impl patches into the replayed graph's node
+// (cudaGraphExecKernelNodeSetParams), so one captured graph serves any
+// destination without a host-to-device copy node on the critical path
+// (a 40-byte memcpy node there cost ~3 us per batch; profiles/r02).
+__global__ void k_batch_prologue(unsigned int* __restrict__ cnts, uint32_t words, unsigned long long* __restrict__ d_desc,
+                                 DescVals dv) {
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) cnts[i] = 0;
+    if (threadIdx.x < 5) d_desc[threadIdx.x] = dv.v[threadIdx.x];
+}
+
 // Every buffer a batch of nq queries touches, sized (grow-only) before any
 // launch so that a captured graph never needs a reallocation. Called again by
 // query_finish_impl: the same sizes return the same pointers.
@@ -2410,7 +2431,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
     // walks serialise inside a warp; profiles/r02/cfg4_dense.md).
     const bool dense_all = big;
     if (!ix.h_pub) {
-        // [0] total, [1] [2] overflow counts, [3] sequence, [4..8] HostDest
+        // [0] total, [1] [2] overflow counts, [3] sequence
         FCLSH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ix.h_pub), 128, cudaHostAllocMapped));
         FCLSH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ix.d_pub), ix.h_pub, 0));
         std::memset(ix.h_pub, 0, 128);
@@ -2440,15 +2461,36 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         }
     };
     const unsigned long long* d_desc = d_seq + 1;
+    // the host destination for this batch (written to d_desc by the prologue,
+    // read by the query kernels and k_scan_compact at run time, so a replayed
+    // graph serves any destination)
+    const bool host_cnt = nq && dest && dest->counters;
+    DescVals dv{};
+    if (host_cnt) {
+        dv.v[0] = reinterpret_cast<uintptr_t>(dest->counters);
+        dv.v[1] = reinterpret_cast<uintptr_t>(dest->q);
+        dv.v[2] = reinterpret_cast<uintptr_t>(dest->id);
+        dv.v[3] = reinterpret_cast<uintptr_t>(dest->dist);
+        dv.v[4] = dest->cap;
+    }
+    cudaGraphNode_t prologue_node = nullptr;
     auto enqueue_common = [&] {
         rec(0);
         // on a side branch beside the hash: clear the batch counters and copy
         // the destination descriptor (read at run time from pinned memory)
         FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
         FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
-        FCLSH_CUDA(cudaMemsetAsync(b.ovf_cnt, 0, 64 + b.ntiles * 8, ix.side));
-        FCLSH_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(d_desc), ix.h_pub + 4, 40, cudaMemcpyHostToDevice,
-                                   ix.side));
+        k_batch_prologue<<<1, 256, 0, ix.side>>>(b.ovf_cnt, uint32_t((64 + b.ntiles * 8) / 4),
+                                                 const_cast<unsigned long long*>(d_desc), dv);
+        FCLSH_LAUNCHED();
+        if (capturing) { // its node, for the per-launch destination patch
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t ndeps = 0;
+            FCLSH_CUDA(cudaStreamGetCaptureInfo(ix.side, &st, nullptr, nullptr, &deps, &ndeps));
+            if (ndeps != 1) throw CudaError("query: prologue node not found in the capture");
+            prologue_node = deps[0];
+        }
         FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
         // the way; with the hash fused into the query kernel it does both
@@ -2492,16 +2534,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
     };
     // the host destination for this batch (read by k_scan_compact at run time,
     // so a replayed graph serves any destination)
-    const bool host_cnt = nq && dest && dest->counters;
-    {
-        volatile unsigned long long* h = ix.h_pub + 4;
-        h[0] = host_cnt ? reinterpret_cast<uintptr_t>(dest->counters) : 0;
-        h[1] = host_cnt ? reinterpret_cast<uintptr_t>(dest->q) : 0;
-        h[2] = host_cnt ? reinterpret_cast<uintptr_t>(dest->id) : 0;
-        h[3] = host_cnt ? reinterpret_cast<uintptr_t>(dest->dist) : 0;
-        h[4] = host_cnt ? dest->cap : 0;
-        std::atomic_thread_fence(std::memory_order_release);
-    }
+
 #ifdef FCLSH_TRACE
     {
         static DevBuf tbuf; // (trace builds: single-threaded tools only)
@@ -2528,7 +2561,22 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
                                               ix.d_pub, d_seq, reinterpret_cast<const void*>(uintptr_t(timing)),
                                               reinterpret_cast<const void*>(uintptr_t(dense_grid)), b.tile_sum,
                                               hash_src};
+        auto patch_prologue = [&] {
+            unsigned int* a0 = b.ovf_cnt;
+            uint32_t a1 = uint32_t((64 + b.ntiles * 8) / 4);
+            unsigned long long* a2 = const_cast<unsigned long long*>(d_desc);
+            void* args[] = {&a0, &a1, &a2, &dv};
+            cudaKernelNodeParams kp = {};
+            kp.func = reinterpret_cast<void*>(k_batch_prologue);
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(256);
+            kp.sharedMemBytes = 0;
+            kp.kernelParams = args;
+            kp.extra = nullptr;
+            FCLSH_CUDA(cudaGraphExecKernelNodeSetParams(ix.gexec, ix.gprologue, &kp));
+        };
         if (ix.gexec && key == ix.gkey) {
+            patch_prologue();
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
         } else if (key == ix.gpending) {
@@ -2551,9 +2599,15 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
                 cudaGraphExecDestroy(ix.gexec);
                 ix.gexec = nullptr;
             }
+            if (ix.gsrc) {
+                cudaGraphDestroy(ix.gsrc);
+                ix.gsrc = nullptr;
+            }
             const cudaError_t ie = cudaGraphInstantiate(&ix.gexec, g, 0);
-            cudaGraphDestroy(g);
+            if (ie != cudaSuccess) cudaGraphDestroy(g);
             FCLSH_CUDA(ie);
+            ix.gsrc = g; // kept: gprologue is one of its nodes
+            ix.gprologue = prologue_node;
             ix.gkey = key;
             FCLSH_CUDA(cudaGraphLaunch(ix.gexec, s));
             launch_counter() += ix.gkernels;
@@ -2733,6 +2787,7 @@ void l2_persist_release(int device) {
 DeviceIndex::~DeviceIndex() {
     if (l2_persist) l2_persist_release(device);
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (gsrc) cudaGraphDestroy(gsrc);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (ev_fork) cudaEventDestroy(ev_fork);

@@ -68,6 +68,8 @@ struct DeviceIndex {
     DevBuf pub_seq_dev, cub_tmp2;
     // the common path as a CUDA graph, keyed by shape + buffers (index.cu)
     cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t gsrc = nullptr;          // the captured graph gexec was instantiated from (owns gprologue)
+    cudaGraphNode_t gprologue = nullptr; // the batch prologue's kernel node (its HostDest patched per launch)
     std::vector<const void*> gkey, gpending;
     uint64_t gkernels = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr; // caller-stream fork / join
