@@ -1918,6 +1918,9 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         hd_s.dist = h ? reinterpret_cast<uint32_t*>(h[3]) : nullptr;
         hd_s.cap = h ? h[4] : 0;
     }
+    // this tile's found counts and result sources, loaded beside the tile sums
+    const unsigned long long f = tid < m ? found_q[q0 + tid] : 0ull;
+    const unsigned long long srcv = tid < m ? src_pos[q0 + tid] : 0ull;
     // prefix of the earlier tiles, and the batch total
     unsigned long long pre = 0, all = 0;
     for (uint32_t i = tid; i < ntiles; i += blockDim.x) {
@@ -1955,8 +1958,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         out_dist = hd.dist;
     }
     // block exclusive scan of this tile's found counts
-    const unsigned long long f = tid < m ? found_q[q0 + tid] : 0ull;
-    if (tid < m) src_s[tid] = src_pos[q0 + tid];
+    if (tid < m) src_s[tid] = srcv;
     unsigned long long x = f;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -2337,7 +2339,8 @@ struct DescVals {
     unsigned long long v[5];
 };
 
-// Batch prologue, one small CTA on the side branch beside the hash: clears
+// Batch prologue, one small CTA (first on the batch's stream, or on a side
+// branch beside a separate hash kernel): clears
 // the batch's counters (overflow counts, result cursor, hand-out counters,
 // per-tile result sums) and writes the host destination to device memory for
 // the query and compaction kernels. The destination arrives as a kernel
@@ -2347,6 +2350,7 @@ struct DescVals {
 // (a 40-byte memcpy node there cost ~3 us per batch; profiles/r02).
 __global__ void k_batch_prologue(unsigned int* __restrict__ cnts, uint32_t words, unsigned long long* __restrict__ d_desc,
                                  DescVals dv) {
+    pdl_trigger(); // (the query kernel's CTAs may launch; they wait for this grid to finish)
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) cnts[i] = 0;
     if (threadIdx.x < 5) d_desc[threadIdx.x] = dv.v[threadIdx.x];
 }
@@ -2476,30 +2480,35 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
     cudaGraphNode_t prologue_node = nullptr;
     auto enqueue_common = [&] {
         rec(0);
-        // on a side branch beside the hash: clear the batch counters and copy
-        // the destination descriptor (read at run time from pinned memory)
-        FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
-        FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
-        k_batch_prologue<<<1, 256, 0, ix.side>>>(b.ovf_cnt, uint32_t((64 + b.ntiles * 8) / 4),
-                                                 const_cast<unsigned long long*>(d_desc), dv);
+        // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
+        // the way; with the hash fused into the query kernel it does both
+        const bool fused_hash = !big && fused_fe(ix) > 0;
+        // the prologue: with the hash fused, first on the batch's stream (the
+        // query kernel follows it by PDL); else on a side branch beside the
+        // hash kernel, joined before the query kernel
+        cudaStream_t ps = fused_hash ? s : ix.side;
+        if (!fused_hash) {
+            FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
+            FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
+        }
+        launch_pdl(k_batch_prologue, 1, 256, 0, ps, b.ovf_cnt, uint32_t((64 + b.ntiles * 8) / 4),
+                   const_cast<unsigned long long*>(d_desc), dv);
         FCLSH_LAUNCHED();
         if (capturing) { // its node, for the per-launch destination patch
             cudaStreamCaptureStatus st;
             const cudaGraphNode_t* deps = nullptr;
             size_t ndeps = 0;
-            FCLSH_CUDA(cudaStreamGetCaptureInfo(ix.side, &st, nullptr, nullptr, &deps, &ndeps));
+            FCLSH_CUDA(cudaStreamGetCaptureInfo(ps, &st, nullptr, nullptr, &deps, &ndeps));
             if (ndeps != 1) throw CudaError("query: prologue node not found in the capture");
             prologue_node = deps[0];
         }
-        FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
-        // hash_src (mapped pinned host rows): hashed from there, copied to d_q on
-        // the way; with the hash fused into the query kernel it does both
-        const bool fused_hash = !big && fused_fe(ix) > 0;
-        if (!fused_hash)
+        if (!fused_hash) {
+            FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
             hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
                       hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
+        }
         rec(1);
-        FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
+        if (!fused_hash) FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
                                                b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
