@@ -1465,6 +1465,7 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
                 const uint32_t t = tb0 + k;
                 len[k] = 0;
                 if (t < tables) {
+                    FCLSH_DCHECK(home_of(key[k], tb) < tb.cells);
                     const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[k], tb);
                     const uint32_t a = __ldg(d), e = __ldg(d + 1);
                     f_start[t] = a;
@@ -1499,6 +1500,8 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
                                 hi = mid;
                         }
                         tt[u] = lo;
+                        FCLSH_DCHECK(lo < tables && f_off[lo] <= j && j < f_off[lo + 1] &&
+                                     f_start[lo] + (j - f_off[lo]) < tb.n);
                         e[u] = tb.data[uint64_t(lo) * tb.n + f_start[lo] + (j - f_off[lo])];
                     }
                 }
