@@ -945,6 +945,7 @@ struct FusedHash {
     const uint64_t* ent_pk = nullptr; // [parts][max_dims] seed << 32 | source bit
     uint64_t prime = 0;
     const uint64_t* hash_src = nullptr; // mapped pinned host rows (null: the device rows)
+    uint32_t smem_bytes = 0; // > 0: the kernel stages col_ptr and ent_pk in shared memory (this many bytes)
 };
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
@@ -958,9 +959,22 @@ __device__ __forceinline__ uint64_t ld_cg(const uint64_t* p) {
     return v;
 }
 
-template <int FE, typename K>
-__device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint32_t words, const uint64_t* qrows,
-                                           K* keys, int lane, uint64_t& rw) {
+// family entries from shared memory (staged per CTA) or through the read-only path
+template <bool SMEM>
+__device__ __forceinline__ uint32_t fam_ld(const uint32_t* p) {
+    if constexpr (SMEM) return *p;
+    else return __ldg(p);
+}
+template <bool SMEM>
+__device__ __forceinline__ uint64_t fam_ld(const uint64_t* p) {
+    if constexpr (SMEM) return *p;
+    else return __ldg(p);
+}
+
+template <int FE, bool SMEM, typename K>
+__device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
+                                           uint64_t q, uint32_t words, const uint64_t* qrows, K* keys, int lane,
+                                           uint64_t& rw) {
     constexpr unsigned kAll = 0xffffffffu;
     const uint64_t* src = (fh.hash_src ? fh.hash_src : qrows) + q * words;
     if (uint32_t(lane) < words) {
@@ -969,8 +983,8 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
     }
     const uint64_t P = fh.prime;
     for (uint32_t p = 0; p < fh.parts; ++p) {
-        const uint32_t* cp = fh.col_ptr + uint64_t(p) * (fh.N + 1);
-        const uint64_t* pk = fh.ent_pk + uint64_t(p) * fh.max_dims;
+        const uint32_t* cp = cp_all + uint64_t(p) * (fh.N + 1);
+        const uint64_t* pk = pk_all + uint64_t(p) * fh.max_dims;
         // the sketch of the lane's FE columns: every column's (seed, bit)
         // entries are loaded kBatch at a time for all FE columns at once (no
         // load waits on another: two L2 round trips per batch of kBatch * FE
@@ -981,8 +995,8 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
 #pragma unroll
         for (int i = 0; i < FE; ++i) {
             const uint32_t c = uint32_t(lane) + 32u * i;
-            b0[i] = __ldg(cp + c);
-            cnt[i] = __ldg(cp + c + 1) - b0[i];
+            b0[i] = fam_ld<SMEM>(cp + c);
+            cnt[i] = fam_ld<SMEM>(cp + c + 1) - b0[i];
             mx = max(mx, cnt[i]);
             t[i] = 0;
         }
@@ -992,7 +1006,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
 #pragma unroll
             for (int i = 0; i < FE; ++i)
 #pragma unroll
-                for (int k = 0; k < kBatch; ++k) e[i][k] = k0 + k < cnt[i] ? __ldg(pk + b0[i] + k0 + k) : 0ull;
+                for (int k = 0; k < kBatch; ++k) e[i][k] = k0 + k < cnt[i] ? fam_ld<SMEM>(pk + b0[i] + k0 + k) : 0ull;
 #pragma unroll
             for (int i = 0; i < FE; ++i)
 #pragma unroll
@@ -1039,7 +1053,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, uint64_t q, uint
     }
 }
 
-template <typename T, int U, int MINB, int FE>
+template <typename T, int U, int MINB, int FE, bool FSM = false>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -1058,6 +1072,23 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
+    // FE > 0 with fh.smem_bytes: the family's column lists (read by every
+    // query's hash) staged once per CTA, so a query's hash waits on no global
+    // load but its row's
+    extern __shared__ __align__(16) unsigned char fam_smem[];
+    const uint32_t* cp_all = fh.col_ptr;
+    const uint64_t* pk_all = fh.ent_pk;
+    if constexpr (FE > 0 && FSM) {
+        uint64_t* pk_s = reinterpret_cast<uint64_t*>(fam_smem);
+        const uint32_t npk = fh.parts * uint32_t(fh.max_dims);
+        uint32_t* cp_s = reinterpret_cast<uint32_t*>(pk_s + npk);
+        const uint32_t ncp = fh.parts * (fh.N + 1);
+        for (uint32_t i = threadIdx.x; i < npk; i += blockDim.x) pk_s[i] = __ldg(fh.ent_pk + i);
+        for (uint32_t i = threadIdx.x; i < ncp; i += blockDim.x) cp_s[i] = __ldg(fh.col_ptr + i);
+        __syncthreads();
+        cp_all = cp_s;
+        pk_all = pk_s;
+    }
     pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
     // the grid's warps take queries 0 .. warps-1 directly (no atomic storm on
     // one counter as every warp starts), later ones from the counter
@@ -1087,7 +1118,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         FCLSH_TRACE_STAMP(q, 5, smid);
 #endif
         if constexpr (FE > 0) {
-            fused_hash<FE>(fh, q, words, qrows, qkeys + q * tables, lane, rw);
+            fused_hash<FE, FSM>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
 #ifdef FCLSH_TRACE
@@ -2200,6 +2231,10 @@ FusedHash fused_params(const DeviceIndex& ix, const uint64_t* hash_src) {
     f.ent_seed = fs.ent_seed.as<uint64_t>();
     f.prime = fs.prime;
     f.hash_src = hash_src;
+    // staged in shared memory when small (cfg3: 5.1 KB per CTA; A/B: FCLSH_FAMILY_GLOBAL=1)
+    static const bool global_only = getenv("FCLSH_FAMILY_GLOBAL") != nullptr;
+    const uint64_t sb = uint64_t(f.parts) * (f.max_dims * 8 + (f.N + 1) * 4);
+    f.smem_bytes = !global_only && sb <= 12 * 1024 ? uint32_t((sb + 15) & ~uint64_t(15)) : 0;
     return f;
 }
 
@@ -2215,21 +2250,29 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
     static const bool v1 = getenv("FCLSH_WARP_V1") != nullptr; // A/B: the unpipelined warp kernel
     if (!shared_set && !v1 && LAYOUT == kLayoutBuckets) {
         const int vec = vec_for(ix.row_words, d_q);
-        auto go = [&](auto kern) {
+        auto go = [&](auto kern, bool use_smem = false) {
+            FusedHash fh = fused_params(ix, hash_src);
+            if (!use_smem) fh.smem_bytes = 0;
+            // carveout: none (all of the unified array as L1 for the probes in
+            // flight), or just enough shared memory for MINB CTAs' staged family
             static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
+            static std::atomic<int> carve_pct{-1};
+            const int want = fh.smem_bytes ? int((uint64_t(fh.smem_bytes + 1024) * 6 * 100 + 228 * 1024 - 1) / (228 * 1024))
+                                           : 0;
             const uint64_t bit = uint64_t(1) << (ix.device & 63);
-            if (!(carved.load(std::memory_order_acquire) & bit)) {
-                FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            if (!(carved.load(std::memory_order_acquire) & bit) || carve_pct.load() != want) {
+                FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(want, 100)));
+                carve_pct.store(want);
                 carved.fetch_or(bit, std::memory_order_acq_rel);
             }
-            int per_sm = resident_ctas(kern, 256, 0, ix.device);
+            int per_sm = resident_ctas(kern, 256, fh.smem_bytes, ix.device);
             static const int cap = getenv("FCLSH_WARP_CTAS") ? atoi(getenv("FCLSH_WARP_CTAS")) : 0; // A/B
             if (cap > 0) per_sm = std::min(per_sm, cap);
             const uint64_t grid = std::max<uint64_t>(
                 1, std::min<uint64_t>((nq + 7) / 8, uint64_t(std::max(per_sm, 1)) * sm_count(ix.device)));
-            launch_pdl(kern, unsigned(grid), 256, 0, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
+            launch_pdl(kern, unsigned(grid), 256, fh.smem_bytes, s, qkeys, nq, uint32_t(ix.tables), view<T>(ix),
                        ix.rows.as<uint64_t>(), d_q, ix.row_words, radius, slot_cap, coll_q, cand_q, found_q, src_pos,
-                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec, fused_params(ix, hash_src));
+                       tmp_id, tmp_dist, ovf, ovf_cnt, qnext, tile_sum, desc, vec, fh);
             FCLSH_LAUNCHED();
         };
         // probes per lane in flight per round: 3 for indexes of <= 400
@@ -2237,16 +2280,17 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
         static const int wu_env = getenv("FCLSH_WARP_U") ? atoi(getenv("FCLSH_WARP_U")) : 0;
         const int wu = wu_env ? wu_env : (ix.tables <= 400 ? 3 : 2);
         const int fe = fused_fe(ix);
+        const bool fsm = fe > 0 && fused_params(ix, hash_src).smem_bytes > 0;
         if (fe == 1)
-            go(k_query_warp_pf<T, 3, 4, 1>);
+            fsm ? go(k_query_warp_pf<T, 3, 4, 1, true>, true) : go(k_query_warp_pf<T, 3, 4, 1>);
         else if (fe == 2)
-            go(k_query_warp_pf<T, 3, 4, 2>);
+            fsm ? go(k_query_warp_pf<T, 3, 4, 2, true>, true) : go(k_query_warp_pf<T, 3, 4, 2>);
         else if (fe == 4 && wu_env == 3)
             go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
-            go(k_query_warp_pf<T, 2, 5, 4>);
+            fsm ? go(k_query_warp_pf<T, 2, 5, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 8)
-            go(k_query_warp_pf<T, 2, 4, 8>);
+            fsm ? go(k_query_warp_pf<T, 2, 4, 8, true>, true) : go(k_query_warp_pf<T, 2, 4, 8>);
         else if (wu == 4)
             go(k_query_warp_pf<T, 4, 3, 0>);
         else if (wu == 3)
