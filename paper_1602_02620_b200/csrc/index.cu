@@ -538,7 +538,6 @@ __global__ void __launch_bounds__(256) k_query_fused(
     const unsigned long long* __restrict__ desc) {
     using E = typename T::E;
     // host destination of the counters (HostDest, null: device only), written as each query completes
-    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     static_assert((WS & (WS - 1)) == 0 && WS >= 128 && WS % 32 == 0, "set size");
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     constexpr uint32_t kMaxD = WS / 4 * 3; // distinct ids a query may have here (set load <= 3/4 + 32)
@@ -550,6 +549,9 @@ __global__ void __launch_bounds__(256) k_query_fused(
     for (int k = lane; k < WS; k += 32) set[k] = kEmpty; // afterwards cleared as it is read
     pdl_trigger();
     pdl_wait(); // the batch's keys (hash kernel) are complete from here on
+    // the host destination (written by the batch prologue, a PDL predecessor:
+    // read only after the wait)
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     // queries are handed out one at a time (a warp that finishes early takes
     // the next), so the last wave does not leave most warps idle
     auto fetch = [&]() -> uint64_t {
@@ -726,12 +728,14 @@ __global__ void __launch_bounds__(256, FCLSH_WARP_MINB) k_query_warp(
     using E = typename T::E;
     constexpr unsigned kAll = 0xffffffffu;
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     const int lane = threadIdx.x & 31;
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
     pdl_wait(); // the batch's keys (hash kernel) are complete from here on
+    // the host destination (written by the batch prologue, a PDL predecessor:
+    // read only after the wait)
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     auto fetch = [&]() -> uint64_t {
         unsigned int v = 0;
         if (lane == 0) v = atomicAdd(qnext, 1u);
@@ -1067,7 +1071,6 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     constexpr unsigned kAll = 0xffffffffu;
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     constexpr uint32_t kStep = 32 * U; // tables per round
-    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     const int lane = threadIdx.x & 31;
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
@@ -1090,6 +1093,9 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         pk_all = pk_s;
     }
     pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
+    // the host destination (written by the batch prologue, a PDL predecessor:
+    // read only after the wait)
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     // the grid's warps take queries 0 .. warps-1 directly (no atomic storm on
     // one counter as every warp starts), later ones from the counter
     const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
@@ -1356,7 +1362,6 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
     uint32_t slot_cap, uint32_t* __restrict__ slot_id, uint32_t* __restrict__ slot_dist, int vec_rows) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(smem); // FCAP found entries
-    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     uint32_t* set = reinterpret_cast<uint32_t*>(fl + FCAP);                // HS ids
     constexpr uint32_t kMaxDistinct = HS / 4 * 3;
     uint16_t* clist = reinterpret_cast<uint16_t*>(set + HS); // set slot of each distinct candidate
@@ -1369,6 +1374,9 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     pdl_trigger();
     pdl_wait(); // the warp kernel's hand-over list is complete from here on
+    // the host destination (written by the batch prologue, a PDL predecessor:
+    // read only after the wait)
+    unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
     if (blockIdx.x >= ns) return; // at most ns CTAs can get a query (usually ns == 0: nothing handed over)
     __shared__ unsigned int next_s;
@@ -2398,6 +2406,7 @@ struct DescVals {
 __global__ void k_batch_prologue(unsigned int* __restrict__ cnts, uint32_t words, unsigned long long* __restrict__ d_desc,
                                  DescVals dv) {
     pdl_trigger(); // (the query kernel's CTAs may launch; they wait for this grid to finish)
+    pdl_wait();    // (and this one for whatever preceded it on the stream: the previous batch's kernels)
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) cnts[i] = 0;
     if (threadIdx.x < 5) d_desc[threadIdx.x] = dv.v[threadIdx.x];
 }
@@ -2533,8 +2542,9 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         // the prologue: with the hash fused, first on the batch's stream (the
         // query kernel follows it by PDL); else on a side branch beside the
         // hash kernel, joined before the query kernel
-        cudaStream_t ps = fused_hash ? s : ix.side;
-        if (!fused_hash) {
+        const bool on_s = fused_hash;
+        cudaStream_t ps = on_s ? s : ix.side;
+        if (!on_s) {
             FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
             FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
         }
@@ -2549,13 +2559,13 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
             if (ndeps != 1) throw CudaError("query: prologue node not found in the capture");
             prologue_node = deps[0];
         }
+        if (!on_s) FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
         if (!fused_hash) {
-            FCLSH_CUDA(cudaEventRecord(ix.ev_join, ix.side));
             hash_rows(*ix.fs, hash_src ? hash_src : d_q, nq, qkeys, sizeof(K), T_, kLayoutPointMajor, s, 0, 0,
                       hash_src ? const_cast<uint64_t*>(d_q) : nullptr);
         }
         rec(1);
-        if (!fused_hash) FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
+        if (!on_s) FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
                                                b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,

@@ -187,6 +187,33 @@ def test_repeated_device_queries_replay_graph(oracle):
             assert set(ix.stage_ms()) == set(F.IndexSet.STAGES)
 
 
+def test_host_and_device_destinations_interleaved(oracle):
+    """Batches with a host result block (fclsh_query) and device-only batches
+    alternate, each shape run eagerly, captured and replayed, with the host
+    blocks freed in between: the batch prologue rewrites the destination every
+    batch and no kernel may act on a previous batch's (freed) block."""
+    import torch
+    rng = np.random.default_rng(15)
+    rows = random_rows(rng, 5000, 128)
+    plan = F.make_plan(128, 4, 1.0, 5000, 1, F.PlanOverride(F.PlanKind.identity, 1))
+    ix = F.build_index(rows, 4, plan, 2, prime=M31)
+    oi = oracle.index_build(rows, 128, 4, 1, 2, override=(0, 1), prime=M31, threads=4)
+    for nq in (200, 333, 200, 1000, 333):
+        q = planted_queries(rng, rows, 128, nq, 5)
+        counters, offsets, ids = oi.query(q, 4, threads=4)
+        qd = torch.from_numpy(q.view(np.int64)).cuda()
+        for k in range(4):
+            if k % 2 == 0:
+                res = ix.query_r_nn(q, 4)  # host result block, freed when res is dropped
+                assert (res.offsets == offsets).all() and (res.id == ids).all(), (nq, k)
+                del res
+            else:
+                tri, off, cnt = _device_triples(ix.query_device(qd, 4))
+                assert (off == offsets.astype(np.int64)).all(), (nq, k)
+                assert (tri[1] == ids.astype(np.int32)).all(), (nq, k)
+                assert (cnt.T == counters.astype(np.int64)).all(), (nq, k)
+
+
 def test_directory_extremes(oracle):
     """A 2-cell directory (long scans) and a fine one give the same answers."""
     rng = np.random.default_rng(9)
