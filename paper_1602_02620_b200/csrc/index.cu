@@ -993,7 +993,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* 
         // entries are loaded kBatch at a time for all FE columns at once (no
         // load waits on another: two L2 round trips per batch of kBatch * FE
         // entries instead of one per entry); a missing entry loads as 0 = seed 0
-        constexpr int kBatch = 4;
+        constexpr int kBatch = SMEM ? 2 : 4; // (shared memory: short latency, fewer registers)
         uint32_t b0[FE], cnt[FE], mx = 0;
         long long t[FE];
 #pragma unroll
@@ -2220,7 +2220,8 @@ int fused_fe(const DeviceIndex& ix) {
     if (off || ix.layout != kLayoutBuckets || ix.wide || fs.classic || ix.prime > 0xFFFFFFFFull) return 0;
     // (N = 512, FE = 16 -- cfg2 -- measured slower fused: 0.139 -> 0.186 ms per
     // batch, the 16-deep register transform spills and delays every query's
-    // probes; the separate hash kernel runs there)
+    // probes; again with the family in shared memory, 4 CTAs/SM: 0.167 ->
+    // 0.184 ms per 11k batch; the separate hash kernel runs there)
     if (ix.tables > 600 || ix.row_words > 32 || fs.order < 32 || fs.order > 256) return 0;
     return int(fs.order / 32);
 }
