@@ -993,7 +993,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* 
         // entries are loaded kBatch at a time for all FE columns at once (no
         // load waits on another: two L2 round trips per batch of kBatch * FE
         // entries instead of one per entry); a missing entry loads as 0 = seed 0
-        constexpr int kBatch = SMEM ? 2 : 4; // (shared memory: short latency, fewer registers)
+        constexpr int kBatch = 4;
         uint32_t b0[FE], cnt[FE], mx = 0;
         long long t[FE];
 #pragma unroll
