@@ -1944,28 +1944,27 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     const unsigned long long* __restrict__ desc) {
     constexpr uint32_t TQ = 1u << kScanTileLog;
     __shared__ unsigned long long off_s[TQ + 1], src_s[TQ], wsum[32];
-    __shared__ unsigned long long prefix_s, grand_s;
-    __shared__ HostDest hd_s;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t t = blockIdx.x / kScanSplit, part = blockIdx.x % kScanSplit; // kScanSplit CTAs per tile
     const uint64_t q0 = uint64_t(t) * TQ;
     const uint32_t m = uint32_t(nq - q0 < TQ ? nq - q0 : TQ);
     const uint32_t ntiles = gridDim.x / kScanSplit;
     pdl_wait(); // the query kernels' outputs are complete from here on
-    if (tid == 0) { // the host destination (null counters: device buffers only)
-        const unsigned long long* h = desc;
-        hd_s.counters = h ? reinterpret_cast<unsigned long long*>(h[0]) : nullptr;
-        hd_s.q = h ? reinterpret_cast<uint32_t*>(h[1]) : nullptr;
-        hd_s.id = h ? reinterpret_cast<uint32_t*>(h[2]) : nullptr;
-        hd_s.dist = h ? reinterpret_cast<uint32_t*>(h[3]) : nullptr;
-        hd_s.cap = h ? h[4] : 0;
-    }
+    // the host destination (null counters: device buffers only), read by
+    // every thread (one L1 line, no barrier)
+    HostDest hd;
+    hd.counters = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
+    hd.q = desc ? reinterpret_cast<uint32_t*>(desc[1]) : nullptr;
+    hd.id = desc ? reinterpret_cast<uint32_t*>(desc[2]) : nullptr;
+    hd.dist = desc ? reinterpret_cast<uint32_t*>(desc[3]) : nullptr;
+    hd.cap = desc ? desc[4] : 0;
     // this tile's found counts and result sources, loaded beside the tile sums
     const unsigned long long f = tid < m ? found_q[q0 + tid] : 0ull;
     const unsigned long long srcv = tid < m ? src_pos[q0 + tid] : 0ull;
-    // prefix of the earlier tiles, and the batch total
+    // prefix of the earlier tiles and the batch total, summed by every warp
+    // over all the tile sums (no barrier; <= 32 loads per lane up to 32k tiles)
     unsigned long long pre = 0, all = 0;
-    for (uint32_t i = tid; i < ntiles; i += blockDim.x) {
+    for (uint32_t i = lane; i < ntiles; i += 32) {
         const unsigned long long v = tile_sum[i];
         all += v;
         if (i < t) pre += v;
@@ -1975,25 +1974,9 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         pre += __shfl_xor_sync(0xffffffffu, pre, o);
         all += __shfl_xor_sync(0xffffffffu, all, o);
     }
-    if (lane == 0) {
-        wsum[wid] = pre;
-        off_s[wid] = all; // (scratch: off_s is filled below)
-    }
-    __syncthreads();
-    if (tid == 0) {
-        unsigned long long p = 0, a = 0;
-        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
-            p += wsum[w];
-            a += off_s[w];
-        }
-        prefix_s = p;
-        grand_s = a;
-    }
-    __syncthreads();
-    const unsigned long long prefix = prefix_s;
-    const HostDest hd = hd_s;
+    const unsigned long long prefix = pre;
     const bool host_cnt = hd.counters != nullptr;
-    const bool host_res = host_cnt && grand_s <= hd.cap;
+    const bool host_res = host_cnt && all <= hd.cap;
     if (host_res) { // results into the host block
         out_q = hd.q;
         out_id = hd.id;
@@ -2081,7 +2064,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
             __threadfence_system();
             const unsigned long long seq = *dseq + 1;
             *dseq = seq;
-            pub[0] = grand_s;
+            pub[0] = all;
             pub[1] = reinterpret_cast<volatile unsigned int*>(cnts)[0];
             pub[2] = reinterpret_cast<volatile unsigned int*>(cnts)[1];
             __threadfence_system();
