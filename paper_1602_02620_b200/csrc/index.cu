@@ -2278,7 +2278,7 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
         else if (fe == 2)
             fsm ? go(k_query_warp_pf<T, 3, 4, 2, true>, true) : go(k_query_warp_pf<T, 3, 4, 2>);
         else if (fe == 4 && wu_env == 3)
-            go(k_query_warp_pf<T, 3, 4, 4>);
+            fsm ? go(k_query_warp_pf<T, 3, 4, 4, true>, true) : go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
             fsm ? go(k_query_warp_pf<T, 2, 5, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 8)
