@@ -87,6 +87,13 @@ constexpr int kSlots = 4; // per bucket
 constexpr uint32_t kBuildSlab = 64; // tables per table-major slab of the bucket build
 constexpr int kScanTileLog = 10; // queries per tile of the found scan (k_scan_compact): 1024
 constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
+// The warp kernel hands out the queries past its first wave from kQCtr
+// counters kQCtrStride words (256 B) apart -- CTA b draws from counter
+// b % kQCtr -- instead of one: ~10k returning atomics on one address
+// serialise in its L2 slice (18.7 % of the kernel's stall samples on cfg3,
+// profiles/r02/ncu_k_query_warp_pf_atomic_cfg3.txt)
+constexpr uint32_t kQCtr = 16, kQCtrStride = 64;
+constexpr uint64_t kCntHeader = 64 + uint64_t(kQCtr) * kQCtrStride * 4; // bytes before the tile sums
 #ifndef FCLSH_FUSED_CAP
 #define FCLSH_FUSED_CAP 256
 #endif
@@ -186,6 +193,38 @@ struct Tables {
 // DRAM read of the home bucket is skipped (cfg2: ~80 % of probes miss, and a
 // clear bit rejects ~37 % of them). No false negatives: every inserted
 // posting sets its bit.
+// Publishing a batch to mapped host memory: release / acquire at system
+// scope (MEMBAR.ALL.SYS) instead of __threadfence_system()'s sequentially
+// consistent fence (MEMBAR.SC.SYS + an L1 invalidate). FCLSH_PUB_SC=1
+// restores the SC fences (A/B).
+#ifndef FCLSH_PUB_SC
+#define FCLSH_PUB_SC 0
+#endif
+// the flag store: every earlier write of this thread (and, cumulatively,
+// those ordered before them by a CTA barrier) is visible to the host first
+__device__ __forceinline__ void pub_flag(unsigned long long* flag, unsigned long long seq) {
+#if FCLSH_PUB_SC
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(flag) = seq;
+#else
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+#endif
+}
+// a CTA's arrival after its writes (acq_rel: the last arriver sees every
+// other CTA's writes before it publishes)
+__device__ __forceinline__ unsigned int pub_arrive(unsigned int* ctr) {
+#if FCLSH_PUB_SC
+    __threadfence_system();
+    const unsigned int d = atomicAdd(ctr, 1u);
+    __threadfence_system();
+    return d;
+#else
+    unsigned int d;
+    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(d) : "l"(ctr) : "memory");
+    return d;
+#endif
+}
+
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -934,10 +973,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do { \
         if (g_trace && lane == 0) g_trace[(q) * 16 + (k)] = (v); \
     } while (0)
+// batch timeline (globaltimer, ns): the first / last stamp of each event over
+// the batch's CTAs (warps for kTlWarpExit); reset per batch by the host and
+// appended to $FCLSH_TL_OUT (tools/trace_query.py)
+enum : int {
+    kTlProEntry, kTlProExit, kTlWarpEntry, kTlWarpEntryLast, kTlWarpWait, kTlWarpExit, kTlDenseEntry, kTlDenseWait,
+    kTlDenseExit, kTlCompEntry, kTlCompWait, kTlCompExit, kTlPublish, kTlCompLoaded, kTlCompScanned, kTlSlots
+};
+__device__ unsigned long long g_tl[16];
+#define FCLSH_TL_MIN(k) \
+    do { \
+        if (threadIdx.x == 0) atomicMin(&g_tl[k], gtimer()); \
+    } while (0)
+#define FCLSH_TL_MAX(k) \
+    do { \
+        if (threadIdx.x == 0) atomicMax(&g_tl[k], gtimer()); \
+    } while (0)
+#define FCLSH_TL_MAXW(k) \
+    do { \
+        if ((threadIdx.x & 31) == 0) atomicMax(&g_tl[k], gtimer()); \
+    } while (0)
 #else
 #define FCLSH_TRACE_STAMP(q, k, v) \
     do { \
     } while (0)
+#define FCLSH_TL_MIN(k) \
+    do { \
+    } while (0)
+#define FCLSH_TL_MAX(k) FCLSH_TL_MIN(k)
+#define FCLSH_TL_MAXW(k) FCLSH_TL_MIN(k)
 #endif
 
 struct FusedHash {
@@ -1075,6 +1139,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     const uint64_t fpol = l2_evict_last_policy();
     const uint64_t bpol = l2_evict_first_policy();
     pdl_trigger();
+    FCLSH_TL_MIN(kTlWarpEntry);
+    FCLSH_TL_MAX(kTlWarpEntryLast);
     // FE > 0 with fh.smem_bytes: the family's column lists (read by every
     // query's hash) staged once per CTA, so a query's hash waits on no global
     // load but its row's
@@ -1093,26 +1159,29 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         pk_all = pk_s;
     }
     pdl_wait(); // the batch's keys (hash kernel; FE > 0: this kernel) are complete from here on
+    FCLSH_TL_MIN(kTlWarpWait);
     // the host destination (written by the batch prologue, a PDL predecessor:
     // read only after the wait)
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
-    // the grid's warps take queries 0 .. warps-1 directly (no atomic storm on
-    // one counter as every warp starts), later ones from the counter
+    // the grid's warps take queries 0 .. warps-1 directly (no atomic storm as
+    // every warp starts); later ones come from counter c = CTA % C, which
+    // hands out nwarp + c, nwarp + c + C, ... The next query is claimed once
+    // the current one's probes are done (the atomic's round trip overlaps its
+    // verify and outputs) and read at the top of the loop.
     const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
-    bool first = true;
-    auto fetch = [&]() -> uint64_t {
-        if (first) {
-            first = false;
-            return gwarp;
-        }
-        unsigned int v = 0;
-        if (lane == 0) v = nwarp + atomicAdd(qnext, 1u);
-        return __shfl_sync(kAll, v, 0);
+    const uint32_t nctr = gridDim.x < kQCtr ? gridDim.x : kQCtr, cj = blockIdx.x % nctr;
+    unsigned int* const my_ctr = qnext + cj * kQCtrStride;
+    unsigned int claimed = 0; // lane 0: the claimed counter value
+    auto claim = [&] {
+        if (lane == 0) claimed = atomicAdd(my_ctr, 1u);
+    };
+    auto next_q = [&]() -> uint64_t {
+        return nwarp + cj + uint64_t(nctr) * __shfl_sync(kAll, claimed, 0);
     };
 #ifdef FCLSH_TRACE
     const unsigned long long t_entry = gtimer();
 #endif
-    for (uint64_t q = fetch(); q < nq; q = fetch()) {
+    for (uint64_t q = gwarp; q < nq; q = next_q()) {
         const K* qk = qkeys + q * tables;
         uint64_t rw = 0; // FE > 0: word `lane` of the query row
 #ifdef FCLSH_TRACE
@@ -1242,6 +1311,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
 #endif
         }
         const uint64_t m = __reduce_add_sync(kAll, coll);
+        claim(); // the warp's next query (read at the top of the loop)
 #ifdef FCLSH_TRACE
         FCLSH_TRACE_STAMP(q, 3, clock64() - c0);
 #endif
@@ -1302,6 +1372,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         FCLSH_TRACE_STAMP(q, 7, nd);
 #endif
     }
+    FCLSH_TL_MAXW(kTlWarpExit);
 }
 
 // Exclusive prefix sum of v over the CTA's threads (blockDim.x a multiple of
@@ -1373,7 +1444,10 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
     constexpr uint32_t kEmpty = 0xFFFFFFFFu;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     pdl_trigger();
+    FCLSH_TL_MIN(kTlDenseEntry);
     pdl_wait(); // the warp kernel's hand-over list is complete from here on
+    FCLSH_TL_MIN(kTlDenseWait);
+    FCLSH_TL_MAX(kTlDenseExit);
     // the host destination (written by the batch prologue, a PDL predecessor:
     // read only after the wait)
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
@@ -1893,8 +1967,7 @@ __global__ void k_compact(uint64_t nq, const unsigned long long* __restrict__ sr
         pub[0] = res_off[nq];
         pub[1] = cnts[0];
         pub[2] = cnts[1];
-        __threadfence_system();
-        *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
+        pub_flag(pub + 3, seq);
     }
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t q = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
@@ -1945,11 +2018,39 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     constexpr uint32_t TQ = 1u << kScanTileLog;
     __shared__ unsigned long long off_s[TQ + 1], src_s[TQ], wsum[32];
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t t = blockIdx.x / kScanSplit, part = blockIdx.x % kScanSplit; // kScanSplit CTAs per tile
+    // grid: kScanSplit CTAs per tile of TQ queries, then one publisher CTA
+    const uint32_t nwork = gridDim.x - 1, ntiles = nwork / kScanSplit;
+    const uint32_t t = blockIdx.x / kScanSplit, part = blockIdx.x % kScanSplit;
     const uint64_t q0 = uint64_t(t) * TQ;
-    const uint32_t m = uint32_t(nq - q0 < TQ ? nq - q0 : TQ);
-    const uint32_t ntiles = gridDim.x / kScanSplit;
+    const uint32_t m = blockIdx.x < nwork ? uint32_t(nq - q0 < TQ ? nq - q0 : TQ) : 0u;
+    if (blockIdx.x == nwork && wid) return; // (the publisher needs one warp)
+    FCLSH_TL_MIN(kTlCompEntry);
     pdl_wait(); // the query kernels' outputs are complete from here on
+    FCLSH_TL_MIN(kTlCompWait);
+    if (blockIdx.x == nwork) {
+        // device outputs: publish as soon as the total is known (the sum of
+        // the tile sums), so the host's return overlaps the compaction; the
+        // caller's reads of the outputs follow this kernel in stream order. A
+        // CTA of its own: the system-scope release (~1.3 us) holds up no
+        // barrier of the compaction's CTAs. Host outputs: published below,
+        // once every CTA's writes are visible.
+        if (!pub || (desc && desc[0])) return;
+        const unsigned long long seq = *dseq + 1;
+        const unsigned int c0 = cnts[0], c1 = cnts[1];
+        unsigned long long all = 0;
+        for (uint32_t i = lane; i < ntiles; i += 32) all += tile_sum[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) all += __shfl_xor_sync(0xffffffffu, all, o);
+        if (lane == 0) {
+            *dseq = seq;
+            pub[0] = all;
+            pub[1] = c0;
+            pub[2] = c1;
+            pub_flag(pub + 3, seq);
+            FCLSH_TL_MAX(kTlPublish);
+        }
+        return;
+    }
     // the host destination (null counters: device buffers only), read by
     // every thread (one L1 line, no barrier)
     HostDest hd;
@@ -1975,6 +2076,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         all += __shfl_xor_sync(0xffffffffu, all, o);
     }
     const unsigned long long prefix = pre;
+    FCLSH_TL_MAX(kTlCompLoaded);
     const bool host_cnt = hd.counters != nullptr;
     const bool host_res = host_cnt && all <= hd.cap;
     if (host_res) { // results into the host block
@@ -2007,23 +2109,14 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     const unsigned long long tile_total = wsum[(blockDim.x >> 5) - 1];
     off_s[tid] = excl;
     if (tid == 0) off_s[TQ] = tile_total;
+    FCLSH_TL_MAX(kTlCompScanned);
     if (part == 0 && tid < m) res_off[q0 + tid] = prefix + excl;
     // (the query kernels wrote the other counters to the host as each query completed)
     if (host_cnt && tid < m && tid / (TQ / kScanSplit) == part) hd.counters[q0 + tid] = prefix + excl;
     const bool last = q0 + TQ >= nq;
     if (part == 0 && last && tid == 0) {
         res_off[nq] = prefix + tile_total;
-        if (host_cnt) {
-            hd.counters[nq] = prefix + tile_total;
-        } else if (pub) { // device outputs: the caller's copies follow the kernel in stream order, publish now
-            const unsigned long long seq = *dseq + 1;
-            *dseq = seq;
-            pub[0] = prefix + tile_total;
-            pub[1] = cnts[0];
-            pub[2] = cnts[1];
-            __threadfence_system();
-            *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
-        }
+        if (host_cnt) hd.counters[nq] = prefix + tile_total;
     }
     __syncthreads();
     // one thread per result of this CTA's share of the tile
@@ -2051,6 +2144,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
         out_id[dst] = uint32_t(ti[src + k] + id_offset);
         out_dist[dst] = td[src + k];
     }
+    FCLSH_TL_MAX(kTlCompExit);
     if (!pub || !host_cnt) return;
     // host outputs: publish once every CTA's writes are visible: the
     // barrier orders the CTA's writes before thread 0's system fence
@@ -2058,17 +2152,15 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     // a fence per thread serialises in the memory system, ~0.3 ms per batch)
     __syncthreads();
     if (tid == 0) {
-        __threadfence_system();
-        const unsigned int done = atomicAdd(cnts + 8, 1u);
-        if (done + 1 == gridDim.x) {
-            __threadfence_system();
+        const unsigned int done = pub_arrive(cnts + 8);
+        if (done + 1 == nwork) {
             const unsigned long long seq = *dseq + 1;
             *dseq = seq;
             pub[0] = all;
             pub[1] = reinterpret_cast<volatile unsigned int*>(cnts)[0];
             pub[2] = reinterpret_cast<volatile unsigned int*>(cnts)[1];
-            __threadfence_system();
-            *reinterpret_cast<volatile unsigned long long*>(pub + 3) = seq;
+            pub_flag(pub + 3, seq);
+            FCLSH_TL_MAX(kTlPublish);
         }
     }
 }
@@ -2391,8 +2483,10 @@ __global__ void k_batch_prologue(unsigned int* __restrict__ cnts, uint32_t words
                                  DescVals dv) {
     pdl_trigger(); // (the query kernel's CTAs may launch; they wait for this grid to finish)
     pdl_wait();    // (and this one for whatever preceded it on the stream: the previous batch's kernels)
+    FCLSH_TL_MIN(kTlProEntry);
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) cnts[i] = 0;
     if (threadIdx.x < 5) d_desc[threadIdx.x] = dv.v[threadIdx.x];
+    FCLSH_TL_MAX(kTlProExit);
 }
 
 // Every buffer a batch of nq queries touches, sized (grow-only) before any
@@ -2430,14 +2524,15 @@ QueryBufs<T> query_bufs(DeviceIndex& ix, uint64_t nq, cudaStream_t s) {
     b.ovf = static_cast<uint32_t*>(ix.overflow.ensure(std::max<uint64_t>(1, nq) * 4));
     b.ovf2 = static_cast<uint32_t*>(ix.overflow2.ensure(std::max<uint64_t>(1, nq) * 4));
     // counters: [0] warp-kernel overflow count, [1] CTA-kernel overflow
-    // count, bytes 8..15: the CTA kernel's result cursor, [4] / [5]: next
-    // query to hand out in the warp / CTA kernel, [8]: k_scan_compact CTAs
-    // done; from byte 64 the results per tile of 1024 queries, added by the
-    // query kernels for k_scan_compact. One memset clears all of it.
+    // count, bytes 8..15: the CTA kernel's result cursor, [5]: next
+    // query to hand out in the CTA kernel, [8]: k_scan_compact CTAs done;
+    // from byte 64 the warp kernel's kQCtr query counters (256 B apart), from
+    // byte kCntHeader the results per tile of 1024 queries, added by the
+    // query kernels for k_scan_compact. The batch prologue clears all of it.
     b.ntiles = (nq + (uint64_t(1) << kScanTileLog) - 1) >> kScanTileLog;
-    b.ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(64 + std::max<uint64_t>(1, b.ntiles) * 8));
+    b.ovf_cnt = static_cast<unsigned int*>(ix.overflow_cnt.ensure(kCntHeader + std::max<uint64_t>(1, b.ntiles) * 8));
     b.res_cursor = reinterpret_cast<unsigned long long*>(b.ovf_cnt + 2);
-    b.tile_sum = reinterpret_cast<unsigned long long*>(b.ovf_cnt + 16);
+    b.tile_sum = reinterpret_cast<unsigned long long*>(b.ovf_cnt + kCntHeader / 4);
     // CTA-kernel result region; queries that do not fit go on to the general path
     b.cta_cap = std::max<uint64_t>(uint64_t(1) << 21, nq * kSlotCap);
     b.cta_id = static_cast<uint32_t*>(ix.res_cta_id.ensure(b.cta_cap * 4));
@@ -2532,7 +2627,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
             FCLSH_CUDA(cudaEventRecord(ix.ev_fork, s));
             FCLSH_CUDA(cudaStreamWaitEvent(ix.side, ix.ev_fork, 0));
         }
-        launch_pdl(k_batch_prologue, 1, 256, 0, ps, b.ovf_cnt, uint32_t((64 + b.ntiles * 8) / 4),
+        launch_pdl(k_batch_prologue, 1, 256, 0, ps, b.ovf_cnt, uint32_t((kCntHeader + b.ntiles * 8) / 4),
                    const_cast<unsigned long long*>(d_desc), dv);
         FCLSH_LAUNCHED();
         if (capturing) { // its node, for the per-launch destination patch
@@ -2552,7 +2647,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         if (!on_s) FCLSH_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
         if (!dense_all)
             launch_fused<T, LAYOUT, kFusedCap>(ix, qkeys, d_q, nq, radius, slot_cap, b.coll_q, b.cand_q, b.found_q,
-                                               b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 4,
+                                               b.src_pos, b.tmp_id, b.tmp_dist, b.ovf, b.ovf_cnt, b.ovf_cnt + 16,
                                                b.tile_sum, d_desc, s, fused_hash ? hash_src : nullptr);
         rec(2);
         auto dense = [&](auto shape) {
@@ -2572,7 +2667,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         }
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
-        launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit), 1024, 0, s, nq,
+        launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit + 1), 1024, 0, s, nq,
                    static_cast<const unsigned long long*>(b.found_q), static_cast<const unsigned long long*>(b.tile_sum),
                    b.res_off, static_cast<const unsigned long long*>(b.src_pos),
                    static_cast<const uint32_t*>(b.tmp_id), static_cast<const uint32_t*>(b.tmp_dist), nq * slot_cap,
@@ -2591,6 +2686,8 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         void* tp = tbuf.ensure(std::max<uint64_t>(1, nq) * 128);
         FCLSH_CUDA(cudaMemsetAsync(tp, 0, std::max<uint64_t>(1, nq) * 128, s));
         FCLSH_CUDA(cudaMemcpyToSymbolAsync(g_trace, &tp, sizeof(tp), 0, cudaMemcpyHostToDevice, s));
+        static const unsigned long long tl0[16] = {~0ull, 0, ~0ull, 0, ~0ull, 0, ~0ull, ~0ull, 0, ~0ull, ~0ull, 0, 0, 0, 0};
+        FCLSH_CUDA(cudaMemcpyToSymbolAsync(g_tl, tl0, sizeof(tl0), 0, cudaMemcpyHostToDevice, s));
     }
 #endif
     DeviceIndex::Pending& p = ix.pending;
@@ -2613,7 +2710,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
                                               hash_src};
         auto patch_prologue = [&] {
             unsigned int* a0 = b.ovf_cnt;
-            uint32_t a1 = uint32_t((64 + b.ntiles * 8) / 4);
+            uint32_t a1 = uint32_t((kCntHeader + b.ntiles * 8) / 4);
             unsigned long long* a2 = const_cast<unsigned long long*>(d_desc);
             void* args[] = {&a0, &a1, &a2, &dv};
             cudaKernelNodeParams kp = {};
@@ -2703,6 +2800,17 @@ QueryOutput query_finish_impl(DeviceIndex& ix) {
                 const unsigned long long hdr[2] = {nq, 16};
                 fwrite(hdr, 8, 2, f);
                 fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+        if (const char* path = getenv("FCLSH_TL_OUT")) {
+            unsigned long long tl[16];
+            FCLSH_CUDA(cudaMemcpyFromSymbol(tl, g_tl, sizeof(tl)));
+            if (FILE* f = fopen(path, "a")) {
+                fprintf(f, "nq=%llu", (unsigned long long)nq);
+                for (int k = 0; k < kTlSlots; ++k)
+                    fprintf(f, " %.2f", tl[k] == ~0ull || tl[k] == 0 ? -1.0 : (double(tl[k]) - double(tl[0])) / 1e3);
+                fprintf(f, "\n");
                 fclose(f);
             }
         }
