@@ -1039,89 +1039,116 @@ __device__ __forceinline__ uint64_t fam_ld(const uint64_t* p) {
     else return __ldg(p);
 }
 
+// One part's keys in registers: key[i] = h[v] for v = lane + 32 i (v = 0 is
+// no table), from the row held as word `lane` on lane `lane` (rw).
 template <int FE, bool SMEM, typename K>
-__device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
-                                           uint64_t q, uint32_t words, const uint64_t* qrows, K* keys, int lane,
-                                           uint64_t& rw) {
+__device__ __forceinline__ void hash_part(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
+                                          uint32_t p, uint32_t words, uint64_t rw, int lane, K (&key)[FE]) {
     constexpr unsigned kAll = 0xffffffffu;
+    const uint64_t P = fh.prime;
+    const uint32_t* cp = cp_all + uint64_t(p) * (fh.N + 1);
+    const uint64_t* pk = pk_all + uint64_t(p) * fh.max_dims;
+    // the sketch of the lane's FE columns: every column's (seed, bit)
+    // entries are loaded kBatch at a time for all FE columns at once (no
+    // load waits on another: two L2 round trips per batch of kBatch * FE
+    // entries instead of one per entry); a missing entry loads as 0 = seed 0
+    constexpr int kBatch = 4;
+    uint32_t b0[FE], cnt[FE], mx = 0;
+    long long t[FE];
+#pragma unroll
+    for (int i = 0; i < FE; ++i) {
+        const uint32_t c = uint32_t(lane) + 32u * i;
+        b0[i] = fam_ld<SMEM>(cp + c);
+        cnt[i] = fam_ld<SMEM>(cp + c + 1) - b0[i];
+        mx = max(mx, cnt[i]);
+        t[i] = 0;
+    }
+    const uint32_t m = __reduce_max_sync(kAll, mx); // warp-uniform trip count (the shuffles need every lane)
+    for (uint32_t k0 = 0; k0 < m; k0 += kBatch) {
+        uint64_t e[FE][kBatch];
+#pragma unroll
+        for (int i = 0; i < FE; ++i)
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k) e[i][k] = k0 + k < cnt[i] ? fam_ld<SMEM>(pk + b0[i] + k0 + k) : 0ull;
+#pragma unroll
+        for (int i = 0; i < FE; ++i)
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k) {
+                const uint32_t pos = uint32_t(e[i][k]);
+                FCLSH_DCHECK((pos >> 6) < words && b0[i] + cnt[i] <= fh.max_dims);
+                const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
+                if ((w >> (pos & 63)) & 1) t[i] += (long long)(e[i][k] >> 32);
+            }
+    }
+#pragma unroll
+    for (int h = 1; h < FE; h <<= 1) { // index bits 5.. : within the lane
+#pragma unroll
+        for (int i = 0; i < FE; ++i)
+            if (!(i & h)) {
+                const long long x = t[i], y = t[i | h];
+                t[i] = x + y;
+                t[i | h] = x - y;
+            }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { // index bits 0..4: across lanes
+#pragma unroll
+        for (int i = 0; i < FE; ++i) {
+            const long long other = __shfl_xor_sync(kAll, t[i], o);
+            t[i] = (lane & o) ? other - t[i] : t[i] + other;
+        }
+    }
+    const long long l1 = __shfl_sync(kAll, t[0], 0); // F[0] = sum of the sketch
+#pragma unroll
+    for (int i = 0; i < FE; ++i) {
+        uint64_t x = uint64_t(l1 - t[i]) >> 1;
+        if (P == 0x7FFFFFFFull) {
+            x = (x & P) + (x >> 31);
+            x = (x & P) + (x >> 31);
+            x = x >= P ? x - P : x;
+        } else {
+            x %= P;
+        }
+        key[i] = K(x);
+    }
+}
+
+// the query row into registers (word `lane` on lane `lane`); rows in mapped
+// host memory are also copied to the device rows
+__device__ __forceinline__ uint64_t fused_row(const FusedHash& fh, uint64_t q, uint32_t words,
+                                              const uint64_t* qrows, int lane) {
     const uint64_t* src = (fh.hash_src ? fh.hash_src : qrows) + q * words;
+    uint64_t rw = 0;
     if (uint32_t(lane) < words) {
         rw = src[lane];
         if (fh.hash_src) const_cast<uint64_t*>(qrows)[q * words + lane] = rw;
     }
-    const uint64_t P = fh.prime;
+    return rw;
+}
+
+template <int FE, bool SMEM, typename K>
+__device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
+                                           uint64_t q, uint32_t words, const uint64_t* qrows, K* keys, int lane,
+                                           uint64_t& rw) {
+    rw = fused_row(fh, q, words, qrows, lane);
     for (uint32_t p = 0; p < fh.parts; ++p) {
-        const uint32_t* cp = cp_all + uint64_t(p) * (fh.N + 1);
-        const uint64_t* pk = pk_all + uint64_t(p) * fh.max_dims;
-        // the sketch of the lane's FE columns: every column's (seed, bit)
-        // entries are loaded kBatch at a time for all FE columns at once (no
-        // load waits on another: two L2 round trips per batch of kBatch * FE
-        // entries instead of one per entry); a missing entry loads as 0 = seed 0
-        constexpr int kBatch = 4;
-        uint32_t b0[FE], cnt[FE], mx = 0;
-        long long t[FE];
-#pragma unroll
-        for (int i = 0; i < FE; ++i) {
-            const uint32_t c = uint32_t(lane) + 32u * i;
-            b0[i] = fam_ld<SMEM>(cp + c);
-            cnt[i] = fam_ld<SMEM>(cp + c + 1) - b0[i];
-            mx = max(mx, cnt[i]);
-            t[i] = 0;
-        }
-        const uint32_t m = __reduce_max_sync(kAll, mx); // warp-uniform trip count (the shuffles need every lane)
-        for (uint32_t k0 = 0; k0 < m; k0 += kBatch) {
-            uint64_t e[FE][kBatch];
-#pragma unroll
-            for (int i = 0; i < FE; ++i)
-#pragma unroll
-                for (int k = 0; k < kBatch; ++k) e[i][k] = k0 + k < cnt[i] ? fam_ld<SMEM>(pk + b0[i] + k0 + k) : 0ull;
-#pragma unroll
-            for (int i = 0; i < FE; ++i)
-#pragma unroll
-                for (int k = 0; k < kBatch; ++k) {
-                    const uint32_t pos = uint32_t(e[i][k]);
-                    FCLSH_DCHECK((pos >> 6) < words && b0[i] + cnt[i] <= fh.max_dims);
-                    const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
-                    if ((w >> (pos & 63)) & 1) t[i] += (long long)(e[i][k] >> 32);
-                }
-        }
-#pragma unroll
-        for (int h = 1; h < FE; h <<= 1) { // index bits 5.. : within the lane
-#pragma unroll
-            for (int i = 0; i < FE; ++i)
-                if (!(i & h)) {
-                    const long long x = t[i], y = t[i | h];
-                    t[i] = x + y;
-                    t[i | h] = x - y;
-                }
-        }
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) { // index bits 0..4: across lanes
-#pragma unroll
-            for (int i = 0; i < FE; ++i) {
-                const long long other = __shfl_xor_sync(kAll, t[i], o);
-                t[i] = (lane & o) ? other - t[i] : t[i] + other;
-            }
-        }
-        const long long l1 = __shfl_sync(kAll, t[0], 0); // F[0] = sum of the sketch
+        K key[FE];
+        hash_part<FE, SMEM>(fh, cp_all, pk_all, p, words, rw, lane, key);
         K* kp = keys + uint64_t(p) * fh.L;
 #pragma unroll
         for (int i = 0; i < FE; ++i) {
             const uint32_t v = uint32_t(lane) + 32u * i;
-            uint64_t x = uint64_t(l1 - t[i]) >> 1;
-            if (P == 0x7FFFFFFFull) {
-                x = (x & P) + (x >> 31);
-                x = (x & P) + (x >> 31);
-                x = x >= P ? x - P : x;
-            } else {
-                x %= P;
-            }
-            if (v) kp[v - 1] = K(x);
+            if (v) kp[v - 1] = key[i];
         }
     }
 }
 
-template <typename T, int U, int MINB, int FE, bool FSM = false>
+// PM (with FE > 0): part-major -- a part's keys are hashed into registers
+// and its tables probed straight from them (lane `lane` of round (p, i) probes
+// the table of v = lane + 32 i), so the keys make no global round trip before
+// the probes, and part p's probes are in flight before part p+1 is hashed;
+// the keys are also stored for the hand-over kernels.
+template <typename T, int U, int MINB, int FE, bool FSM = false, bool PM = false>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -1192,7 +1219,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         FCLSH_TRACE_STAMP(q, 5, smid);
 #endif
-        if constexpr (FE > 0) {
+        if constexpr (FE > 0 && !PM) {
             fused_hash<FE, FSM>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
@@ -1245,6 +1272,71 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                 mm &= mm - 1;
             }
         };
+        // the run of full buckets after a home bucket whose last slot is taken (~3 %)
+        auto probe_run = [&](bool cont, uint64_t kk, uint32_t t) {
+            uint64_t b = home_of(kk, tb) + 1;
+            const E* base = tb.data + uint64_t(t) * tb.nbuckets * kSlots;
+            while (__any_sync(kAll, cont)) {
+                E x[kSlots];
+#pragma unroll
+                for (int j = 0; j < kSlots; ++j) x[j] = T::make(~0ull, ~0u);
+                b &= tb.nbuckets - 1;
+                if (cont) load_bucket(base + b * kSlots, x);
+                offer_bucket(x, cont, kk);
+                cont = cont && !T::empty(x[kSlots - 1]);
+                ++b;
+            }
+        };
+        if constexpr (FE > 0 && PM) {
+            rw = fused_row(fh, q, words, qrows, lane);
+            K* const qkw = qkeys + q * tables;
+            // every part is hashed and its keys stored even once the query is
+            // handed over (> 32 distinct ids): the CTA kernel probes from them
+            for (uint32_t p = 0; p < fh.parts; ++p) {
+                K key[FE];
+                hash_part<FE, FSM>(fh, cp_all, pk_all, p, words, rw, lane, key);
+                bool live[FE];
+#pragma unroll
+                for (int i = 0; i < FE; ++i) {
+                    const uint32_t v = uint32_t(lane) + 32u * i, t = p * fh.L + v - 1;
+                    if (v) qkw[t] = key[i];
+                    live[i] = !over && v != 0 && (!tb.filter || filter_pass(tb, t, uint64_t(key[i]), fpol));
+                }
+#pragma unroll
+                for (int i0 = 0; i0 < FE; i0 += U) {
+                    if (over) break;
+                    E sl[U][kSlots];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) { // U home buckets in flight
+                        const int i = i0 + u;
+                        const uint32_t t = p * fh.L + uint32_t(lane) + 32u * i - 1;
+                        if (i < FE && live[i < FE ? i : 0]) {
+                            FCLSH_DCHECK(t < tables && home_of(uint64_t(key[i]), tb) < tb.nbuckets);
+                            load_bucket_probe(tb.data + (uint64_t(t) * tb.nbuckets + home_of(uint64_t(key[i]), tb)) * kSlots,
+                                              sl[u], bpol);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kSlots; ++j) sl[u][j] = T::make(~0ull, ~0u);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int i = i0 + u;
+                        if (i >= FE) break;
+                        const uint64_t kk = uint64_t(key[i]);
+                        const bool lv = live[i];
+                        offer_bucket(sl[u], lv, kk);
+                        probe_run(lv && !T::empty(sl[u][kSlots - 1]), kk, p * fh.L + uint32_t(lane) + 32u * i - 1);
+                    }
+#ifdef FCLSH_TRACE
+                    {
+                        const uint32_t r = p * ((FE + U - 1) / U) + i0 / U;
+                        if (r < 8) FCLSH_TRACE_STAMP(q, 8 + r, clock64() - c0);
+                    }
+#endif
+                }
+            }
+        } else {
         // the pipeline: keys of rounds c, c+1, c+2 and the filter result of c+1
         K k0[U], k1[U], k2[U];
         bool p1[U];
@@ -1285,20 +1377,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
                 const uint64_t kk = uint64_t(k0[u]);
                 const bool live = p0[u];
                 offer_bucket(sl[u], live, kk);
-                // the run continues into the next bucket (~3 %)
-                bool cont = live && !T::empty(sl[u][kSlots - 1]);
-                uint64_t b = home_of(kk, tb) + 1;
-                const E* base = tb.data + uint64_t(base_t + u * 32 + lane) * tb.nbuckets * kSlots;
-                while (__any_sync(kAll, cont)) {
-                    E x[kSlots];
-#pragma unroll
-                    for (int j = 0; j < kSlots; ++j) x[j] = T::make(~0ull, ~0u);
-                    b &= tb.nbuckets - 1;
-                    if (cont) load_bucket(base + b * kSlots, x);
-                    offer_bucket(x, cont, kk);
-                    cont = cont && !T::empty(x[kSlots - 1]);
-                    ++b;
-                }
+                probe_run(live && !T::empty(sl[u][kSlots - 1]), kk, base_t + u * 32 + lane);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1310,6 +1389,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             if (base_t / kStep < 8) FCLSH_TRACE_STAMP(q, 8 + base_t / kStep, clock64() - c0);
 #endif
         }
+        } // (pipelined rounds)
         const uint64_t m = __reduce_add_sync(kAll, coll);
         claim(); // the warp's next query (read at the top of the loop)
 #ifdef FCLSH_TRACE
@@ -1319,7 +1399,18 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         uint32_t dist = 0;
         if constexpr (FE > 0) { // the query row is in registers (word w on lane w)
             const uint64_t* r = rows + uint64_t(over || uint32_t(lane) >= nd ? 0 : list) * words;
-            for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __shfl_sync(kAll, rw, w));
+            if (words % 4 == 0) { // 256-bit loads of the candidate row (stored rows are 32-B aligned)
+                for (uint32_t w = 0; w < words; w += 4) {
+                    unsigned long long a0, a1, a2, a3;
+                    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                        : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3)
+                        : "l"(r + w));
+                    dist += __popcll(a0 ^ __shfl_sync(kAll, rw, w)) + __popcll(a1 ^ __shfl_sync(kAll, rw, w + 1)) +
+                            __popcll(a2 ^ __shfl_sync(kAll, rw, w + 2)) + __popcll(a3 ^ __shfl_sync(kAll, rw, w + 3));
+                }
+            } else {
+                for (uint32_t w = 0; w < words; ++w) dist += __popcll(__ldg(r + w) ^ __shfl_sync(kAll, rw, w));
+            }
             if (over || uint32_t(lane) >= nd) dist = 0;
         } else if (!over && uint32_t(lane) < nd) {
             dist = row_distance(rows + uint64_t(list) * words, qrows + q * words, words, vec_rows);
@@ -2365,16 +2456,28 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
         const int wu = wu_env ? wu_env : (ix.tables <= 400 ? 3 : 2);
         const int fe = fused_fe(ix);
         const bool fsm = fe > 0 && fused_params(ix, hash_src).smem_bytes > 0;
+        // part-major fused hash (keys in registers) with the family in shared
+        // memory for one-register parts (cfg1: 34.2 -> 35.7 M q/s); cfg3
+        // measured slower part-major (fused kernel 88.3 -> 89.7 us, replayed
+        // 1M batch 157.5 -> 145.3 M q/s: profiles/r02/ab_part_major.txt).
+        // A/B: FCLSH_FUSED_PM=1 (every FE), FCLSH_FUSED_PF=1 (never)
+        static const bool pf_env = getenv("FCLSH_FUSED_PF") != nullptr;
+        static const bool pm_env = getenv("FCLSH_FUSED_PM") != nullptr;
+        const bool pm = fsm && !pf_env && (fe == 1 || pm_env);
         if (fe == 1)
-            fsm ? go(k_query_warp_pf<T, 3, 4, 1, true>, true) : go(k_query_warp_pf<T, 3, 4, 1>);
+            pm ? go(k_query_warp_pf<T, 3, 4, 1, true, true>, true)
+               : fsm ? go(k_query_warp_pf<T, 3, 4, 1, true>, true) : go(k_query_warp_pf<T, 3, 4, 1>);
         else if (fe == 2)
-            fsm ? go(k_query_warp_pf<T, 3, 4, 2, true>, true) : go(k_query_warp_pf<T, 3, 4, 2>);
+            pm ? go(k_query_warp_pf<T, 2, 5, 2, true, true>, true)
+               : fsm ? go(k_query_warp_pf<T, 3, 4, 2, true>, true) : go(k_query_warp_pf<T, 3, 4, 2>);
         else if (fe == 4 && wu_env == 3)
             fsm ? go(k_query_warp_pf<T, 3, 4, 4, true>, true) : go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
-            fsm ? go(k_query_warp_pf<T, 2, 5, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
+            pm ? go(k_query_warp_pf<T, 2, 5, 4, true, true>, true)
+               : fsm ? go(k_query_warp_pf<T, 2, 5, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 8)
-            fsm ? go(k_query_warp_pf<T, 2, 4, 8, true>, true) : go(k_query_warp_pf<T, 2, 4, 8>);
+            pm ? go(k_query_warp_pf<T, 2, 4, 8, true, true>, true)
+               : fsm ? go(k_query_warp_pf<T, 2, 4, 8, true>, true) : go(k_query_warp_pf<T, 2, 4, 8>);
         else if (wu == 4)
             go(k_query_warp_pf<T, 4, 3, 0>);
         else if (wu == 3)
