@@ -93,6 +93,9 @@ constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
 // serialise in its L2 slice (18.7 % of the kernel's stall samples on cfg3,
 // profiles/r02/ncu_k_query_warp_pf_atomic_cfg3.txt)
 constexpr uint32_t kQCtr = 16, kQCtrStride = 64;
+#ifndef FCLSH_FE4_MINB
+#define FCLSH_FE4_MINB 5 // CTAs per SM of the cfg3 warp kernel (A/B builds: 6 same, 7-8 spill and lose 17 %)
+#endif
 constexpr uint64_t kCntHeader = 64 + uint64_t(kQCtr) * kQCtrStride * 4; // bytes before the tile sums
 #ifndef FCLSH_FUSED_CAP
 #define FCLSH_FUSED_CAP 256
@@ -2474,7 +2477,7 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
             fsm ? go(k_query_warp_pf<T, 3, 4, 4, true>, true) : go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
             pm ? go(k_query_warp_pf<T, 2, 5, 4, true, true>, true)
-               : fsm ? go(k_query_warp_pf<T, 2, 5, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
+               : fsm ? go(k_query_warp_pf<T, 2, FCLSH_FE4_MINB, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
         else if (fe == 8)
             pm ? go(k_query_warp_pf<T, 2, 4, 8, true, true>, true)
                : fsm ? go(k_query_warp_pf<T, 2, 4, 8, true>, true) : go(k_query_warp_pf<T, 2, 4, 8>);
