@@ -1133,6 +1133,18 @@ std::unique_ptr<DeviceFamilySet> make_device_family_set(const Plan& plan, std::v
             std::vector<uint64_t> pk(eseed.size());
             for (size_t k = 0; k < pk.size(); ++k) pk[k] = (eseed[k] << 32) | epos[k];
             FCLSH_CUDA(cudaMemcpy(fs->ent_pk.ensure(pk.size() * 8), pk.data(), pk.size() * 8, cudaMemcpyHostToDevice));
+            if (N <= (uint64_t(1) << 16) && plan.dims <= (uint64_t(1) << 16)) {
+                // the fused query hash's position-parallel sketch: one entry per
+                // view position (missing positions of a short part: seed 0)
+                std::vector<uint64_t> sk(size_t(fs->parts) * fs->max_part_dims, 0);
+                for (uint32_t p = 0; p < fs->parts; ++p) {
+                    const Family& f = families[p];
+                    for (uint64_t j = 0; j < f.dims; ++j)
+                        sk[size_t(p) * fs->max_part_dims + j] =
+                            (f.seeds[j] << 32) | (uint64_t(f.mapping[j]) << 16) | uint64_t(plan.source_bit(p, j));
+                }
+                FCLSH_CUDA(cudaMemcpy(fs->ent_sk.ensure(sk.size() * 8), sk.data(), sk.size() * 8, cudaMemcpyHostToDevice));
+            }
         }
     }
 

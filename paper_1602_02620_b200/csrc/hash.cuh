@@ -44,6 +44,7 @@ struct DeviceFamilySet {
     DevBuf ent_pos;  // uint32 [parts][max_dims]
     DevBuf ent_seed; // uint64 [parts][max_dims]
     DevBuf ent_pk;   // uint64 [parts][max_dims]: seed << 32 | source bit, primes < 2^32 (the fused query hash)
+    DevBuf ent_sk;   // uint64 [parts][max_dims], view order: seed << 32 | column << 16 | source bit (fused hash, N <= 2^16, d <= 2^16)
     uint64_t max_part_dims = 0;
     DevBuf scratch;  // generic path workspace
 

@@ -1014,6 +1014,8 @@ struct FusedHash {
     const uint32_t* ent_pos = nullptr; // [parts][max_dims] source-row bit
     const uint64_t* ent_seed = nullptr;
     const uint64_t* ent_pk = nullptr; // [parts][max_dims] seed << 32 | source bit
+    const uint64_t* ent_sk = nullptr; // [parts][max_dims] seed << 32 | column << 16 | source bit (view order)
+    uint32_t sk_warp_bytes = 0;       // > 0: position-parallel sketch; per-warp scratch after the family
     uint64_t prime = 0;
     const uint64_t* hash_src = nullptr; // mapped pinned host rows (null: the device rows)
     uint32_t smem_bytes = 0; // > 0: the kernel stages col_ptr and ent_pk in shared memory (this many bytes)
@@ -1116,6 +1118,77 @@ __device__ __forceinline__ void hash_part(const FusedHash& fh, const uint32_t* c
     }
 }
 
+// hash_part with a position-parallel sketch: lane k takes view positions k,
+// k + 32, ... of the part (entries seed << 32 | column << 16 | source bit,
+// staged in shared memory), tests its row bit (the row staged in this warp's
+// shared scratch) and adds the seed's two 16-bit halves to the column's two
+// 32-bit shared accumulators (RED.ADD on shared memory: integer, so the
+// order does not matter). ceil(d'/32) entries per lane instead of FE x the
+// longest column list (cfg3: 8 against 32 entry slots per part and lane).
+template <int FE, typename K>
+__device__ __forceinline__ void hash_part_sk(const FusedHash& fh, const uint64_t* sk_all, uint32_t p,
+                                             const uint32_t* row_s, uint32_t* acc, int lane, K (&key)[FE]) {
+    constexpr unsigned kAll = 0xffffffffu;
+    constexpr uint32_t N = 32u * FE;
+    const uint64_t P = fh.prime;
+    uint32_t* lo = acc;
+    uint32_t* hi = acc + N;
+#pragma unroll
+    for (int i = 0; i < 2 * FE; ++i) acc[lane + 32 * i] = 0;
+    __syncwarp();
+    const uint64_t* e = sk_all + uint64_t(p) * fh.max_dims;
+    const uint32_t nent = uint32_t(fh.max_dims);
+#pragma unroll 4
+    for (uint32_t k = lane; k < nent; k += 32) {
+        const uint64_t x = e[k];
+        const uint32_t pos = uint32_t(x) & 0xFFFFu, col = uint32_t(x) >> 16;
+        FCLSH_DCHECK(col < N);
+        if ((row_s[pos >> 5] >> (pos & 31)) & 1u) {
+            const uint32_t sd = uint32_t(x >> 32);
+            atomicAdd(lo + col, sd & 0xFFFFu);
+            atomicAdd(hi + col, sd >> 16);
+        }
+    }
+    __syncwarp();
+    long long t[FE];
+#pragma unroll
+    for (int i = 0; i < FE; ++i) {
+        const uint32_t c = uint32_t(lane) + 32u * i;
+        t[i] = (long long)lo[c] + ((long long)hi[c] << 16);
+    }
+#pragma unroll
+    for (int h = 1; h < FE; h <<= 1) { // index bits 5.. : within the lane
+#pragma unroll
+        for (int i = 0; i < FE; ++i)
+            if (!(i & h)) {
+                const long long x = t[i], y = t[i | h];
+                t[i] = x + y;
+                t[i | h] = x - y;
+            }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { // index bits 0..4: across lanes
+#pragma unroll
+        for (int i = 0; i < FE; ++i) {
+            const long long other = __shfl_xor_sync(kAll, t[i], o);
+            t[i] = (lane & o) ? other - t[i] : t[i] + other;
+        }
+    }
+    const long long l1 = __shfl_sync(kAll, t[0], 0); // F[0] = sum of the sketch
+#pragma unroll
+    for (int i = 0; i < FE; ++i) {
+        uint64_t x = uint64_t(l1 - t[i]) >> 1;
+        if (P == 0x7FFFFFFFull) {
+            x = (x & P) + (x >> 31);
+            x = (x & P) + (x >> 31);
+            x = x >= P ? x - P : x;
+        } else {
+            x %= P;
+        }
+        key[i] = K(x);
+    }
+}
+
 // the query row into registers (word `lane` on lane `lane`); rows in mapped
 // host memory are also copied to the device rows
 __device__ __forceinline__ uint64_t fused_row(const FusedHash& fh, uint64_t q, uint32_t words,
@@ -1129,14 +1202,21 @@ __device__ __forceinline__ uint64_t fused_row(const FusedHash& fh, uint64_t q, u
     return rw;
 }
 
-template <int FE, bool SMEM, typename K>
+template <int FE, bool SMEM, bool SK, typename K>
 __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
                                            uint64_t q, uint32_t words, const uint64_t* qrows, K* keys, int lane,
-                                           uint64_t& rw) {
+                                           uint64_t& rw, uint64_t* row_s, uint32_t* acc) {
     rw = fused_row(fh, q, words, qrows, lane);
+    if constexpr (SK) {
+        if (uint32_t(lane) < words) row_s[lane] = rw;
+        __syncwarp();
+    }
     for (uint32_t p = 0; p < fh.parts; ++p) {
         K key[FE];
-        hash_part<FE, SMEM>(fh, cp_all, pk_all, p, words, rw, lane, key);
+        if constexpr (SK)
+            hash_part_sk<FE>(fh, pk_all, p, reinterpret_cast<const uint32_t*>(row_s), acc, lane, key);
+        else
+            hash_part<FE, SMEM>(fh, cp_all, pk_all, p, words, rw, lane, key);
         K* kp = keys + uint64_t(p) * fh.L;
 #pragma unroll
         for (int i = 0; i < FE; ++i) {
@@ -1151,7 +1231,9 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* 
 // the table of v = lane + 32 i), so the keys make no global round trip before
 // the probes, and part p's probes are in flight before part p+1 is hashed;
 // the keys are also stored for the hand-over kernels.
-template <typename T, int U, int MINB, int FE, bool FSM = false, bool PM = false>
+// SK (with FSM): the position-parallel sketch (hash_part_sk); the family's
+// entries and every warp's row + column accumulators in shared memory.
+template <typename T, int U, int MINB, int FE, bool FSM = false, bool PM = false, bool SK = false>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -1177,7 +1259,18 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     extern __shared__ __align__(16) unsigned char fam_smem[];
     const uint32_t* cp_all = fh.col_ptr;
     const uint64_t* pk_all = fh.ent_pk;
-    if constexpr (FE > 0 && FSM) {
+    uint64_t* row_s = nullptr; // SK: this warp's row and column accumulators
+    uint32_t* acc_s = nullptr;
+    if constexpr (FE > 0 && FSM && SK) {
+        uint64_t* sk_s = reinterpret_cast<uint64_t*>(fam_smem);
+        const uint32_t nsk = fh.parts * uint32_t(fh.max_dims);
+        for (uint32_t i = threadIdx.x; i < nsk; i += blockDim.x) sk_s[i] = __ldg(fh.ent_sk + i);
+        unsigned char* wbase = fam_smem + size_t(nsk) * 8 + size_t(threadIdx.x >> 5) * fh.sk_warp_bytes;
+        acc_s = reinterpret_cast<uint32_t*>(wbase);
+        row_s = reinterpret_cast<uint64_t*>(wbase + size_t(FE) * 32 * 2 * 4);
+        __syncthreads();
+        pk_all = sk_s;
+    } else if constexpr (FE > 0 && FSM) {
         uint64_t* pk_s = reinterpret_cast<uint64_t*>(fam_smem);
         const uint32_t npk = fh.parts * uint32_t(fh.max_dims);
         uint32_t* cp_s = reinterpret_cast<uint32_t*>(pk_s + npk);
@@ -1223,7 +1316,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         FCLSH_TRACE_STAMP(q, 5, smid);
 #endif
         if constexpr (FE > 0 && !PM) {
-            fused_hash<FE, FSM>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw);
+            fused_hash<FE, FSM, SK>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw, row_s, acc_s);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
 #ifdef FCLSH_TRACE
@@ -1292,12 +1385,19 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         };
         if constexpr (FE > 0 && PM) {
             rw = fused_row(fh, q, words, qrows, lane);
+            if constexpr (SK) {
+                if (uint32_t(lane) < words) row_s[lane] = rw;
+                __syncwarp();
+            }
             K* const qkw = qkeys + q * tables;
             // every part is hashed and its keys stored even once the query is
             // handed over (> 32 distinct ids): the CTA kernel probes from them
             for (uint32_t p = 0; p < fh.parts; ++p) {
                 K key[FE];
-                hash_part<FE, FSM>(fh, cp_all, pk_all, p, words, rw, lane, key);
+                if constexpr (SK)
+                    hash_part_sk<FE>(fh, pk_all, p, reinterpret_cast<const uint32_t*>(row_s), acc_s, lane, key);
+                else
+                    hash_part<FE, FSM>(fh, cp_all, pk_all, p, words, rw, lane, key);
                 bool live[FE];
 #pragma unroll
                 for (int i = 0; i < FE; ++i) {
@@ -2405,6 +2505,7 @@ FusedHash fused_params(const DeviceIndex& ix, const uint64_t* hash_src) {
     f.max_dims = fs.max_part_dims;
     f.col_ptr = fs.col_ptr.as<uint32_t>();
     f.ent_pk = fs.ent_pk.as<uint64_t>();
+    f.ent_sk = fs.ent_sk.as<uint64_t>();
     f.ent_pos = fs.ent_pos.as<uint32_t>();
     f.ent_seed = fs.ent_seed.as<uint64_t>();
     f.prime = fs.prime;
@@ -2428,9 +2529,13 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
     static const bool v1 = getenv("FCLSH_WARP_V1") != nullptr; // A/B: the unpipelined warp kernel
     if (!shared_set && !v1 && LAYOUT == kLayoutBuckets) {
         const int vec = vec_for(ix.row_words, d_q);
-        auto go = [&](auto kern, bool use_smem = false) {
+        auto go = [&](auto kern, bool use_smem = false, int sk_fe = 0) {
             FusedHash fh = fused_params(ix, hash_src);
             if (!use_smem) fh.smem_bytes = 0;
+            if (sk_fe) { // position-parallel sketch: entries + per-warp row and column accumulators
+                fh.sk_warp_bytes = uint32_t((uint64_t(sk_fe) * 32 * 2 * 4 + uint64_t(ix.row_words) * 8 + 15) & ~uint64_t(15));
+                fh.smem_bytes = uint32_t((uint64_t(fh.parts) * fh.max_dims * 8 + 15) & ~uint64_t(15)) + 8 * fh.sk_warp_bytes;
+            }
             // carveout: none (all of the unified array as L1 for the probes in
             // flight), or just enough shared memory for MINB CTAs' staged family
             static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
@@ -2467,7 +2572,19 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
         static const bool pf_env = getenv("FCLSH_FUSED_PF") != nullptr;
         static const bool pm_env = getenv("FCLSH_FUSED_PM") != nullptr;
         const bool pm = fsm && !pf_env && (fe == 1 || pm_env);
-        if (fe == 1)
+        // the position-parallel sketch (hash_part_sk) for FE = 1 (cfg1: 35.4 ->
+        // 36.7 M q/s); for cfg3 (FE = 4) its 1 KB of accumulators per warp
+        // take L1 from the probes in flight: kernel 88.4 -> 91.8 us
+        // (profiles/r02/ab_sketch.txt). A/B: FCLSH_SKETCH_COLS=1 keeps the
+        // per-column lists, FCLSH_SKETCH_ALL=1 uses the sketch for FE = 4 too
+        static const bool cols_env = getenv("FCLSH_SKETCH_COLS") != nullptr;
+        static const bool sk4_env = getenv("FCLSH_SKETCH_ALL") != nullptr;
+        const bool sk = fsm && !cols_env && fused_params(ix, hash_src).ent_sk != nullptr;
+        if (fe == 1 && pm && sk)
+            go(k_query_warp_pf<T, 3, 4, 1, true, true, true>, true, 1);
+        else if (fe == 4 && !pm && wu_env != 3 && sk && sk4_env)
+            go(k_query_warp_pf<T, 2, FCLSH_FE4_MINB, 4, true, false, true>, true, 4);
+        else if (fe == 1)
             pm ? go(k_query_warp_pf<T, 3, 4, 1, true, true>, true)
                : fsm ? go(k_query_warp_pf<T, 3, 4, 1, true>, true) : go(k_query_warp_pf<T, 3, 4, 1>);
         else if (fe == 2)
