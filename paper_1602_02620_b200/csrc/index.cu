@@ -2540,8 +2540,10 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
             // flight), or just enough shared memory for MINB CTAs' staged family
             static std::atomic<uint64_t> carved{0}; // devices whose carveout is set (per instantiation)
             static std::atomic<int> carve_pct{-1};
-            const int want = fh.smem_bytes ? int((uint64_t(fh.smem_bytes + 1024) * 6 * 100 + 228 * 1024 - 1) / (228 * 1024))
-                                           : 0;
+            static const int carve_env = getenv("FCLSH_CARVE") ? atoi(getenv("FCLSH_CARVE")) : -1; // A/B (%)
+            const int want = carve_env >= 0 ? carve_env
+                             : fh.smem_bytes ? int((uint64_t(fh.smem_bytes + 1024) * 6 * 100 + 228 * 1024 - 1) / (228 * 1024))
+                                             : 0;
             const uint64_t bit = uint64_t(1) << (ix.device & 63);
             if (!(carved.load(std::memory_order_acquire) & bit) || carve_pct.load() != want) {
                 FCLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(want, 100)));
