@@ -85,8 +85,14 @@ struct WideEntry { // 8-byte keys: {key, id}
 
 constexpr int kSlots = 4; // per bucket
 constexpr uint32_t kBuildSlab = 64; // tables per table-major slab of the bucket build
-constexpr int kScanTileLog = 10; // queries per tile of the found scan (k_scan_compact): 1024
-constexpr int kScanSplit = 8;    // CTAs sharing one tile's copying
+#ifndef FCLSH_SCAN_TILE_LOG
+#define FCLSH_SCAN_TILE_LOG 10
+#endif
+#ifndef FCLSH_SCAN_SPLIT
+#define FCLSH_SCAN_SPLIT 8
+#endif
+constexpr int kScanTileLog = FCLSH_SCAN_TILE_LOG; // queries per tile of the found scan (k_scan_compact), = its CTA size
+constexpr int kScanSplit = FCLSH_SCAN_SPLIT;      // CTAs sharing one tile's copying
 // The warp kernel hands out the queries past its first wave from kQCtr
 // counters kQCtrStride words (256 B) apart -- CTA b draws from counter
 // b % kQCtr -- instead of one: ~10k returning atomics on one address
@@ -2290,7 +2296,7 @@ __global__ void __launch_bounds__(1024) k_scan_compact(
     if (lane == 31) wsum[wid] = x;
     __syncthreads();
     if (wid == 0) {
-        unsigned long long w = wsum[lane];
+        unsigned long long w = lane < (blockDim.x >> 5) ? wsum[lane] : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
@@ -2892,7 +2898,7 @@ void query_enqueue_impl(DeviceIndex& ix, const uint64_t* d_q, uint64_t nq, uint3
         }
         rec(3);
         rec(4); // (one kernel: scan, offsets, compaction, publish)
-        launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit + 1), 1024, 0, s, nq,
+        launch_pdl(k_scan_compact, unsigned(b.ntiles * kScanSplit + 1), 1u << kScanTileLog, 0, s, nq,
                    static_cast<const unsigned long long*>(b.found_q), static_cast<const unsigned long long*>(b.tile_sum),
                    b.res_off, static_cast<const unsigned long long*>(b.src_pos),
                    static_cast<const uint32_t*>(b.tmp_id), static_cast<const uint32_t*>(b.tmp_dist), nq * slot_cap,
