@@ -371,3 +371,22 @@ def test_home_bucket_spread_for_primes_below_a_power_of_two(oracle, prime):
     rows = random_rows(rng, 4000, d)
     q = planted_queries(rng, rows, d, 120, 6)
     check_against_oracle(oracle, rows, q, d, 4, (0, 1), prime, layouts=("buckets", "csr"))
+
+
+@pytest.mark.parametrize("extra", [-1, 0, 1, 15, 16, 17, 700])
+def test_query_handout_around_the_first_wave(oracle, extra):
+    """The warp kernel's first wave takes queries 0 .. warps-1 by warp index and
+    hands the rest out from 16 counters (CTA b draws from counter b mod 16):
+    batches just below, at and past the first wave's size (every counter
+    empty, one query, each counter's first, a second round) answer every
+    query exactly once. cfg3's shape (d = 512, two 256-bit parts, per-part
+    radius 6: the fused hash, 5 CTAs/SM of 8 warps on this GPU)."""
+    import torch
+    rng = np.random.default_rng(1000 + extra)
+    d, r = 512, 12
+    rows = random_rows(rng, 20000, d)
+    wave = 5 * 8 * torch.cuda.get_device_properties(0).multi_processor_count
+    nq = wave + extra
+    q = planted_queries(rng, rows, d, nq, r)
+    res = check_against_oracle(oracle, rows, q, d, r, (2, 2), M31, layouts=("buckets",))
+    assert res.found.sum() >= nq  # every planted query finds its source row
