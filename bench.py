@@ -45,6 +45,7 @@ import numpy as np  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
+RANDOM_READ_CEILING = 41.5e9  # random 32-B reads/s, tools/rand_bench.cu (profiles/r01/rand_bench.txt)
 METRIC = "queries/sec at 100% recall (result set == oracle)"
 HEADLINE = 3
 M31 = (1 << 31) - 1
@@ -453,6 +454,19 @@ def run_config(ctx, cfg, scaling, spr, args, flush, stream, clocks, hbm, peak_sr
                        "bytes_note": "per (query, table) the key + one random 32-B bucket sector (also for the "
                                      "probes the L2 key filter skips), per distinct candidate max(32, d/8) B, per "
                                      "result 8 B, query rows once; traffic = measured DRAM bytes per launch (ncu)"}
+    # the same kernel against the GPU's random-access ceiling: its random
+    # 32-B reads (a bucket per probe, CSR: a directory and a cell entry; a row
+    # per distinct candidate; the query rows) per second over the ~41.5 G
+    # reads/s tools/rand_bench.cu measured (profiles/r01/rand_bench.txt), the
+    # bound this kernel meets before the HBM byte bound
+    reads = (nq * T_ * (1 if layout_b else 2) + cand.sum()) / S + nq
+    out["roofline"]["random_reads_per_launch"] = reads
+    out["roofline"]["random_reads_per_s"] = reads / (dur / 1e3)
+    out["roofline"]["vs_random_read_ceiling"] = reads / (dur / 1e3) / RANDOM_READ_CEILING
+    out["roofline"]["random_read_ceiling"] = {"value": RANDOM_READ_CEILING, "unit": "reads/s",
+                                              "source": "tools/rand_bench.cu (profiles/r01/rand_bench.txt: 41-43 G "
+                                                        "random 32-B reads/s on this B200); probes the key filter "
+                                                        "skips are counted as reads"}
     hash_ms = stage_avg.get("hash", 0)
     if hash_ms > 0:
         hb = nq * (cfg.dims / 8 + T_ * 4)
@@ -512,6 +526,9 @@ def replay_batch(ctx, cl, q, q_dev, cfg, args, flush, stream, clocks):
         if 4 <= cfg.per_part_radius <= 7 and T_ <= 600:  # hash fused into the kernel: its key writes too
             algo += nq * T_ * 4
         verify = cand * (4 + R_) + found * 12 + nq * cfg.dims / 8
+        reads = nq * T_ + cand + nq  # bucket layout (the replayed configs' shard layout)
+        out.update({"random_reads_per_s": reads / (dur / 1e3),
+                    "vs_random_read_ceiling": reads / (dur / 1e3) / RANDOM_READ_CEILING})
         out.update({"kernel_ms": dur, "kernel_us_per_query": 1e3 * dur / nq,
                     "roofline_frac": algo / (dur / 1e3) / 1e9 / hbm_peak()[0], "algorithmic_bytes": algo,
                     "verify_bytes": verify, "verify_share_of_algorithmic_bytes": verify / algo,
