@@ -522,6 +522,14 @@ __device__ void bitonic_sort(Ptr a, uint32_t len, uint32_t pow2) {
     }
 }
 
+// 4-byte global -> shared copies in flight without registers (cp.async)
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_ix() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_ix() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <typename T>
 __global__ void __launch_bounds__(512) k_sort_big(const uint32_t* __restrict__ dir, uint64_t cells, uint64_t n,
                                                   typename T::E* __restrict__ entries, const uint2* __restrict__ big,
@@ -1653,7 +1661,20 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
     unsigned long long* const hc = desc ? reinterpret_cast<unsigned long long*>(desc[0]) : nullptr;
     const unsigned int ns = ovf ? *ovf_cnt : direct_n;
     if (blockIdx.x >= ns) return; // at most ns CTAs can get a query (usually ns == 0: nothing handed over)
-    __shared__ unsigned int next_s;
+    __shared__ unsigned int next_s, pf_next_s;
+    // CSR, flattened: the next query's keys and directory words are fetched
+    // while this query verifies (keys into f_key, cell bounds by cp.async
+    // into f_start / f_off), so its directory round trips overlap this one's
+    // verify and outputs (FCLSH_DENSE_PF=0 build: off, A/B)
+#ifndef FCLSH_DENSE_PF
+#define FCLSH_DENSE_PF 1
+#endif
+    const bool flat_pf = FCLSH_DENSE_PF && LAYOUT == kLayoutCsr && tables <= uint32_t(kFlatTables);
+    bool pf_have = false; // this query's directory words were prefetched
+    // the flattened CSR phase's per-table arrays (CSR shared memory only)
+    uint32_t* const f_off = reinterpret_cast<uint32_t*>(clist + kMaxDistinct + (kMaxDistinct & 1)); // [tables + 1]
+    uint32_t* const f_start = f_off + kFlatTables + 1;                                              // [tables]
+    uint64_t* const f_key = reinterpret_cast<uint64_t*>(f_start + kFlatTables + (kFlatTables & 1) + 1); // [tables]
     // dynamic hand-out (query costs vary widely on clustered data); the next
     // query is claimed as the current one starts, so the atomic's round trip
     // overlaps the probes
@@ -1764,28 +1785,35 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
             // (adjacent entries, coalesced) instead of walked by one thread
             // while the CTA waits for it at the barrier.
             using E = typename T::E;
-            uint32_t* const f_off = reinterpret_cast<uint32_t*>(clist + kMaxDistinct + (kMaxDistinct & 1)); // [tables + 1]
-            uint32_t* const f_start = f_off + kFlatTables + 1;                                              // [tables]
-            uint64_t* const f_key = reinterpret_cast<uint64_t*>(f_start + kFlatTables + (kFlatTables & 1) + 1); // [tables]
             constexpr int kPer = (kFlatTables + NT - 1) / NT; // tables per thread
             uint32_t len[kPer], loc = 0;
             const uint32_t tb0 = tid * kPer;
-            uint64_t key[kPer];
+            if (pf_have) { // fetched during the previous query (this thread's own tables)
+                cp_async_wait_all_ix();
 #pragma unroll
-            for (int k = 0; k < kPer; ++k) key[k] = tb0 + k < tables ? uint64_t(qk[tb0 + k]) : 0ull;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k) {
-                const uint32_t t = tb0 + k;
-                len[k] = 0;
-                if (t < tables) {
-                    FCLSH_DCHECK(home_of(key[k], tb) < tb.cells);
-                    const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[k], tb);
-                    const uint32_t a = __ldg(d), e = __ldg(d + 1);
-                    f_start[t] = a;
-                    f_key[t] = key[k];
-                    len[k] = e - a;
+                for (int k = 0; k < kPer; ++k) {
+                    const uint32_t t = tb0 + k;
+                    len[k] = t < tables ? f_off[t] - f_start[t] : 0u;
+                    loc += len[k];
                 }
-                loc += len[k];
+            } else {
+                uint64_t key[kPer];
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) key[k] = tb0 + k < tables ? uint64_t(qk[tb0 + k]) : 0ull;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    const uint32_t t = tb0 + k;
+                    len[k] = 0;
+                    if (t < tables) {
+                        FCLSH_DCHECK(home_of(key[k], tb) < tb.cells);
+                        const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key[k], tb);
+                        const uint32_t a = __ldg(d), e = __ldg(d + 1);
+                        f_start[t] = a;
+                        f_key[t] = key[k];
+                        len[k] = e - a;
+                    }
+                    loc += len[k];
+                }
             }
             uint32_t total = 0;
             uint32_t run = block_exclusive_scan(loc, scan_ws, total);
@@ -1832,8 +1860,20 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
             }
         }
         atomicAdd(&coll_s, coll);
+        if (tid == 0) pf_next_s = claimed; // (the claim made at this query's start has returned)
         __syncthreads();
         const uint32_t ncand = cand_s;
+        // the next query's keys (this thread's tables), loaded beside the verify
+        constexpr int kPf = (kFlatTables + NT - 1) / NT;
+        typename T::K pf_key[kPf];
+        const uint32_t pf_s = pf_next_s;
+        const bool pf = flat_pf && pf_s < ns;
+        if (pf) {
+            const uint64_t qn = ovf ? ovf[pf_s] : pf_s;
+            const typename T::K* qkn = qkeys + qn * tables;
+#pragma unroll
+            for (int k = 0; k < kPf; ++k) pf_key[k] = tid * kPf + k < tables ? qkn[tid * kPf + k] : typename T::K(0);
+        }
         // phase 2: verify the distinct candidates only
         if (!bad_s) {
             const uint64_t* qr = qrows + q * words;
@@ -1850,6 +1890,22 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
                 }
             }
         }
+        if (pf) { // phase 1 is done with f_key / f_start / f_off: the next query's go there
+#pragma unroll
+            for (int k = 0; k < kPf; ++k) {
+                const uint32_t t = tid * kPf + k;
+                if (t < tables) {
+                    const uint64_t key = uint64_t(pf_key[k]);
+                    FCLSH_DCHECK(home_of(key, tb) < tb.cells);
+                    const uint32_t* d = tb.dir + uint64_t(t) * (tb.cells + 1) + home_of(key, tb);
+                    f_key[t] = key;
+                    cp_async4(f_start + t, d);     // the cell's first entry
+                    cp_async4(f_off + t, d + 1);   // and its end (phase 1 turns it into the length)
+                }
+            }
+            cp_async_commit_ix();
+        }
+        pf_have = pf;
         __syncthreads();
         // clear what this query wrote (all of it when the list is incomplete)
         if (ncand <= kMaxDistinct) {
