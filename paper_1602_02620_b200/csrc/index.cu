@@ -1695,6 +1695,11 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
             bad_s = 0;
         }
         __syncthreads();
+        // the next query's prefetch (CSR, flattened): its keys, loaded during phase 1
+        constexpr int kPf = (kFlatTables + NT - 1) / NT;
+        typename T::K pf_key[kPf];
+        uint32_t pf_s = 0;
+        bool pf = false;
         // phase 1: probe, dedup into the set, list each new id's slot
         const typename T::K* qk = qkeys + q * tables;
         uint32_t coll = 0;
@@ -1816,6 +1821,7 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
                 }
             }
             uint32_t total = 0;
+            if (tid == 0) pf_next_s = claimed; // (read after the scan's barriers)
             uint32_t run = block_exclusive_scan(loc, scan_ws, total);
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
@@ -1824,6 +1830,16 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
             }
             if (tid == 0) f_off[tables] = total;
             __syncthreads();
+            // the next query's keys (this thread's tables), in flight beside
+            // the entry loads; their directory words follow after the verify
+            pf_s = pf_next_s;
+            pf = flat_pf && pf_s < ns;
+            if (pf) {
+                const uint64_t qn = ovf ? ovf[pf_s] : pf_s;
+                const typename T::K* qkn = qkeys + qn * tables;
+#pragma unroll
+                for (int k = 0; k < kPf; ++k) pf_key[k] = tb0 + k < tables ? qkn[tb0 + k] : typename T::K(0);
+            }
             for (uint32_t j0 = tid; j0 < total && !bad_s; j0 += kFlatU * nt) {
                 E e[kFlatU];
                 uint32_t tt[kFlatU];
@@ -1860,20 +1876,8 @@ __global__ void __launch_bounds__(NT, MINB) k_query_dense(
             }
         }
         atomicAdd(&coll_s, coll);
-        if (tid == 0) pf_next_s = claimed; // (the claim made at this query's start has returned)
         __syncthreads();
         const uint32_t ncand = cand_s;
-        // the next query's keys (this thread's tables), loaded beside the verify
-        constexpr int kPf = (kFlatTables + NT - 1) / NT;
-        typename T::K pf_key[kPf];
-        const uint32_t pf_s = pf_next_s;
-        const bool pf = flat_pf && pf_s < ns;
-        if (pf) {
-            const uint64_t qn = ovf ? ovf[pf_s] : pf_s;
-            const typename T::K* qkn = qkeys + qn * tables;
-#pragma unroll
-            for (int k = 0; k < kPf; ++k) pf_key[k] = tid * kPf + k < tables ? qkn[tid * kPf + k] : typename T::K(0);
-        }
         // phase 2: verify the distinct candidates only
         if (!bad_s) {
             const uint64_t* qr = qrows + q * words;
