@@ -618,6 +618,9 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
     constexpr int NP = N / 2; // column pairs per part
     static_assert(G > 1 && (EG == 1 || EG == 2), "phase-2 layout");
     constexpr double kTwo52 = 4503599627370496.0;
+    // added to every final-stage value D (even): moves O = D/2 by P - 0x43300000 (mod P), which
+    // cancels the exponent bits 0x43300000 that the high word of 2^52 + D carries (see finish)
+    constexpr double kFinishBias = 2.0 * double(kP31 - 0x43300000u);
 
     extern __shared__ __align__(16) unsigned char smem[];
     double* xbuf = reinterpret_cast<double*>(smem);                            // WARPS x 32*EP
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
             double T = x[0];
 #pragma unroll
             for (int o = 1; o < G; o <<= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
-            const double Tp = T + kTwo52;
+            const double Tp = T + (kTwo52 + kFinishBias);
             // transpose (warp-local): element c = hb*E + j lives at xs[hb*EP + j]
 #pragma unroll
             for (int j = 0; j < E; j += 2) *reinterpret_cast<double2*>(xs_w + j) = make_double2(x[j], x[j + 1]);
@@ -734,8 +737,10 @@ __global__ void __launch_bounds__(32 * pm_warps<LOGN>(), 1) k_hash_f64_pm(const 
                 // D = bits & (2^52 - 1) = dh * 2^32 + lo (even), O = D / 2 = dh * 2^31 + lo / 2
                 // == dh + lo / 2 (mod P)
                 // O' = dh + lo/2 < 2P: one conditional subtraction, as an unsigned min
-                const uint32_t lo = uint32_t(__double2loint(v)), dh = uint32_t(__double2hiint(v)) & 0xFFFFFu;
-                const uint32_t o = (lo >> 1) + dh;
+                // the high word is 0x43300000 + dh (dh < 2^20) and kFinishBias has already moved O by
+                // -0x43300000 (mod P): no mask; lo/2 + dh + 0x43300000 < 2^31 + 2^20 + 0x43300000 < 2P
+                const uint32_t lo = uint32_t(__double2loint(v)), hi = uint32_t(__double2hiint(v));
+                const uint32_t o = (lo >> 1) + hi;
                 return min(o, o - kP31);
             };
             if (my_point < p.n) {
@@ -813,6 +818,9 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
     constexpr int NP = N / 2; // column pairs per part
     static_assert(G > 1 && EG >= 1 && E % 2 == 0, "layout");
     constexpr double kTwo52 = 4503599627370496.0;
+    // added to every final-stage value D (even): moves O = D/2 by P - 0x43300000 (mod P), which
+    // cancels the exponent bits 0x43300000 that the high word of 2^52 + D carries (see finish)
+    constexpr double kFinishBias = 2.0 * double(kP31 - 0x43300000u);
 
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int S = LOGN + 3; // outcome bit of the table byte offset
@@ -925,7 +933,7 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
             double T = x[0];
 #pragma unroll
             for (int o = 1; o < G; o <<= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
-            const double Tp = T + kTwo52;
+            const double Tp = T + (kTwo52 + kFinishBias);
             // transpose, G columns per round: x[k*G + h] <- element h*E + k*G + g
 #pragma unroll
             for (int k = 0; k < EG; ++k) {
@@ -960,8 +968,10 @@ __global__ void __launch_bounds__(32 * pt_warps<LOGN>(), 1) k_hash_f64_pt(const 
                 }
             }
             auto finish = [](double v) -> uint32_t {
-                const uint32_t lo = uint32_t(__double2loint(v)), dh = uint32_t(__double2hiint(v)) & 0xFFFFFu;
-                const uint32_t o = (lo >> 1) + dh;
+                // the high word is 0x43300000 + dh (dh < 2^20) and kFinishBias has already moved O by
+                // -0x43300000 (mod P): no mask; lo/2 + dh + 0x43300000 < 2^31 + 2^20 + 0x43300000 < 2P
+                const uint32_t lo = uint32_t(__double2loint(v)), hi = uint32_t(__double2hiint(v));
+                const uint32_t o = (lo >> 1) + hi;
                 return min(o, o - kP31);
             };
             // element (k, h) is code v = h*E + k*G + g: G consecutive keys per store
