@@ -133,3 +133,46 @@ def test_partition_parts_fold_the_permutation(oracle):
         fam = ix.family(p)
         m, s, rr, k = oi.family(p)
         assert (fam.mapping == m).all() and (fam.seeds == s).all() and fam.radius == rr == 6
+
+
+_VARIANT_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_1602_02620_b200 import fclsh as F
+from tests.helpers import random_rows
+orc = O.best()
+rng = np.random.default_rng(5)
+for radius, d in [(2, 7), (5, 64), (6, 100), (8, 512), (9, 1000), (10, 1024), (10, 2048)]:
+    m, s, k = orc.build_family(d, radius, 77 + radius, prime=F.M31)
+    f = F.build_covering_family(d, radius, 77 + radius, prime=F.M31)
+    rows = random_rows(rng, 333, d)
+    rows[0] = 0
+    rows[1] = ~np.uint64(0)
+    if d % 64:
+        rows[1, -1] &= np.uint64((1 << (d % 64)) - 1)
+    want = orc.hash_batch(m, s, d, radius, F.M31, rows, kind=k, threads=4)
+    for kb in (4, 8):
+        got = F.hash_batch(f, rows, key_bytes=kb)
+        assert (got.astype(np.uint64) == want).all(), (radius, d, kb)
+print("variant ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"FCLSH_HASH_F64_PM": "1"}, {"FCLSH_HASH_INT": "1"}, {"FCLSH_HASH_PK32": "1"}],
+                         ids=["default", "f64_pm", "int_planes", "pk32"])
+def test_hash_kernel_variants(env):
+    """The 2^31-1 kernels the launcher falls back to (family table too large
+    for the 12-warp layout, A/B knobs) hold the same keys as the default one:
+    each variant in its own process (the knobs are read once), 4- and 8-byte
+    keys, against hash_batch_into (covering.cpp:169-182)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
