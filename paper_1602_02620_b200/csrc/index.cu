@@ -1060,7 +1060,11 @@ __device__ __forceinline__ uint64_t fam_ld(const uint64_t* p) {
 
 // One part's keys in registers: key[i] = h[v] for v = lane + 32 i (v = 0 is
 // no table), from the row held as word `lane` on lane `lane` (rw).
-template <int FE, bool SMEM, typename K>
+// R32 (rows of <= 16 words, d <= 1024): the row is also held as 32-bit half `lane` on lane
+// `lane`, so an entry's row bit costs one 32-bit shuffle instead of a 64-bit one (two SHFLs):
+// cfg3's probe kernel 90.0 -> 87.0 us (profiles/r02/ab_fused_row32.txt). A compile-time choice:
+// the kernel sits at its register cap and a run-time branch here spills.
+template <int FE, bool SMEM, bool R32 = false, typename K>
 __device__ __forceinline__ void hash_part(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
                                           uint32_t p, uint32_t words, uint64_t rw, int lane, K (&key)[FE]) {
     constexpr unsigned kAll = 0xffffffffu;
@@ -1083,6 +1087,8 @@ __device__ __forceinline__ void hash_part(const FusedHash& fh, const uint32_t* c
         t[i] = 0;
     }
     const uint32_t m = __reduce_max_sync(kAll, mx); // warp-uniform trip count (the shuffles need every lane)
+    uint32_t rh = 0;
+    if constexpr (R32) rh = uint32_t(__shfl_sync(kAll, rw, lane >> 1) >> ((lane & 1) * 32));
     for (uint32_t k0 = 0; k0 < m; k0 += kBatch) {
         uint64_t e[FE][kBatch];
 #pragma unroll
@@ -1095,8 +1101,14 @@ __device__ __forceinline__ void hash_part(const FusedHash& fh, const uint32_t* c
             for (int k = 0; k < kBatch; ++k) {
                 const uint32_t pos = uint32_t(e[i][k]);
                 FCLSH_DCHECK((pos >> 6) < words && b0[i] + cnt[i] <= fh.max_dims);
-                const uint64_t w = __shfl_sync(kAll, rw, int(pos >> 6));
-                if ((w >> (pos & 63)) & 1) t[i] += (long long)(e[i][k] >> 32);
+                uint32_t w; // the 32-bit half of the row that holds bit `pos`
+                if constexpr (R32) {
+                    w = __shfl_sync(kAll, rh, int(pos >> 5));
+                } else {
+                    const uint64_t w64 = __shfl_sync(kAll, rw, int(pos >> 6));
+                    w = uint32_t(w64 >> (pos & 32u));
+                }
+                if ((w >> (pos & 31)) & 1) t[i] += (long long)(e[i][k] >> 32);
             }
     }
 #pragma unroll
@@ -1216,7 +1228,7 @@ __device__ __forceinline__ uint64_t fused_row(const FusedHash& fh, uint64_t q, u
     return rw;
 }
 
-template <int FE, bool SMEM, bool SK, typename K>
+template <int FE, bool SMEM, bool SK, bool R32 = false, typename K>
 __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* cp_all, const uint64_t* pk_all,
                                            uint64_t q, uint32_t words, const uint64_t* qrows, K* keys, int lane,
                                            uint64_t& rw, uint64_t* row_s, uint32_t* acc) {
@@ -1230,7 +1242,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* 
         if constexpr (SK)
             hash_part_sk<FE>(fh, pk_all, p, reinterpret_cast<const uint32_t*>(row_s), acc, lane, key);
         else
-            hash_part<FE, SMEM>(fh, cp_all, pk_all, p, words, rw, lane, key);
+            hash_part<FE, SMEM, R32>(fh, cp_all, pk_all, p, words, rw, lane, key);
         K* kp = keys + uint64_t(p) * fh.L;
 #pragma unroll
         for (int i = 0; i < FE; ++i) {
@@ -1247,7 +1259,7 @@ __device__ __forceinline__ void fused_hash(const FusedHash& fh, const uint32_t* 
 // the keys are also stored for the hand-over kernels.
 // SK (with FSM): the position-parallel sketch (hash_part_sk); the family's
 // entries and every warp's row + column accumulators in shared memory.
-template <typename T, int U, int MINB, int FE, bool FSM = false, bool PM = false, bool SK = false>
+template <typename T, int U, int MINB, int FE, bool FSM = false, bool PM = false, bool SK = false, bool R32 = false>
 __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
     typename T::K* qkeys, uint64_t nq, uint32_t tables, const Tables<T> tb,
     const uint64_t* __restrict__ rows, const uint64_t* __restrict__ qrows, uint32_t words, uint32_t radius,
@@ -1330,7 +1342,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         FCLSH_TRACE_STAMP(q, 5, smid);
 #endif
         if constexpr (FE > 0 && !PM) {
-            fused_hash<FE, FSM, SK>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw, row_s, acc_s);
+            fused_hash<FE, FSM, SK, R32>(fh, cp_all, pk_all, q, words, qrows, qkeys + q * tables, lane, rw, row_s, acc_s);
             __syncwarp(); // the keys (written across lanes) are visible to the loads below
         }
 #ifdef FCLSH_TRACE
@@ -2662,7 +2674,9 @@ void launch_fused(DeviceIndex& ix, typename T::K* qkeys, const uint64_t* d_q, ui
             fsm ? go(k_query_warp_pf<T, 3, 4, 4, true>, true) : go(k_query_warp_pf<T, 3, 4, 4>);
         else if (fe == 4) // (cfg3: U = 2 at 5 CTAs/SM measured ~4 % ahead of U = 3 at 4)
             pm ? go(k_query_warp_pf<T, 2, 5, 4, true, true>, true)
-               : fsm ? go(k_query_warp_pf<T, 2, FCLSH_FE4_MINB, 4, true>, true) : go(k_query_warp_pf<T, 2, 5, 4>);
+               : !fsm ? go(k_query_warp_pf<T, 2, 5, 4>)
+                 : ix.row_words <= 16 ? go(k_query_warp_pf<T, 2, FCLSH_FE4_MINB, 4, true, false, false, true>, true)
+                                      : go(k_query_warp_pf<T, 2, FCLSH_FE4_MINB, 4, true>, true);
         else if (fe == 8)
             pm ? go(k_query_warp_pf<T, 2, 4, 8, true, true>, true)
                : fsm ? go(k_query_warp_pf<T, 2, 4, 8, true>, true) : go(k_query_warp_pf<T, 2, 4, 8>);
