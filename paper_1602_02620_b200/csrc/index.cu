@@ -61,6 +61,9 @@ struct NarrowEntry { // key < 2^32: one u64, (key << 32 | id) orders as (key, id
     __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return (E(k) << 32) | i; }
     __device__ __forceinline__ static bool less(E a, E b) { return a < b; }
     __device__ __forceinline__ static bool empty(E e) { return e == ~0ull; }
+    // a posting of key k (k < prime <= 2^32 - 1, so an empty slot's key field 0xFFFFFFFF never
+    // equals one): one 32-bit compare instead of the 64-bit empty test and key compare
+    __device__ __forceinline__ static bool match(E e, uint64_t k) { return uint32_t(e >> 32) == uint32_t(k); }
     __host__ __device__ static constexpr unsigned char empty_byte() { return 0xFF; }
     // claim slot p for e; true if this thread placed it
     __device__ __forceinline__ static bool claim(E* p, E e) { return atomicCAS(p, ~0ull, e) == ~0ull; }
@@ -75,6 +78,7 @@ struct WideEntry { // 8-byte keys: {key, id}
     __device__ __forceinline__ static E make(uint64_t k, uint32_t i) { return make_ulonglong2(k, i); }
     __device__ __forceinline__ static bool less(E a, E b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
     __device__ __forceinline__ static bool empty(E e) { return e.x == ~0ull; }
+    __device__ __forceinline__ static bool match(E e, uint64_t k) { return e.x == k; } // k < prime < 2^63
     __host__ __device__ static constexpr unsigned char empty_byte() { return 0xFF; }
     __device__ __forceinline__ static bool claim(E* p, E e) {
         if (atomicCAS(&p->x, ~0ull, e.x) != ~0ull) return false;
@@ -1385,7 +1389,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
         auto offer_bucket = [&](const E (&bk)[kSlots], bool live, uint64_t kk) {
             uint32_t mm = 0;
 #pragma unroll
-            for (int i = 0; i < kSlots; ++i) mm |= uint32_t(live && !T::empty(bk[i]) && T::key(bk[i]) == kk) << i;
+            for (int i = 0; i < kSlots; ++i) mm |= uint32_t(T::match(bk[i], kk)) << i;
+            mm = live ? mm : 0u;
             coll += __popc(mm);
             while (__any_sync(kAll, mm != 0)) {
                 const int i = __ffs(mm) - 1;
