@@ -1550,7 +1550,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             dist = row_distance(rows + uint64_t(list) * words, qrows + q * words, words, vec_rows);
         }
         const bool pass = !over && uint32_t(lane) < nd && dist <= radius;
-        const uint32_t nfound = __popc(__ballot_sync(kAll, pass));
+        const uint32_t pass_mask = __ballot_sync(kAll, pass);
+        const uint32_t nfound = __popc(pass_mask);
         if (over || nfound > slot_cap) {
             if (lane == 0) {
                 const unsigned int at = atomicAdd(overflow_count, 1u);
@@ -1561,17 +1562,22 @@ __global__ void __launch_bounds__(256, MINB) k_query_warp_pf(
             }
             continue;
         }
-        // ascending ids: bitonic sort across the warp (non-passes = +inf)
+        // ascending ids: bitonic sort across the warp (non-passes = +inf); one
+        // result (the usual query: its planted near point) just moves to lane 0
         unsigned long long mine = pass ? (static_cast<unsigned long long>(list) << 32) | dist : ~0ull;
+        if (nfound == 1) {
+            mine = __shfl_sync(kAll, mine, __ffs(pass_mask) - 1);
+        } else if (nfound > 1) {
 #pragma unroll
-        for (int k = 2; k <= 32; k <<= 1) {
+            for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const unsigned long long other = __shfl_xor_sync(kAll, mine, j);
-                const bool up = (lane & k) == 0;
-                const bool lower = (lane & j) == 0;
-                const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
-                mine = (lower == up) ? lo : hi;
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const unsigned long long other = __shfl_xor_sync(kAll, mine, j);
+                    const bool up = (lane & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const unsigned long long lo = mine < other ? mine : other, hi = mine < other ? other : mine;
+                    mine = (lower == up) ? lo : hi;
+                }
             }
         }
         if (uint32_t(lane) < nfound) {
