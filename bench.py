@@ -330,7 +330,8 @@ def run_config(ctx, cfg, scaling, spr, args, flush, stream, clocks, hbm, peak_sr
     def step():
         return cl.query_device(q_dev, cfg.radius, stream, nq=nq)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, args.warmup)):  # warm-up steps run like the timed ones: L2 flushed first
+        flush()                           # (the first step after a first flush measured ~190 us, tools/step_variance.py)
         step()
     sync_all(ctx.devices)
     F.launch_count_reset()
@@ -632,6 +633,7 @@ def bench_hash(ctx, args, hbm, peak_src, flush, stream, threads, clocks):
             F.hash_batch_device(fam, d_rows[c0:c0 + m], keys, layout=1, key_stride=L, stream=stream)
 
     for _ in range(max(3, args.warmup)):
+        flush()
         step()
     torch.cuda.synchronize(dev)
     ctx.barrier()
